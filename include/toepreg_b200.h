@@ -1,0 +1,129 @@
+/*
+ * toepreg_b200.h - C ABI of the B200 superfast Tikhonov-Toeplitz solver.
+ *
+ * The reference package (toepreg 0.1.0, /root/reference/pkg) is pure Python;
+ * its boundary for this path is the Python call
+ *     solve_tikhonov(problem, config=None) -> SolveReport
+ * (ref: pkg/src/toepreg/solver.py:58-78, re-exported at __init__.py:5-14),
+ * with the inner operator rec_tan_int(system, ...) (ref: tanint.py:457-467).
+ * The entry points below are what that boundary binds to through ctypes
+ * (see INTEGRATION.md); the Python shim paper_1302_6945_b200.solve_tikhonov
+ * mirrors the reference signature on top of them.
+ *
+ * Conventions
+ *  - complex values are interleaved (re, im) float64, all pointers passed to
+ *    tr_solve_batch are DEVICE pointers owned by the caller;
+ *  - Toeplitz generators follow the reference layout: length rows+cols-1,
+ *    top-right -> bottom-left, entry (i,j) = gen[i - j + cols - 1]
+ *    (ref: toeplitz.py:1-7);
+ *  - a batch stride of 0 means "shared by every system of the batch"
+ *    (e.g. config 2: one T, 64 right-hand sides);
+ *  - the library keeps no pointer after return; concurrent calls are safe
+ *    on distinct streams and workspaces.
+ *
+ * Return codes: 0 ok; 2 invalid arguments (-> ValueError); 3 at least one
+ * system singular (-> SingularSystemError, per-system status in tr_diag);
+ * 4 CUDA error (-> RuntimeError); 5 capacity exceeded (too many deferred
+ * conditions for the workspace).
+ */
+#ifndef TOEPREG_B200_H
+#define TOEPREG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { TR_GENERAL = 0, TR_L2 = 1, TR_GRAMIAN = 2 };
+enum { TR_FILL_AUTO = 0, TR_FILL_ZERO = 1, TR_FILL_ECHO = 2 };
+
+/* Problem shape + SolverConfig (ref: solver.py:39-45, toeplitz.py:167-233). */
+typedef struct tr_desc {
+  int32_t variant;          /* TR_GENERAL / TR_L2 / TR_GRAMIAN */
+  int64_t m;                /* rows of T (gramian: = n) */
+  int64_t n;                /* unknowns */
+  int64_t p_rows;           /* rows of L (general/gramian; l2: = n) */
+  int32_t n_lim;            /* SolverConfig.n_lim (256) */
+  double pivot_threshold;   /* SolverConfig.pivot_threshold (1e-8) */
+  int32_t fill;             /* SolverConfig.fill */
+  int32_t paired;           /* SolverConfig.paired */
+  int32_t force_even;       /* SolverConfig.force_even */
+  int32_t refine;           /* extra iterative-refinement solves (0 = reference) */
+} tr_desc;
+
+/* Per-system report (ref: SolveReport solver.py:48-55, TanIntDiagnostics
+ * tanint.py:72-85). */
+typedef struct tr_diag {
+  int32_t status;               /* 0 ok, 3 singular, 5 capacity */
+  int32_t difficult_points;
+  int64_t conditions_total;
+  int32_t recursion_depth;
+  int32_t retried_leaves;
+  double max_column_scale;
+  int64_t final_col_degrees[8];
+  double relative_residual;
+  int32_t trim_overflow;        /* products truncated at the degree bound */
+  int32_t pad;
+} tr_diag;
+
+/* Bytes of device workspace tr_solve_batch needs for `batch` systems. */
+size_t tr_workspace_bytes(const tr_desc* d, int64_t batch);
+
+/* Circulant order N = n_tilde + k of the extended system (ref
+ * extension.py:42-68, :190-193) and the tree shape, for diagnostics. */
+int tr_plan_info(const tr_desc* d, int64_t* order, int64_t* leaves, int32_t* depth,
+                 int64_t* max_leaf_conditions);
+
+/* Solve `batch` independent systems.  Device inputs:
+ *   T_gen  [batch][m+n-1]     (general, l2)          stride T_bs
+ *   L_gen  [batch][p_rows+n-1](general, gramian)     stride L_bs
+ *   G_col  [batch][n]         (gramian: first column of T^H T)  stride G_bs
+ *   beta_sq[batch]            (l2: |beta|^2, real)   stride beta_bs
+ *   rhs    [batch][m] = b, or [batch][n] = normal rhs y = T^H b when
+ *          rhs_is_normal (always for gramian)        stride rhs_bs
+ * Outputs: x_out [batch][n] (device), diag_host [batch] (host, may be NULL).
+ * The call is stream-ordered; when diag_host is non-NULL it synchronises the
+ * stream to fill it. */
+int tr_solve_batch(const tr_desc* d, int64_t batch,
+                   const double* T_gen, int64_t T_bs,
+                   const double* L_gen, int64_t L_bs,
+                   const double* G_col, int64_t G_bs,
+                   const double* beta_sq, int64_t beta_bs,
+                   const double* rhs, int64_t rhs_bs, int32_t rhs_is_normal,
+                   double* x_out, tr_diag* diag_host,
+                   void* workspace, size_t ws_bytes, void* stream);
+
+/* Host-buffer convenience entry (what a non-CUDA caller binds): copies the
+ * inputs in, solves, copies x out.  Same argument meaning, HOST pointers. */
+int tr_solve_batch_host(const tr_desc* d, int64_t batch,
+                        const double* T_gen, int64_t T_bs,
+                        const double* L_gen, int64_t L_bs,
+                        const double* G_col, int64_t G_bs,
+                        const double* beta_sq, int64_t beta_bs,
+                        const double* rhs, int64_t rhs_bs, int32_t rhs_is_normal,
+                        double* x_out, tr_diag* diag_host);
+
+/* Stage entry points mirroring reference helpers, for stage-level parity:
+ *  tr_grid_eval   ~ fftpoly.grid_eval(coeffs, N, offset, stride) (:64-89)
+ *  tr_fft         ~ batched unnormalised DFT, sign +1/-1
+ *  tr_matpoly_mul ~ fftpoly.matpoly_multiply(a, b) (:233-249), untrimmed
+ *  tr_assemble    ~ extension.assemble(problem).weights (:267-273)
+ * All pointers are device pointers; all are stream-ordered on `stream`. */
+int tr_fft(const double* in, double* out, int64_t n, int64_t lines, int32_t sign, void* stream);
+int tr_grid_eval(const double* coeffs, int64_t lines, int64_t length, int64_t n_nodes,
+                 int64_t offset, int64_t stride, double* out, void* stream);
+int tr_matpoly_mul(const double* a, int64_t la, const double* b, int64_t lb, int32_t p,
+                   double* out, void* stream);
+int tr_assemble(const tr_desc* d, const double* T_gen, const double* L_gen, const double* G_col,
+                const double* beta_sq, const double* rhs, int32_t rhs_is_normal,
+                double* weights_out, void* stream);
+
+/* Last error message of the calling thread. */
+const char* tr_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOEPREG_B200_H */

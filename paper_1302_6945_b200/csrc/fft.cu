@@ -1,0 +1,415 @@
+// Batched complex128 multi-pass Stockham FFT (see fft.cuh).
+#include "fft.cuh"
+
+#include <math.h>
+#include <map>
+#include <mutex>
+#include <vector>
+
+namespace {
+
+constexpr int FFT_THREADS = 256;
+constexpr int FFT_TILE = 4096;                 // complex values per CTA tile
+constexpr int FFT_MAXE = FFT_TILE / FFT_THREADS;  // values per thread
+
+struct PassArgs {
+  long long n;
+  int R, Ns, T, LB, LS, nst, sign;
+  int rad[16];
+  const cplx* twN;
+  const cplx* twR;
+  const cplx* in;
+  long long in_ls, in_len;
+  cplx* out;
+  long long out_ls;
+  long long lines;
+  long long tiles;  // n / R / T
+};
+
+TR_D cplx tw_lookup(const cplx* tab, long long idx, int sign) {
+  cplx w = __ldg(&tab[idx]);
+  return sign < 0 ? cconj(w) : w;
+}
+
+template <int RS>
+TR_D void dft_small(cplx* a, int sign) {
+  if (RS == 2) {
+    cplx t = a[0];
+    a[0] = cadd(t, a[1]);
+    a[1] = csub(t, a[1]);
+  } else if (RS == 4) {
+    cplx t0 = cadd(a[0], a[2]), t1 = csub(a[0], a[2]);
+    cplx t2 = cadd(a[1], a[3]), d = csub(a[1], a[3]);
+    cplx t3 = sign > 0 ? cmk(-d.y, d.x) : cmk(d.y, -d.x);  // d * (i*sign)
+    a[0] = cadd(t0, t2);
+    a[2] = csub(t0, t2);
+    a[1] = cadd(t1, t3);
+    a[3] = csub(t1, t3);
+  } else if (RS == 8) {
+    cplx e[4] = {a[0], a[2], a[4], a[6]};
+    cplx o[4] = {a[1], a[3], a[5], a[7]};
+    dft_small<4>(e, sign);
+    dft_small<4>(o, sign);
+    const double c = 0.70710678118654752440;
+    double s = (double)sign;
+    // o[v] *= w8^(sign v)
+    cplx o1 = cmk(c * (o[1].x - s * o[1].y), c * (o[1].y + s * o[1].x));
+    cplx o2 = cmk(-s * o[2].y, s * o[2].x);
+    cplx o3 = cmk(-c * (o[3].x + s * o[3].y), c * (s * o[3].x - o[3].y));
+    a[0] = cadd(e[0], o[0]);
+    a[4] = csub(e[0], o[0]);
+    a[1] = cadd(e[1], o1);
+    a[5] = csub(e[1], o1);
+    a[2] = cadd(e[2], o2);
+    a[6] = csub(e[2], o2);
+    a[3] = cadd(e[3], o3);
+    a[7] = csub(e[3], o3);
+  }
+}
+
+// One Stockham stage of radix RS over all smem lines (power-of-two radix).
+template <int RS>
+TR_D void smem_stage_pow2(cplx* s, const PassArgs& a, int NsS, int nlines_tile) {
+  const int R = a.R;
+  const int per_line = R / RS;
+  const int total = per_line * nlines_tile;
+  const int mtot = NsS * RS;  // sub-transform length after this stage
+  const int twstep = R / mtot;
+  cplx v[FFT_MAXE];
+#pragma unroll
+  for (int it = 0; it < FFT_MAXE / RS; ++it) {
+    int bidx = threadIdx.x + it * FFT_THREADS;
+    if (bidx < total) {
+      int line = bidx / per_line, b = bidx - line * per_line;
+      int k = b % NsS;
+      cplx* base = s + line * a.LS;
+#pragma unroll
+      for (int u = 0; u < RS; ++u) {
+        cplx x = base[b + u * per_line];
+        if (NsS > 1 && u > 0) x = cmul(x, tw_lookup(a.twR, (long long)u * k * twstep, a.sign));
+        v[it * RS + u] = x;
+      }
+      dft_small<RS>(&v[it * RS], a.sign);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < FFT_MAXE / RS; ++it) {
+    int bidx = threadIdx.x + it * FFT_THREADS;
+    if (bidx < total) {
+      int line = bidx / per_line, b = bidx - line * per_line;
+      int k = b % NsS;
+      cplx* base = s + line * a.LS;
+      int o = (b / NsS) * mtot + k;
+#pragma unroll
+      for (int u = 0; u < RS; ++u) base[o + u * NsS] = v[it * RS + u];
+    }
+  }
+  __syncthreads();
+}
+
+// Direct DFT stage of odd radix q (first stage, so NsS == 1: no twiddles).
+TR_D void smem_stage_odd(cplx* s, const PassArgs& a, int q, int nlines_tile) {
+  const int R = a.R;
+  const int per_line = R / q;
+  const int total = R * nlines_tile;  // outputs
+  const int wstep = R / q;
+  cplx v[FFT_MAXE];
+#pragma unroll
+  for (int it = 0; it < FFT_MAXE; ++it) {
+    int oi = threadIdx.x + it * FFT_THREADS;
+    if (oi < total) {
+      int line = oi / R, r = oi - line * R;
+      int b = r / q, vv = r - b * q;
+      const cplx* base = s + line * a.LS;
+      cplx acc = cmk(0.0, 0.0);
+      for (int u = 0; u < q; ++u) {
+        int e = (u * vv) % q;
+        acc = cfma(base[b + u * per_line], tw_lookup(a.twR, (long long)e * wstep, a.sign), acc);
+      }
+      v[it] = acc;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < FFT_MAXE; ++it) {
+    int oi = threadIdx.x + it * FFT_THREADS;
+    if (oi < total) {
+      int line = oi / R, r = oi - line * R;
+      int b = r / q, vv = r - b * q;
+      // NsS == 1: output position b*q + vv == r
+      s[line * a.LS + b * q + vv] = v[it];
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(FFT_THREADS) fft_pass_kernel(PassArgs a) {
+  extern __shared__ cplx smem[];
+  const int R = a.R, T = a.T, LB = a.LB;
+  const long long tile = blockIdx.x;
+  const long long line0 = (long long)blockIdx.y * LB;
+  const long long j0 = tile * T;
+  const long long stride_in = a.n / R;  // distance between butterfly inputs
+  const int nel = LB * T * R;
+  const int nlines_tile = LB * T;
+
+  // ---- load (t fastest, then r, then line) with the inter-pass twiddle ----
+  for (int idx = threadIdx.x; idx < nel; idx += FFT_THREADS) {
+    int t = idx % T;
+    int r = (idx / T) % R;
+    int lb = idx / (T * R);
+    long long line = line0 + lb;
+    cplx x = cmk(0.0, 0.0);
+    if (line < a.lines) {
+      long long j = j0 + t;
+      long long e = j + (long long)r * stride_in;
+      if (e < a.in_len) x = a.in[line * a.in_ls + e];
+      if (a.Ns > 1 && r > 0) {
+        long long k = j % a.Ns;
+        long long m = ((long long)r * k) * (a.n / ((long long)a.Ns * R));
+        x = cmul(x, tw_lookup(a.twN, m % a.n, a.sign));
+      }
+    }
+    smem[(lb * T + t) * a.LS + r] = x;
+  }
+  __syncthreads();
+
+  // ---- length-R sub-transform of every staged line ----
+  int NsS = 1;
+  for (int st = 0; st < a.nst; ++st) {
+    int rs = a.rad[st];
+    if (rs == 8) smem_stage_pow2<8>(smem, a, NsS, nlines_tile);
+    else if (rs == 4) smem_stage_pow2<4>(smem, a, NsS, nlines_tile);
+    else if (rs == 2) smem_stage_pow2<2>(smem, a, NsS, nlines_tile);
+    else smem_stage_odd(smem, a, rs, nlines_tile);
+    NsS *= rs;
+  }
+
+  // ---- store: y[(j/Ns)*Ns*R + q*Ns + (j%Ns)] ----
+  for (int idx = threadIdx.x; idx < nel; idx += FFT_THREADS) {
+    int t, q, lb;
+    if (a.Ns == 1) {  // each j owns a contiguous run of R outputs
+      q = idx % R;
+      t = (idx / R) % T;
+      lb = idx / (T * R);
+    } else {
+      t = idx % T;
+      q = (idx / T) % R;
+      lb = idx / (T * R);
+    }
+    long long line = line0 + lb;
+    if (line >= a.lines) continue;
+    long long j = j0 + t;
+    long long k = j % a.Ns;
+    long long o = (j / a.Ns) * (long long)a.Ns * R + (long long)q * a.Ns + k;
+    a.out[line * a.out_ls + o] = smem[(lb * T + t) * a.LS + q];
+  }
+}
+
+struct TwKey {
+  int dev;
+  long long n;
+  bool operator<(const TwKey& o) const { return dev != o.dev ? dev < o.dev : n < o.n; }
+};
+std::mutex g_mu;
+std::map<TwKey, cplx*> g_tw;
+
+void split_pow2(int R, int* rad, int* nst) {
+  // odd part first, then 8s, then a 4 or 2 remainder
+  int q = R;
+  while ((q & 1) == 0) q >>= 1;
+  int p2 = R / q;
+  int k = 0;
+  if (q > 1) rad[k++] = q;
+  while (p2 >= 8) { rad[k++] = 8; p2 /= 8; }
+  if (p2 == 4) rad[k++] = 4;
+  else if (p2 == 2) rad[k++] = 2;
+  *nst = k;
+}
+
+long long odd_part(long long n) {
+  while (n > 0 && (n & 1) == 0) n >>= 1;
+  return n;
+}
+
+}  // namespace
+
+const cplx* twiddle_table(long long n) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_mu);
+  TwKey key{dev, n};
+  auto it = g_tw.find(key);
+  if (it != g_tw.end()) return it->second;
+  std::vector<cplx> h((size_t)n);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (long long k = 0; k < n; ++k) {
+    // exact symmetric reduction keeps the table symmetric to the last bit
+    long long r = k;
+    long double ang = two_pi * (long double)r / (long double)n;
+    h[(size_t)k] = cmk((double)cosl(ang), (double)sinl(ang));
+  }
+  // exact values at the quarter points
+  if (n % 4 == 0) {
+    h[(size_t)(n / 4)] = cmk(0.0, 1.0);
+    h[(size_t)(3 * n / 4)] = cmk(0.0, -1.0);
+  }
+  if (n % 2 == 0) h[(size_t)(n / 2)] = cmk(-1.0, 0.0);
+  cplx* d = nullptr;
+  if (cudaMalloc(&d, sizeof(cplx) * (size_t)n) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, h.data(), sizeof(cplx) * (size_t)n, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  g_tw[key] = d;
+  return d;
+}
+
+bool fft_supported(long long n) {
+  if (n < 1) return false;
+  return odd_part(n) <= FFT_MAX_ODD;
+}
+
+long long fft_good_len(long long n) {
+  if (n <= 1) return 1;
+  // candidates 2^a * q, q in a small odd set; cost ~ len * (log2 len + q/4)
+  static const int qs[] = {1, 3, 5, 7, 9, 15};
+  long long best = -1;
+  double best_cost = 1e300;
+  for (int q : qs) {
+    long long len = q;
+    while (len < n) len *= 2;
+    double cost = (double)len * (log2((double)len) + 0.25 * q);
+    if (cost < best_cost) { best_cost = cost; best = len; }
+  }
+  return best;
+}
+
+int fft_plan(long long n, FftPlan* out) {
+  if (!fft_supported(n)) {
+    tr_set_error("fft length %lld has an odd factor above %d", n, FFT_MAX_ODD);
+    return 2;
+  }
+  FftPlan p;
+  p.n = n;
+  p.twN = twiddle_table(n);
+  if (!p.twN) { tr_set_error("twiddle table allocation failed (n=%lld)", n); return 4; }
+  long long q = odd_part(n);
+  long long p2 = n / q;
+  std::vector<long long> radices;
+  if (n <= FFT_TILE) {
+    radices.push_back(n);
+  } else {
+    // passes of radix <= 1024 (so T >= 4); the odd factor rides in the first
+    int a = 0;
+    while ((p2 >> a) > 1) ++a;           // p2 = 2^a
+    int npass = (n <= 1024LL * 1024LL) ? 2 : 3;
+    // later passes take powers of two, balanced, each <= 2^10
+    int lg = 0;
+    while ((1LL << lg) < n) ++lg;
+    int b_each = (lg + npass - 1) / npass;
+    if (b_each > 10) b_each = 10;
+    std::vector<long long> tail;
+    int used = 0;
+    for (int i = 1; i < npass; ++i) {
+      int b = b_each;
+      if (used + b > a) b = a - used;
+      tail.push_back(1LL << b);
+      used += b;
+    }
+    long long first = q << (a - used);
+    // rebalance if the first pass is too large
+    for (size_t i = 0; first > 1024 && i < tail.size(); ++i) {
+      while (first > 1024 && tail[i] < 1024 && (first % 2 == 0)) { tail[i] *= 2; first /= 2; }
+    }
+    if (first > 1024) { tr_set_error("fft length %lld cannot be split", n); return 2; }
+    radices.push_back(first);
+    for (long long t : tail) radices.push_back(t);
+  }
+  (void)p2;
+  if (radices.size() > 3) { tr_set_error("fft length %lld needs too many passes", n); return 2; }
+  p.npass = (int)radices.size();
+  long long Ns = 1;
+  for (int i = 0; i < p.npass; ++i) {
+    FftPass& ps = p.pass[i];
+    ps.R = (int)radices[i];
+    ps.Ns = (int)Ns;
+    if (p.npass == 1) {
+      ps.T = 1;
+      ps.LB = (int)(FFT_TILE / ps.R);
+      if (ps.LB > 64) ps.LB = 64;
+      if (ps.LB < 1) ps.LB = 1;
+    } else {
+      ps.LB = 1;
+      long long T = FFT_TILE / ps.R;
+      long long nj = n / ps.R;
+      if (T > nj) T = nj;
+      // T must divide n/R
+      while (nj % T) T >>= 1;
+      ps.T = (int)T;
+    }
+    split_pow2(ps.R, ps.rad, &ps.nst);
+    ps.twR = twiddle_table(ps.R);
+    if (!ps.twR) { tr_set_error("twiddle table allocation failed (R=%d)", ps.R); return 4; }
+    Ns *= ps.R;
+  }
+  *out = p;
+  return 0;
+}
+
+static int launch_pass(const FftPlan& p, int i, const cplx* in, long long in_ls, long long in_len,
+                       cplx* out, long long out_ls, long long lines, int sign, cudaStream_t st) {
+  const FftPass& ps = p.pass[i];
+  PassArgs a;
+  a.n = p.n;
+  a.R = ps.R;
+  a.Ns = ps.Ns;
+  a.T = ps.T;
+  a.LB = ps.LB;
+  int nl = ps.LB * ps.T;
+  a.LS = ps.R + (nl > 1 ? 1 : 0);
+  a.nst = ps.nst;
+  for (int k = 0; k < 16; ++k) a.rad[k] = ps.rad[k];
+  a.sign = sign;
+  a.twN = p.twN;
+  a.twR = ps.twR;
+  a.in = in;
+  a.in_ls = in_ls;
+  a.in_len = in_len;
+  a.out = out;
+  a.out_ls = out_ls;
+  a.lines = lines;
+  a.tiles = p.n / ps.R / ps.T;
+  size_t smem = sizeof(cplx) * (size_t)nl * a.LS;
+  dim3 grid((unsigned)a.tiles, (unsigned)((lines + ps.LB - 1) / ps.LB));
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(fft_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+    attr_set = true;
+  }
+  fft_pass_kernel<<<grid, FFT_THREADS, smem, st>>>(a);
+  return 0;
+}
+
+int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len, cplx* out,
+             long long out_ls, cplx* scratch, long long lines, int sign, cudaStream_t st) {
+  if (lines <= 0) return 0;
+  if (in_len > p.n) in_len = p.n;
+  const long long n = p.n;
+  if (p.npass == 1) {
+    launch_pass(p, 0, in, in_ls, in_len, out, out_ls, lines, sign, st);
+  } else if (p.npass == 2) {
+    launch_pass(p, 0, in, in_ls, in_len, scratch, n, lines, sign, st);
+    launch_pass(p, 1, scratch, n, n, out, out_ls, lines, sign, st);
+  } else {
+    // in -> scratch -> out -> scratch, then copy back into out
+    launch_pass(p, 0, in, in_ls, in_len, scratch, n, lines, sign, st);
+    launch_pass(p, 1, scratch, n, n, out, out_ls, lines, sign, st);
+    launch_pass(p, 2, out, out_ls, n, scratch, n, lines, sign, st);
+    TR_CUDA_CHECK(cudaMemcpy2DAsync(out, sizeof(cplx) * out_ls, scratch, sizeof(cplx) * n,
+                                    sizeof(cplx) * n, lines, cudaMemcpyDeviceToDevice, st));
+  }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}

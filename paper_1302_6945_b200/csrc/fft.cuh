@@ -1,0 +1,49 @@
+// Batched complex128 FFT for lengths 2^a * q (q odd, q <= 63).
+//
+// Multi-pass Stockham autosort: a length-n transform is split into 1-3
+// passes of radix R_i <= 4096 (one kernel launch each).  Inside a pass a CTA
+// stages a tile of T consecutive butterflies (x LB lines) in shared memory and
+// runs the length-R sub-transform there with radix-8/4/2 stages plus at most
+// one direct odd-radix stage.  Twiddles come from exp(+2 pi i k / n) tables
+// computed in long double on the host (0.5 ulp), conjugated for sign < 0.
+//
+//   y[k] = sum_j x[j] * exp(sign * 2 pi i j k / n)     (unnormalized)
+#pragma once
+#include "common.cuh"
+
+struct FftPass {
+  int R;       // sub-transform length of this pass
+  int Ns;      // product of the radices of earlier passes
+  int T;       // consecutive butterflies per CTA tile
+  int LB;      // lines per CTA (single-pass plans only)
+  int nst;     // number of in-smem stages
+  int rad[16]; // in-smem stage radices (first the odd one, then 8/4/2)
+  const cplx* twR;  // table exp(2 pi i k / R)
+};
+
+struct FftPlan {
+  long long n = 0;
+  int npass = 0;
+  FftPass pass[3];
+  const cplx* twN = nullptr;  // table exp(2 pi i k / n)
+};
+
+// Plan (cached per device and length).  Returns 0 on success.
+int fft_plan(long long n, FftPlan* out);
+// Largest odd factor a plan may contain.
+constexpr int FFT_MAX_ODD = 63;
+// True when n = 2^a * q with q odd <= FFT_MAX_ODD.
+bool fft_supported(long long n);
+// Smallest supported length >= n with cheap factors (cost-ranked).
+long long fft_good_len(long long n);
+
+// Batched transform of `lines` lines.  Line i of the input starts at
+// in + i*in_ls and holds in_len <= n valid values (zero-padded to n); the
+// output line i starts at out + i*out_ls.  `scratch` must hold lines*n
+// values.  in == out is allowed.
+int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len,
+             cplx* out, long long out_ls, cplx* scratch, long long lines, int sign,
+             cudaStream_t st);
+
+// Twiddle table exp(2 pi i k / n), k < n (cached, device memory).
+const cplx* twiddle_table(long long n);

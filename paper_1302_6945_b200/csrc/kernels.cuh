@@ -1,0 +1,108 @@
+// Kernel launch interfaces shared by the solver orchestration.
+#pragma once
+#include "common.cuh"
+
+enum { VAR_GENERAL = 0, VAR_L2 = 1, VAR_GRAMIAN = 2 };
+enum { SEQ_PLAIN = 0, SEQ_ADJOINT = 1, SEQ_HERM = 2, SEQ_RHS = 3 };
+
+// One generator-form block (or an rhs vector) feeding the extension /
+// circulant embedding kernels.
+struct SeqDesc {
+  const cplx* g;        // generator (or first column for SEQ_HERM, rhs for SEQ_RHS)
+  long long bstride;    // per-system stride in complex elements (0 = shared)
+  long long len;        // generator length (2n-1 for SEQ_HERM, vector length for SEQ_RHS)
+  int kind;
+  int echo;             // echo fill for the extension (ref extension.py:76-102)
+  long long rows, cols; // block shape (for the circulant embedding)
+};
+struct SeqBatch {
+  SeqDesc d[6];
+};
+
+struct AsmArgs {
+  int variant, rows, P, nblk;
+  long long N, n, m, pl;
+  const cplx* spec;      // [sys][nblk][N] block spectra
+  const double* beta_sq; // |beta|^2 per system
+  long long beta_bstride;
+  const cplx* twN;
+  cplx* W;               // [sys][N][rows][P]
+  cplx* Wp;              // pristine copy (may be null)
+};
+
+int launch_ext_seq(cplx* out, long long N, const SeqBatch& sb, int nblk, long long nsys, cudaStream_t st);
+int launch_emb_col(cplx* out, long long q, const SeqBatch& sb, int nfill, int nblk, long long nsys,
+                   cudaStream_t st);
+int launch_assemble(const AsmArgs& a, long long nsys, cudaStream_t st);
+int launch_spec_mul(cplx* out, long long out_bs, const cplx* a, long long a_bs, const cplx* b,
+                    long long b_bs, long long q, double scale, long long nsys, cudaStream_t st,
+                    int conj_b = 0);
+int launch_mask_scale(cplx* buf, long long bs, long long q, long long keep, double scale,
+                      long long nsys, cudaStream_t st);
+int launch_accum(cplx* acc, long long acc_bs, const cplx* src, long long src_bs, long long n,
+                 double scale, int overwrite, long long nsys, cudaStream_t st);
+int launch_residual(cplx* r, const cplx* ax, const cplx* x, const cplx* y, long long n,
+                    const double* beta_sq, long long beta_bs, int add_ridge, long long nsys,
+                    cudaStream_t st);
+
+// ---- tree (tree.cu) ----
+// G[sys][c][e][q] = sum_{l = q mod cnt, l < L} B[sys][e][l] w_N^(o_c l)
+int launch_twist_fold(cplx* G, const cplx* B, long long b_sys, long long b_cap, int PP, long long L,
+                      long long o0, long long o1, int noff, long long cnt, long long N,
+                      const cplx* twN, long long nsys, cudaStream_t st);
+// W[sys][o_c + s t][r][:] <- W[..][r][:] . Bval(t)   with Bval from G (after the DFT)
+int launch_apply_update(cplx* W, long long w_sys, const cplx* G, int rows, int P, long long o0,
+                        long long o1, int noff, long long stride, long long cnt, long long nsys,
+                        cudaStream_t st);
+// FA[sys][f] <- FA[sys][f] @ FB[sys][f]  (P x P per frequency f < R)
+int launch_pointwise_matmul(cplx* FA, const cplx* FB, int P, long long R, long long nsys,
+                            cudaStream_t st);
+struct TrimArgs {
+  const cplx* F;       // [sys][PP][R] unnormalised product (x R)
+  long long R;
+  long long L;         // untrimmed product length (<= R)
+  int P;
+  double* prof;        // [sys][L] scratch
+  unsigned long long* red;  // [sys][2 + P] : gmax, last, colmax[P]
+  cplx* out;           // [sys][PP][cap]
+  long long out_sys, cap, cap_node;
+  double* max_scale;   // [sys]
+  int* trim_over;      // [sys] count of truncated (beyond bound) products
+};
+int launch_trim_normalize(const TrimArgs& a, long long nsys, cudaStream_t st);
+
+// ---- finish (finish.cu) ----
+struct CleanupArgs {
+  cplx* B;             // root basis [sys][PP][cap] (normalized, len = Lroot bound)
+  long long b_sys, cap;
+  long long len0;      // current (bound) length of the root basis
+  int P, rows;
+  long long N;
+  const cplx* Wp;      // pristine weights
+  const cplx* twN;
+  int2* defer;
+  int* dcount;
+  int dmax;
+  int* cd;
+  double thr;
+  double* max_scale;
+  int* status;
+  int* blen;           // [sys] resulting length
+  cplx* tmp;           // [sys][P][cap] scratch
+};
+int launch_cleanup(const CleanupArgs& a, long long nsys, cudaStream_t st);
+struct ExtractArgs {
+  const cplx* B;
+  long long b_sys, cap;
+  const int* blen;      // may be null -> cap
+  int P;
+  const int* cd;
+  long long n;
+  cplx* x;              // [sys][n]
+  int* status;
+};
+int launch_extract(const ExtractArgs& a, long long nsys, cudaStream_t st);
+// per-system ||v||_2 with a fixed reduction order (chunk partials, then sum)
+int launch_norms(const cplx* v, long long n, long long nsys, double* partial, int nchunk,
+                 double* out, cudaStream_t st);
+int launch_add_inplace(cplx* x, const cplx* d, long long n, long long nsys, cudaStream_t st);

@@ -1,0 +1,46 @@
+// Leaf serial sweep (ref: pkg/src/toepreg/tanint.py:395-434 _serial_leaf,
+// :189-217 _serial_core, :137-186 _Workspace, :262-270 _self_residual,
+// :220-259 absorption orders).
+#pragma once
+#include "common.cuh"
+
+struct LeafArgs {
+  // condition data
+  const cplx* W;        // current weights [sys][N][rows][P]
+  long long w_sys;      // system stride (complex elements)
+  long long N;
+  int rows, P;
+  // leaf node set: offsets o[0..noff) + stride*t, t < M
+  long long o0, o1;
+  int noff;
+  long long stride;
+  int M;                // nodes per coset
+  int count;            // leaf nodes = noff * M
+  int K;                // conditions = rows * count
+  // absorption orders
+  int nattempts;
+  int ord_stride[4];    // perm[i] = (i * s) % count   (ord_reverse: use reversed)
+  int ord_reverse[4];
+  const cplx* twN;      // exp(2 pi i k / N)
+  double thr;           // pivot threshold
+  double check_tol;     // leaf self-check tolerance (1e-11)
+  // per-system state
+  int* cd;              // [sys][8] column degrees (in/out)
+  cplx* out;            // output cube [sys][P*P][cap]
+  long long out_sys;
+  int cap;
+  cplx* scratch;        // same layout as out, for retry attempts
+  int2* defer;          // [sys][dmax] (node, row)
+  int* dcount;          // [sys]
+  int dmax;
+  double* max_scale;    // [sys]
+  int* retried;         // [sys]
+  int* status;          // [sys]
+  double* res_out;      // [sys] best self residual (diagnostic), may be null
+  int* len_out;         // [sys] basis length (diagnostic), may be null
+};
+
+// Launch the register-resident sweep for every system of the batch.
+int leaf_launch(const LeafArgs& a, int nsys, cudaStream_t st);
+// Whether a (P, K) leaf fits the register kernels.
+bool leaf_supported(int P, int K);

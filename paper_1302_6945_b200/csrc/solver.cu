@@ -1,0 +1,1012 @@
+// Host runtime: tree plan, workspace layout, stage orchestration, C ABI.
+//
+// The reference walks its divide-and-conquer tree recursively per solve
+// (ref: pkg/src/toepreg/tanint.py:312-454).  The tree depends only on the
+// problem shape, so here it is planned once per shape (cached) and executed
+// as a flat, level-synchronous op list over a whole batch of systems: every
+// leaf / coset update / combine of the tree is ONE launch over all systems.
+// Lengths are data dependent only through trimming; each node's basis
+// length is bounded by the shifted-degree bookkeeping (max end degree minus
+// min start degree + 1, exact for the water-filling degree multiset), so
+// every FFT size and buffer is fixed on the host and nothing syncs mid-solve.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/toepreg_b200.h"
+#include "fft.cuh"
+#include "kernels.cuh"
+#include "leaf.cuh"
+
+// ------------------------------------------------------------ error state
+static thread_local std::string g_err;
+void tr_set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+extern "C" const char* tr_last_error(void) { return g_err.c_str(); }
+
+#define TR_TRY(expr)          \
+  do {                        \
+    int _rc = (expr);         \
+    if (_rc) return _rc;      \
+  } while (0)
+
+namespace {
+
+constexpr double GOLDEN = 0.6180339887498949;  // ref tanint.py:234
+constexpr double LEAF_CHECK_TOL = 1e-11;       // ref tanint.py:244
+constexpr int DMAX = 512;                       // deferred conditions per system
+constexpr int TRIM_SLACK = 16;
+constexpr int NORM_CHUNKS = 64;
+
+enum { OP_LEAF = 0, OP_UPDATE = 1, OP_COMBINE = 2 };
+
+struct Op {
+  int kind;
+  long long o0 = 0, o1 = 0;
+  int noff = 1;
+  long long stride = 1;
+  int slot_out = -1, slot_a = -1, slot_b = -1;
+  long long cap_a = 0, cap_b = 0, cap_out = 0, R = 0;
+  int K = 0, count = 0, M = 0, depth = 0;
+  int nattempts = 1;
+  int ord_stride[4] = {1, 1, 1, 1};
+  int ord_rev[4] = {0, 0, 0, 0};
+};
+
+struct Plan {
+  tr_desc d;
+  int variant, rows, P, PP;
+  long long n, m, pl, N, q;
+  std::vector<long long> tau;
+  std::vector<Op> ops;
+  std::vector<long long> slot_cap;
+  int depth = 0, root_slot = 2;
+  long long leaves = 0, Kmax = 0, root_cap = 0, leaf_slot_cap = 0;
+  long long Rmax = 1, cnt_max = 1, Lmax = 1;
+  int nblk = 0;
+  std::map<long long, FftPlan> fft;
+  bool fft_ready = false;
+};
+
+int gcd_ll(long long a, long long b) {
+  while (b) { long long t = a % b; a = b; b = t; }
+  return (int)a;
+}
+
+int pyround(double v) { return (int)nearbyint(v); }  // Python round(): half to even
+
+// ref extension.py:42-68
+int opt_extend_detail(long long n_tilde, long long n_lim, int rows, bool paired, bool force_even,
+                      long long* k, int* p, long long* M) {
+  if (n_tilde < 1) { tr_set_error("system size must be positive"); return 2; }
+  if (n_lim < rows) { tr_set_error("serial budget must allow at least one node per row"); return 2; }
+  long long factor = paired ? 2 * rows : rows;
+  int pp = 0;
+  long long m = n_tilde;
+  while (factor * m > n_lim) {
+    if (m <= (force_even ? 2 : 1)) { tr_set_error("serial budget too small to terminate the split"); return 2; }
+    ++pp;
+    m = (m + 1) / 2;
+    if (force_even && (m % 2)) m += 1;
+  }
+  *k = (m << pp) - n_tilde;
+  *p = pp;
+  *M = m;
+  return 0;
+}
+
+struct Builder {
+  Plan& pl;
+  std::vector<int> ms;  // degree multiset (sorted)
+  explicit Builder(Plan& p) : pl(p) {}
+
+  void waterfill(long long steps) {
+    for (long long s = 0; s < steps; ++s) {
+      ms[0] += 1;
+      std::sort(ms.begin(), ms.end());
+    }
+  }
+  int slot_for(int depth, int side) {
+    int id = 2 * depth + side;
+    if ((int)pl.slot_cap.size() <= id) pl.slot_cap.resize(id + 1, 0);
+    return id;
+  }
+  // ref tanint.py:354-366
+  bool split(const std::vector<long long>& off, long long stride, std::vector<long long>& left,
+             std::vector<long long>& right, long long& ns) {
+    long long n = pl.N;
+    if (off.size() == 1) {
+      long long o = off[0];
+      if (pl.d.paired && n % (4 * stride) == 0) {
+        left = {o, o + stride};
+        right = {o + 2 * stride, o + 3 * stride};
+        ns = 4 * stride;
+        return true;
+      }
+      if (n % (2 * stride) == 0) {
+        left = {o};
+        right = {o + stride};
+        ns = 2 * stride;
+        return true;
+      }
+      return false;
+    }
+    if (n % (2 * stride) == 0) {
+      left = {off[0], off[1]};
+      right = {off[0] + stride, off[1] + stride};
+      ns = 2 * stride;
+      return true;
+    }
+    left = {off[0]};
+    right = {off[1]};
+    ns = stride;
+    return true;
+  }
+  long long node(const std::vector<long long>& off, long long stride, int depth, int slot) {
+    pl.depth = std::max(pl.depth, depth);
+    long long count = (long long)pl.rows * (long long)off.size() * (pl.N / stride);
+    std::vector<long long> left, right;
+    long long ns = 0;
+    bool cut = count > pl.d.n_lim && split(off, stride, left, right, ns);
+    if (!cut) {
+      Op op;
+      op.kind = OP_LEAF;
+      op.o0 = off[0];
+      op.o1 = off.size() > 1 ? off[1] : 0;
+      op.noff = (int)off.size();
+      op.stride = stride;
+      op.M = (int)(pl.N / stride);
+      op.count = op.noff * op.M;
+      op.K = (int)count;
+      op.slot_out = slot;
+      op.depth = depth;
+      int c = op.count;
+      if (c <= 2) {
+        op.nattempts = 1;
+        op.ord_stride[0] = 1;
+      } else {
+        int s = pyround(GOLDEN * c);
+        int s0 = s;
+        while (gcd_ll(s0, c) != 1) ++s0;
+        op.nattempts = 4;
+        op.ord_stride[0] = s0;
+        int bumps[2] = {2, 5};
+        for (int b = 0; b < 2; ++b) {
+          int t = s + bumps[b];
+          while (gcd_ll(t, c) != 1) ++t;
+          op.ord_stride[1 + b] = t;
+        }
+        op.ord_stride[3] = s0;
+        op.ord_rev[3] = 1;
+      }
+      pl.ops.push_back(op);
+      pl.leaves += 1;
+      pl.Kmax = std::max<long long>(pl.Kmax, count);
+      waterfill(count);
+      long long cap = count + 1;
+      pl.slot_cap[slot] = std::max(pl.slot_cap[slot], cap);
+      pl.leaf_slot_cap = std::max(pl.leaf_slot_cap, cap);
+      return cap;
+    }
+    int start_min = ms.front();
+    int sl = slot_for(depth + 1, 0), sr = slot_for(depth + 1, 1);
+    long long ca = node(left, ns, depth + 1, sl);
+    Op up;
+    up.kind = OP_UPDATE;
+    up.o0 = right[0];
+    up.o1 = right.size() > 1 ? right[1] : 0;
+    up.noff = (int)right.size();
+    up.stride = ns;
+    up.slot_a = sl;
+    up.cap_a = ca;
+    up.depth = depth;
+    pl.ops.push_back(up);
+    pl.cnt_max = std::max(pl.cnt_max, (long long)up.noff * (pl.N / ns));
+    long long cb = node(right, ns, depth + 1, sr);
+    long long bound = (long long)ms.back() - start_min + 1;
+    Op cm;
+    cm.kind = OP_COMBINE;
+    cm.slot_a = sl;
+    cm.slot_b = sr;
+    cm.cap_a = ca;
+    cm.cap_b = cb;
+    cm.slot_out = slot;
+    cm.depth = depth;
+    long long full = ca + cb - 1;
+    cm.cap_out = std::min(bound + TRIM_SLACK, full);
+    cm.R = fft_good_len(full);
+    pl.Rmax = std::max(pl.Rmax, cm.R);
+    pl.Lmax = std::max(pl.Lmax, full);
+    pl.ops.push_back(cm);
+    pl.slot_cap[slot] = std::max(pl.slot_cap[slot], cm.cap_out);
+    return cm.cap_out;
+  }
+};
+
+std::mutex g_plan_mu;
+std::map<std::string, Plan*> g_plans;
+
+int get_plan(const tr_desc* d, Plan** out) {
+  if (!d) { tr_set_error("null descriptor"); return 2; }
+  if (d->variant < 0 || d->variant > 2) { tr_set_error("unknown variant %d", d->variant); return 2; }
+  if (d->n < 1 || d->m < 1 || (d->variant != TR_L2 && d->p_rows < 1)) {
+    tr_set_error("matrix dimensions must be positive");
+    return 2;
+  }
+  if (d->fill < 0 || d->fill > 2) { tr_set_error("unknown fill policy"); return 2; }
+  if (!(d->pivot_threshold >= 0.0)) { tr_set_error("pivot threshold must be non-negative"); return 2; }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  char key[256];
+  snprintf(key, sizeof key, "%d|%d|%lld|%lld|%lld|%d|%.17g|%d|%d|%d", dev, d->variant,
+           (long long)d->m, (long long)d->n, (long long)(d->variant == TR_L2 ? 0 : d->p_rows),
+           d->n_lim, d->pivot_threshold, d->fill, d->paired, d->force_even);
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  auto it = g_plans.find(key);
+  if (it != g_plans.end()) { *out = it->second; return 0; }
+
+  Plan* p = new Plan();
+  p->d = *d;
+  p->variant = d->variant;
+  p->n = d->n;
+  p->m = d->variant == TR_GRAMIAN ? d->n : d->m;
+  p->pl = d->variant == TR_L2 ? d->n : d->p_rows;
+  p->rows = d->variant == TR_GENERAL ? 3 : 2;
+  p->P = d->variant == TR_GENERAL ? 7 : 5;
+  p->PP = p->P * p->P;
+  long long nt = p->variant == TR_L2 ? p->m + p->n
+               : p->variant == TR_GENERAL ? std::max(p->m, p->pl) + p->n
+                                          : std::max(p->n, p->pl) + p->n;
+  long long k, M;
+  int pp;
+  int rc = opt_extend_detail(nt, d->n_lim, p->rows, d->paired != 0, d->force_even != 0, &k, &pp, &M);
+  if (rc) { delete p; return rc; }
+  p->N = nt + k;
+  long long N = p->N, n = p->n, m = p->m, pl = p->pl;
+  if (p->variant == TR_L2) p->tau = {n - 1, m - 1, N - n - 1, N - m - 1, 0};
+  else if (p->variant == TR_GENERAL) p->tau = {n - 1, m - 1, pl - 1, N - n - 1, N - m - 1, N - pl - 1, 0};
+  else p->tau = {n - 1, pl - 1, N - n - 1, N - pl - 1, 0};
+  p->nblk = p->variant == TR_L2 ? 3 : p->variant == TR_GENERAL ? 5 : 4;
+  long long need = p->variant == TR_L2 ? m + n - 1
+                 : p->variant == TR_GENERAL ? std::max(m + n, pl + n) - 1
+                                            : std::max(2 * n, pl + n) - 1;
+  need = std::max(need, m + n - 1);
+  p->q = fft_good_len(need);
+  if (!fft_supported(N)) {
+    tr_set_error("circulant order %lld has an odd factor above %d", N, FFT_MAX_ODD);
+    delete p;
+    return 2;
+  }
+  Builder b(*p);
+  for (long long t : p->tau) b.ms.push_back((int)-t);
+  std::sort(b.ms.begin(), b.ms.end());
+  int root = b.slot_for(1, 0);
+  p->root_slot = root;
+  p->root_cap = b.node({0}, 1, 1, root);
+  p->slot_cap[root] = std::max(p->slot_cap[root], p->root_cap + DMAX + 1);
+  for (const Op& op : p->ops)
+    if (op.kind == OP_LEAF && !leaf_supported(p->P, op.K)) {
+      tr_set_error("leaf of %d conditions (p=%d) exceeds the register kernel; lower n_lim", op.K, p->P);
+      delete p;
+      return 2;
+    }
+  g_plans[key] = p;
+  *out = p;
+  return 0;
+}
+
+// FFT plans (twiddle tables in device memory) are built on first use, so the
+// shape planning above also works on a machine without a GPU.
+int ensure_fft(Plan* p) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  if (p->fft_ready) return 0;
+  std::vector<long long> sizes = {p->N, p->q};
+  for (const Op& op : p->ops) {
+    if (op.kind == OP_UPDATE) sizes.push_back(p->N / op.stride);
+    if (op.kind == OP_COMBINE) sizes.push_back(op.R);
+  }
+  for (long long s : sizes) {
+    if (p->fft.count(s)) continue;
+    FftPlan fp;
+    int rc = fft_plan(s, &fp);
+    if (rc) return rc;
+    p->fft[s] = fp;
+  }
+  p->fft_ready = true;
+  return 0;
+}
+
+// ------------------------------------------------------------ workspace
+struct Carve {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t count) {
+    off = (off + 255) & ~(size_t)255;
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += sizeof(T) * count;
+    return p;
+  }
+};
+
+struct WS {
+  cplx *W, *Wp, *Y, *X, *X2, *Rv, *AX;
+  cplx* spec_emb;  // [nsys or 1][5][q]
+  std::vector<cplx*> slot;
+  cplx* leaf_scratch;
+  cplx *S1, *S2, *S3;
+  double* prof;
+  unsigned long long* red;
+  int *cd, *dcount, *retried, *status, *trim_over, *blen;
+  int2* defer;
+  double *max_scale, *partial, *nrm, *res_out;
+  int* len_out;
+  cplx* clean_tmp;
+};
+
+size_t layout(const Plan& p, long long nsys, char* base, WS* w) {
+  Carve c{base};
+  const long long N = p.N, n = p.n, q = p.q;
+  const size_t wsz = (size_t)nsys * N * p.rows * p.P;
+  w->W = c.take<cplx>(wsz);
+  w->Wp = c.take<cplx>(wsz);
+  w->Y = c.take<cplx>((size_t)nsys * n);
+  w->X = c.take<cplx>((size_t)nsys * n);
+  w->X2 = c.take<cplx>((size_t)nsys * n);
+  w->Rv = c.take<cplx>((size_t)nsys * n);
+  w->AX = c.take<cplx>((size_t)nsys * n);
+  w->spec_emb = c.take<cplx>((size_t)nsys * 5 * q);
+  w->slot.assign(p.slot_cap.size(), nullptr);
+  for (size_t s = 0; s < p.slot_cap.size(); ++s)
+    if (p.slot_cap[s] > 0) w->slot[s] = c.take<cplx>((size_t)nsys * p.PP * p.slot_cap[s]);
+  w->leaf_scratch = c.take<cplx>((size_t)nsys * p.PP * std::max<long long>(p.leaf_slot_cap, 1) *
+                                 1);
+  size_t big = std::max<size_t>({(size_t)p.nblk * N, (size_t)p.PP * p.cnt_max,
+                                 (size_t)p.PP * p.Rmax, (size_t)q});
+  // the leaf scratch must match the widest slot a leaf writes to
+  long long widest_leaf_slot = 1;
+  for (const Op& op : p.ops)
+    if (op.kind == OP_LEAF) widest_leaf_slot = std::max(widest_leaf_slot, p.slot_cap[op.slot_out]);
+  w->leaf_scratch = c.take<cplx>((size_t)nsys * p.PP * widest_leaf_slot);
+  w->S1 = c.take<cplx>((size_t)nsys * big);
+  w->S2 = c.take<cplx>((size_t)nsys * big);
+  w->S3 = c.take<cplx>((size_t)nsys * big);
+  w->prof = c.take<double>((size_t)nsys * p.Lmax);
+  w->red = c.take<unsigned long long>((size_t)nsys * (2 + p.P));
+  w->cd = c.take<int>((size_t)nsys * 8);
+  w->dcount = c.take<int>((size_t)nsys);
+  w->retried = c.take<int>((size_t)nsys);
+  w->status = c.take<int>((size_t)nsys);
+  w->trim_over = c.take<int>((size_t)nsys);
+  w->blen = c.take<int>((size_t)nsys);
+  w->len_out = c.take<int>((size_t)nsys);
+  w->defer = c.take<int2>((size_t)nsys * DMAX);
+  w->max_scale = c.take<double>((size_t)nsys);
+  w->res_out = c.take<double>((size_t)nsys);
+  w->partial = c.take<double>((size_t)nsys * NORM_CHUNKS);
+  w->nrm = c.take<double>((size_t)nsys * 2);
+  w->clean_tmp = c.take<cplx>((size_t)nsys * p.P * p.slot_cap[p.root_slot]);
+  return c.off + 256;
+}
+
+// ------------------------------------------------------------ execution
+struct Inputs {
+  const cplx *T, *L, *G, *rhs;
+  long long T_bs, L_bs, G_bs, rhs_bs;
+  const double* beta_sq;
+  long long beta_bs;
+  int rhs_is_normal;
+};
+
+__global__ void init_state_kernel(int* cd, int P, const long long* tau_dummy, int* dcount, int* retried,
+                                  int* status, int* trim_over, double* max_scale, long long nsys,
+                                  int t0, int t1, int t2, int t3, int t4, int t5, int t6) {
+  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= nsys) return;
+  int tv[7] = {t0, t1, t2, t3, t4, t5, t6};
+  for (int i = 0; i < 8; ++i) cd[s * 8 + i] = i < P ? -tv[i] : 0;
+  dcount[s] = 0;
+  retried[s] = 0;
+  status[s] = 0;
+  trim_over[s] = 0;
+  max_scale[s] = 1.0;
+}
+
+const FftPlan& F(const Plan& p, long long n) { return p.fft.at(n); }
+
+SeqDesc seq(const cplx* g, long long bs, long long len, int kind, int echo, long long rows,
+            long long cols) {
+  SeqDesc s;
+  s.g = g;
+  s.bstride = bs;
+  s.len = len;
+  s.kind = kind;
+  s.echo = echo;
+  s.rows = rows;
+  s.cols = cols;
+  return s;
+}
+
+// circulant-embedding spectra of the blocks used by T^H b and the normal
+// operator: l2 {T, T^H}; general {T, T^H, L, L^H}; gramian {G, L, L^H}
+int embed_spectra(const Plan& p, const Inputs& in, long long nsys, const WS& w, cudaStream_t st,
+                  long long* spec_bs) {
+  SeqBatch sb;
+  int nb = 0;
+  const long long n = p.n, m = p.m, pl = p.pl;
+  bool shared = true;
+  if (p.variant == TR_L2 || p.variant == TR_GENERAL) {
+    sb.d[nb++] = seq(in.T, in.T_bs, m + n - 1, SEQ_PLAIN, 0, m, n);
+    sb.d[nb++] = seq(in.T, in.T_bs, m + n - 1, SEQ_ADJOINT, 0, n, m);
+    shared = shared && in.T_bs == 0;
+  }
+  if (p.variant == TR_GENERAL || p.variant == TR_GRAMIAN) {
+    sb.d[nb++] = seq(in.L, in.L_bs, pl + n - 1, SEQ_PLAIN, 0, pl, n);
+    sb.d[nb++] = seq(in.L, in.L_bs, pl + n - 1, SEQ_ADJOINT, 0, n, pl);
+    shared = shared && in.L_bs == 0;
+  }
+  if (p.variant == TR_GRAMIAN) {
+    sb.d[nb++] = seq(in.G, in.G_bs, 2 * n - 1, SEQ_HERM, 0, n, n);
+    shared = shared && in.G_bs == 0;
+  }
+  long long ns = shared ? 1 : nsys;
+  TR_TRY(launch_emb_col(w.spec_emb, p.q, sb, nb, 5, ns, st));
+  // unused block lines (nb < 5) are zero-filled by the kernel only for nb
+  // blocks; transform the ones we filled
+  (void)nb;
+  TR_TRY(fft_exec(F(p, p.q), w.spec_emb, p.q, p.q, w.spec_emb, p.q, w.S3, ns * 5, -1, st));
+  *spec_bs = shared ? 0 : 5 * p.q;
+  return 0;
+}
+
+// Block index of a spectrum inside spec_emb
+enum { E_T = 0, E_TH = 1 };
+int eidx(const Plan& p, int which) {
+  // which: 0 T, 1 T^H, 2 L, 3 L^H, 4 G
+  if (p.variant == TR_L2) return which;
+  if (p.variant == TR_GENERAL) return which;
+  // gramian: L, L^H, G
+  return which == 2 ? 0 : which == 3 ? 1 : 2;
+}
+
+// acc (=|+=) B2^H-side gram term: adj(B) (B x) from FX = fft(x)
+int gram_term(const Plan& p, long long nsys, const WS& w, long long sbs, int fwd, int adj,
+              long long rows_blk, int overwrite, cudaStream_t st) {
+  const long long q = p.q;
+  const cplx* Ef = w.spec_emb + (long long)eidx(p, fwd) * q;
+  const cplx* Ea = w.spec_emb + (long long)eidx(p, adj) * q;
+  TR_TRY(launch_spec_mul(w.S2, q, w.S1, q, Ef, sbs, q, 1.0, nsys, st));
+  TR_TRY(fft_exec(F(p, q), w.S2, q, q, w.S2, q, w.S3, nsys, +1, st));
+  TR_TRY(launch_mask_scale(w.S2, q, q, rows_blk, 1.0 / (double)q, nsys, st));
+  TR_TRY(fft_exec(F(p, q), w.S2, q, q, w.S2, q, w.S3, nsys, -1, st));
+  TR_TRY(launch_spec_mul(w.S2, q, w.S2, q, Ea, sbs, q, 1.0 / (double)q, nsys, st));
+  TR_TRY(fft_exec(F(p, q), w.S2, q, q, w.S2, q, w.S3, nsys, +1, st));
+  TR_TRY(launch_accum(w.AX, p.n, w.S2, q, p.n, 1.0, overwrite, nsys, st));
+  return 0;
+}
+
+// AX = (T^H T + L^H L) x  (l2 ridge added in the residual kernel)
+int normal_apply(const Plan& p, long long nsys, const WS& w, long long sbs, const cplx* x,
+                 cudaStream_t st) {
+  const long long q = p.q, n = p.n;
+  TR_TRY(fft_exec(F(p, q), x, n, n, w.S1, q, w.S3, nsys, -1, st));
+  if (p.variant == TR_L2) {
+    TR_TRY(gram_term(p, nsys, w, sbs, 0, 1, p.m, 1, st));
+  } else if (p.variant == TR_GENERAL) {
+    TR_TRY(gram_term(p, nsys, w, sbs, 0, 1, p.m, 1, st));
+    TR_TRY(gram_term(p, nsys, w, sbs, 2, 3, p.pl, 0, st));
+  } else {
+    const cplx* Eg = w.spec_emb + (long long)eidx(p, 4) * q;
+    TR_TRY(launch_spec_mul(w.S2, q, w.S1, q, Eg, sbs, q, 1.0 / (double)q, nsys, st));
+    TR_TRY(fft_exec(F(p, q), w.S2, q, q, w.S2, q, w.S3, nsys, +1, st));
+    TR_TRY(launch_accum(w.AX, n, w.S2, q, n, 1.0, 1, nsys, st));
+    TR_TRY(gram_term(p, nsys, w, sbs, 2, 3, p.pl, 0, st));
+  }
+  return 0;
+}
+
+// Stages 1-4 for normal right-hand sides Y -> solution X
+int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, const cplx* Y,
+               cplx* X, cudaStream_t st) {
+  const long long N = p.N, n = p.n;
+  const int P = p.P, PP = p.PP, rows = p.rows;
+  int t[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < P; ++i) t[i] = (int)p.tau[i];
+  init_state_kernel<<<(unsigned)((nsys + 127) / 128), 128, 0, st>>>(
+      w.cd, P, nullptr, w.dcount, w.retried, w.status, w.trim_over, w.max_scale, nsys, t[0], t[1],
+      t[2], t[3], t[4], t[5], t[6]);
+  TR_CUDA_CHECK(cudaGetLastError());
+
+  // ---- stage 1-2: extended generators -> spectra -> weights ----
+  const cplx* twN = F(p, N).twN;
+  auto echo_for = [&](long long len) {
+    long long k = N - len;
+    int f = p.d.fill;
+    if (k <= 0) return 0;
+    if (f == TR_FILL_ZERO) return 0;
+    if (f == TR_FILL_ECHO) return 1;
+    return k <= 1 ? 0 : 1;
+  };
+  SeqBatch sb;
+  const long long m = p.m, pl = p.pl;
+  if (p.variant == TR_L2) {
+    sb.d[0] = seq(in.T, in.T_bs, m + n - 1, SEQ_ADJOINT, echo_for(m + n - 1), 0, 0);
+    sb.d[1] = seq(in.T, in.T_bs, m + n - 1, SEQ_PLAIN, echo_for(m + n - 1), 0, 0);
+    sb.d[2] = seq(Y, n, n, SEQ_RHS, 0, 0, 0);
+  } else if (p.variant == TR_GENERAL) {
+    sb.d[0] = seq(in.T, in.T_bs, m + n - 1, SEQ_ADJOINT, echo_for(m + n - 1), 0, 0);
+    sb.d[1] = seq(in.L, in.L_bs, pl + n - 1, SEQ_ADJOINT, echo_for(pl + n - 1), 0, 0);
+    sb.d[2] = seq(Y, n, n, SEQ_RHS, 0, 0, 0);
+    sb.d[3] = seq(in.T, in.T_bs, m + n - 1, SEQ_PLAIN, echo_for(m + n - 1), 0, 0);
+    sb.d[4] = seq(in.L, in.L_bs, pl + n - 1, SEQ_PLAIN, echo_for(pl + n - 1), 0, 0);
+  } else {
+    sb.d[0] = seq(in.G, in.G_bs, 2 * n - 1, SEQ_HERM, echo_for(2 * n - 1), 0, 0);
+    sb.d[1] = seq(in.L, in.L_bs, pl + n - 1, SEQ_ADJOINT, echo_for(pl + n - 1), 0, 0);
+    sb.d[2] = seq(Y, n, n, SEQ_RHS, 0, 0, 0);
+    sb.d[3] = seq(in.L, in.L_bs, pl + n - 1, SEQ_PLAIN, echo_for(pl + n - 1), 0, 0);
+  }
+  TR_TRY(launch_ext_seq(w.S1, N, sb, p.nblk, nsys, st));
+  TR_TRY(fft_exec(F(p, N), w.S1, N, N, w.S1, N, w.S2, nsys * p.nblk, +1, st));
+  AsmArgs aa;
+  aa.variant = p.variant;
+  aa.rows = rows;
+  aa.P = P;
+  aa.nblk = p.nblk;
+  aa.N = N;
+  aa.n = n;
+  aa.m = m;
+  aa.pl = pl;
+  aa.spec = w.S1;
+  aa.beta_sq = in.beta_sq;
+  aa.beta_bstride = in.beta_bs;
+  aa.twN = twN;
+  aa.W = w.W;
+  aa.Wp = w.Wp;
+  static const double one = 1.0;
+  (void)one;
+  TR_TRY(launch_assemble(aa, nsys, st));
+
+  // ---- stage 3: the tree ----
+  const long long w_sys = N * rows * P;
+  for (const Op& op : p.ops) {
+    if (op.kind == OP_LEAF) {
+      LeafArgs la;
+      la.W = w.W;
+      la.w_sys = w_sys;
+      la.N = N;
+      la.rows = rows;
+      la.P = P;
+      la.o0 = op.o0;
+      la.o1 = op.o1;
+      la.noff = op.noff;
+      la.stride = op.stride;
+      la.M = op.M;
+      la.count = op.count;
+      la.K = op.K;
+      la.nattempts = op.nattempts;
+      for (int i = 0; i < 4; ++i) {
+        la.ord_stride[i] = op.ord_stride[i];
+        la.ord_reverse[i] = op.ord_rev[i];
+      }
+      la.twN = twN;
+      la.thr = p.d.pivot_threshold;
+      la.check_tol = LEAF_CHECK_TOL;
+      la.cd = w.cd;
+      la.cap = (int)p.slot_cap[op.slot_out];
+      la.out = w.slot[op.slot_out];
+      la.out_sys = (long long)PP * la.cap;
+      la.scratch = w.leaf_scratch;
+      la.defer = w.defer;
+      la.dcount = w.dcount;
+      la.dmax = DMAX;
+      la.max_scale = w.max_scale;
+      la.retried = w.retried;
+      la.status = w.status;
+      la.res_out = w.res_out;
+      la.len_out = w.len_out;
+      TR_TRY(leaf_launch(la, (int)nsys, st));
+    } else if (op.kind == OP_UPDATE) {
+      long long cnt = N / op.stride;
+      long long scap = p.slot_cap[op.slot_a];
+      TR_TRY(launch_twist_fold(w.S1, w.slot[op.slot_a], PP * scap, scap, PP, op.cap_a, op.o0, op.o1,
+                               op.noff, cnt, N, twN, nsys, st));
+      TR_TRY(fft_exec(F(p, cnt), w.S1, cnt, cnt, w.S1, cnt, w.S2, nsys * op.noff * PP, +1, st));
+      TR_TRY(launch_apply_update(w.W, w_sys, w.S1, rows, P, op.o0, op.o1, op.noff, op.stride, cnt,
+                                 nsys, st));
+    } else {
+      long long R = op.R;
+      long long ca = p.slot_cap[op.slot_a], cb = p.slot_cap[op.slot_b];
+      const FftPlan& fp = F(p, R);
+      TR_TRY(fft_exec(fp, w.slot[op.slot_a], ca, op.cap_a, w.S1, R, w.S3, nsys * PP, -1, st));
+      TR_TRY(fft_exec(fp, w.slot[op.slot_b], cb, op.cap_b, w.S2, R, w.S3, nsys * PP, -1, st));
+      TR_TRY(launch_pointwise_matmul(w.S1, w.S2, P, R, nsys, st));
+      TR_TRY(fft_exec(fp, w.S1, R, R, w.S1, R, w.S3, nsys * PP, +1, st));
+      TrimArgs ta;
+      ta.F = w.S1;
+      ta.R = R;
+      ta.L = op.cap_a + op.cap_b - 1;
+      ta.P = P;
+      ta.prof = w.prof;
+      ta.red = w.red;
+      ta.out = w.slot[op.slot_out];
+      ta.cap = p.slot_cap[op.slot_out];
+      ta.out_sys = (long long)PP * ta.cap;
+      ta.cap_node = op.cap_out;
+      ta.max_scale = w.max_scale;
+      ta.trim_over = w.trim_over;
+      TR_TRY(launch_trim_normalize(ta, nsys, st));
+    }
+  }
+
+  // ---- cleanup of deferred conditions, then stage 4 ----
+  CleanupArgs ca;
+  ca.B = w.slot[p.root_slot];
+  ca.cap = p.slot_cap[p.root_slot];
+  ca.b_sys = (long long)PP * ca.cap;
+  ca.len0 = p.root_cap;
+  ca.P = P;
+  ca.rows = rows;
+  ca.N = N;
+  ca.Wp = w.Wp;
+  ca.twN = twN;
+  ca.defer = w.defer;
+  ca.dcount = w.dcount;
+  ca.dmax = DMAX;
+  ca.cd = w.cd;
+  ca.thr = p.d.pivot_threshold;
+  ca.max_scale = w.max_scale;
+  ca.status = w.status;
+  ca.blen = w.blen;
+  ca.tmp = w.clean_tmp;
+  TR_TRY(launch_cleanup(ca, nsys, st));
+  ExtractArgs ea;
+  ea.B = ca.B;
+  ea.b_sys = ca.b_sys;
+  ea.cap = ca.cap;
+  ea.blen = w.blen;
+  ea.P = P;
+  ea.cd = w.cd;
+  ea.n = n;
+  ea.x = X;
+  ea.status = w.status;
+  TR_TRY(launch_extract(ea, nsys, st));
+  return 0;
+}
+
+int normal_rhs(const Plan& p, const Inputs& in, long long nsys, const WS& w, long long sbs,
+               cudaStream_t st) {
+  const long long n = p.n, q = p.q;
+  if (in.rhs_is_normal || p.variant == TR_GRAMIAN) {
+    TR_CUDA_CHECK(cudaMemcpy2DAsync(w.Y, sizeof(cplx) * n, in.rhs, sizeof(cplx) * in.rhs_bs,
+                                    sizeof(cplx) * n, nsys, cudaMemcpyDeviceToDevice, st));
+    return 0;
+  }
+  // y = T^H b by circulant embedding (ref toeplitz.py:93-111, :229-233)
+  TR_TRY(fft_exec(F(p, q), in.rhs, in.rhs_bs, p.m, w.S1, q, w.S3, nsys, -1, st));
+  const cplx* Eth = w.spec_emb + (long long)eidx(p, 1) * q;
+  TR_TRY(launch_spec_mul(w.S1, q, w.S1, q, Eth, sbs, q, 1.0, nsys, st));
+  TR_TRY(fft_exec(F(p, q), w.S1, q, q, w.S1, q, w.S3, nsys, +1, st));
+  TR_TRY(launch_accum(w.Y, n, w.S1, q, n, 1.0 / (double)q, 1, nsys, st));
+  return 0;
+}
+
+int solve_chunk(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx* x_out,
+                cudaStream_t st, tr_diag* diag_host) {
+  const long long n = p.n;
+  long long sbs = 0;
+  TR_TRY(embed_spectra(p, in, nsys, w, st, &sbs));
+  TR_TRY(normal_rhs(p, in, nsys, w, sbs, st));
+  TR_TRY(solve_core(p, in, nsys, w, w.Y, w.X, st));
+  const int add_ridge = p.variant == TR_L2;
+  for (int r = 0; r < p.d.refine; ++r) {
+    // r = y - A x ; solve A d = r ; x += d
+    TR_TRY(normal_apply(p, nsys, w, sbs, w.X, st));
+    TR_TRY(launch_residual(w.Rv, w.AX, w.X, w.Y, n, in.beta_sq, in.beta_bs, add_ridge, nsys, st));
+    TR_TRY(solve_core(p, in, nsys, w, w.Rv, w.X2, st));
+    TR_TRY(launch_add_inplace(w.X, w.X2, n, nsys, st));
+  }
+  // residual for the report (ref solver.py:72-75)
+  TR_TRY(normal_apply(p, nsys, w, sbs, w.X, st));
+  TR_TRY(launch_residual(w.Rv, w.AX, w.X, w.Y, n, in.beta_sq, in.beta_bs, add_ridge, nsys, st));
+  TR_TRY(launch_norms(w.Rv, n, nsys, w.partial, NORM_CHUNKS, w.nrm, st));
+  TR_TRY(launch_norms(w.Y, n, nsys, w.partial, NORM_CHUNKS, w.nrm + nsys, st));
+  TR_CUDA_CHECK(cudaMemcpyAsync(x_out, w.X, sizeof(cplx) * nsys * n, cudaMemcpyDeviceToDevice, st));
+  if (diag_host) {
+    std::vector<int> cd(nsys * 8), dc(nsys), rt(nsys), stt(nsys), tro(nsys);
+    std::vector<double> ms(nsys), nr(2 * nsys);
+    TR_CUDA_CHECK(cudaMemcpyAsync(cd.data(), w.cd, sizeof(int) * nsys * 8, cudaMemcpyDeviceToHost, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(dc.data(), w.dcount, sizeof(int) * nsys, cudaMemcpyDeviceToHost, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(rt.data(), w.retried, sizeof(int) * nsys, cudaMemcpyDeviceToHost, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(stt.data(), w.status, sizeof(int) * nsys, cudaMemcpyDeviceToHost, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(tro.data(), w.trim_over, sizeof(int) * nsys, cudaMemcpyDeviceToHost, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(ms.data(), w.max_scale, sizeof(double) * nsys, cudaMemcpyDeviceToHost, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(nr.data(), w.nrm, sizeof(double) * 2 * nsys, cudaMemcpyDeviceToHost, st));
+    TR_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (long long s = 0; s < nsys; ++s) {
+      tr_diag& dg = diag_host[s];
+      memset(&dg, 0, sizeof dg);
+      dg.status = stt[s];
+      dg.difficult_points = dc[s];
+      dg.conditions_total = (long long)p.rows * p.N;
+      dg.recursion_depth = p.depth;
+      dg.retried_leaves = rt[s];
+      dg.max_column_scale = ms[s];
+      for (int i = 0; i < p.P; ++i) dg.final_col_degrees[i] = cd[s * 8 + i];
+      double den = nr[nsys + s];
+      dg.relative_residual = nr[s] / (den > 0.0 ? den : 1.0);
+      dg.trim_overflow = tro[s];
+    }
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" size_t tr_workspace_bytes(const tr_desc* d, int64_t batch) {
+  Plan* p;
+  if (get_plan(d, &p)) return 0;
+  WS w;
+  return layout(*p, batch, nullptr, &w);
+}
+
+extern "C" int tr_plan_info(const tr_desc* d, int64_t* order, int64_t* leaves, int32_t* depth,
+                            int64_t* max_leaf_conditions) {
+  Plan* p;
+  TR_TRY(get_plan(d, &p));
+  if (order) *order = p->N;
+  if (leaves) *leaves = p->leaves;
+  if (depth) *depth = p->depth;
+  if (max_leaf_conditions) *max_leaf_conditions = p->Kmax;
+  return 0;
+}
+
+extern "C" int tr_solve_batch(const tr_desc* d, int64_t batch, const double* T_gen, int64_t T_bs,
+                              const double* L_gen, int64_t L_bs, const double* G_col, int64_t G_bs,
+                              const double* beta_sq, int64_t beta_bs, const double* rhs,
+                              int64_t rhs_bs, int32_t rhs_is_normal, double* x_out,
+                              tr_diag* diag_host, void* workspace, size_t ws_bytes, void* stream) {
+  Plan* p;
+  TR_TRY(get_plan(d, &p));
+  if (batch <= 0) return 0;
+  TR_TRY(ensure_fft(p));
+  WS w;
+  size_t need = layout(*p, batch, nullptr, &w);
+  if (!workspace || ws_bytes < need) {
+    tr_set_error("workspace too small: need %zu bytes, got %zu", need, ws_bytes);
+    return 2;
+  }
+  if (p->variant != TR_GRAMIAN && !T_gen) { tr_set_error("T generator required"); return 2; }
+  if (p->variant != TR_L2 && !L_gen) { tr_set_error("L generator required"); return 2; }
+  if (p->variant == TR_GRAMIAN && !G_col) { tr_set_error("G column required"); return 2; }
+  if (p->variant == TR_L2 && !beta_sq) { tr_set_error("beta_sq required"); return 2; }
+  if (!rhs || !x_out) { tr_set_error("rhs and x_out required"); return 2; }
+  layout(*p, batch, (char*)workspace, &w);
+  static const double zero = 0.0;
+  (void)zero;
+  Inputs in;
+  in.T = reinterpret_cast<const cplx*>(T_gen);
+  in.L = reinterpret_cast<const cplx*>(L_gen);
+  in.G = reinterpret_cast<const cplx*>(G_col);
+  in.rhs = reinterpret_cast<const cplx*>(rhs);
+  in.T_bs = T_bs;
+  in.L_bs = L_bs;
+  in.G_bs = G_bs;
+  in.rhs_bs = rhs_bs;
+  in.beta_sq = beta_sq;
+  in.beta_bs = beta_bs;
+  in.rhs_is_normal = rhs_is_normal;
+  // beta_sq is only read for l2; point others at the workspace norm slot
+  if (!in.beta_sq) { in.beta_sq = w.nrm; in.beta_bs = 0; }
+  cudaStream_t st = (cudaStream_t)stream;
+  TR_TRY(solve_chunk(*p, in, batch, w, reinterpret_cast<cplx*>(x_out), st, diag_host));
+  if (diag_host) {
+    for (long long s = 0; s < batch; ++s) {
+      if (diag_host[s].status == 3) return 3;
+      if (diag_host[s].status == 5) {
+        tr_set_error("system %lld: more than %d deferred conditions", s, DMAX);
+        return 5;
+      }
+    }
+  }
+  return 0;
+}
+
+extern "C" int tr_solve_batch_host(const tr_desc* d, int64_t batch, const double* T_gen, int64_t T_bs,
+                                   const double* L_gen, int64_t L_bs, const double* G_col,
+                                   int64_t G_bs, const double* beta_sq, int64_t beta_bs,
+                                   const double* rhs, int64_t rhs_bs, int32_t rhs_is_normal,
+                                   double* x_out, tr_diag* diag_host) {
+  Plan* p;
+  TR_TRY(get_plan(d, &p));
+  if (batch <= 0) return 0;
+  const long long n = p->n, m = p->m, pl = p->pl;
+  auto sz = [&](const void* ptr, long long bs, long long len) -> size_t {
+    if (!ptr) return 0;
+    return sizeof(cplx) * (size_t)(bs ? bs * (batch - 1) + len : len);
+  };
+  size_t bT = sz(T_gen, T_bs, m + n - 1), bL = sz(L_gen, L_bs, pl + n - 1), bG = sz(G_col, G_bs, n);
+  size_t bB = beta_sq ? sizeof(double) * (size_t)(beta_bs ? beta_bs * (batch - 1) + 1 : 1) : 0;
+  long long rlen = (rhs_is_normal || p->variant == TR_GRAMIAN) ? n : m;
+  size_t bR = sz(rhs, rhs_bs, rlen), bX = sizeof(cplx) * (size_t)batch * n;
+  size_t ws = tr_workspace_bytes(d, batch);
+  char* dev = nullptr;
+  size_t total = bT + bL + bG + bB + bR + bX + ws + 8 * 256;
+  TR_CUDA_CHECK(cudaMalloc(&dev, total));
+  Carve c{dev};
+  double* dT = bT ? c.take<double>(bT / 8) : nullptr;
+  double* dL = bL ? c.take<double>(bL / 8) : nullptr;
+  double* dG = bG ? c.take<double>(bG / 8) : nullptr;
+  double* dB = bB ? c.take<double>(bB / 8) : nullptr;
+  double* dR = c.take<double>(bR / 8);
+  double* dX = c.take<double>(bX / 8);
+  char* dW = c.take<char>(ws);
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (bT) cudaMemcpyAsync(dT, T_gen, bT, cudaMemcpyHostToDevice, st);
+  if (bL) cudaMemcpyAsync(dL, L_gen, bL, cudaMemcpyHostToDevice, st);
+  if (bG) cudaMemcpyAsync(dG, G_col, bG, cudaMemcpyHostToDevice, st);
+  if (bB) cudaMemcpyAsync(dB, beta_sq, bB, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(dR, rhs, bR, cudaMemcpyHostToDevice, st);
+  int rc = tr_solve_batch(d, batch, dT, T_bs, dL, L_bs, dG, G_bs, dB, beta_bs, dR, rhs_bs,
+                          rhs_is_normal, dX, diag_host, dW, ws, st);
+  if (rc == 0 || rc == 3) cudaMemcpyAsync(x_out, dX, bX, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  cudaFree(dev);
+  return rc;
+}
+
+// ---------------------------------------------------------------- stages
+extern "C" int tr_fft(const double* in, double* out, int64_t n, int64_t lines, int32_t sign,
+                      void* stream) {
+  FftPlan fp;
+  TR_TRY(fft_plan(n, &fp));
+  cplx* scratch = nullptr;
+  TR_CUDA_CHECK(cudaMalloc(&scratch, sizeof(cplx) * (size_t)n * lines));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = fft_exec(fp, reinterpret_cast<const cplx*>(in), n, n, reinterpret_cast<cplx*>(out), n,
+                    scratch, lines, sign >= 0 ? 1 : -1, st);
+  cudaStreamSynchronize(st);
+  cudaFree(scratch);
+  return rc;
+}
+
+extern "C" int tr_grid_eval(const double* coeffs, int64_t lines, int64_t length, int64_t n_nodes,
+                            int64_t offset, int64_t stride, double* out, void* stream) {
+  if (n_nodes < 1 || stride < 1 || n_nodes % stride) {
+    tr_set_error("stride must be a positive divisor of the grid size");
+    return 2;
+  }
+  long long cnt = n_nodes / stride;
+  FftPlan fpn, fpc;
+  TR_TRY(fft_plan(n_nodes, &fpn));
+  TR_TRY(fft_plan(cnt, &fpc));
+  cplx* scratch = nullptr;
+  TR_CUDA_CHECK(cudaMalloc(&scratch, sizeof(cplx) * (size_t)cnt * lines));
+  cudaStream_t st = (cudaStream_t)stream;
+  long long off = ((offset % n_nodes) + n_nodes) % n_nodes;
+  int rc = launch_twist_fold(reinterpret_cast<cplx*>(out), reinterpret_cast<const cplx*>(coeffs),
+                             length, length, 1, length, off, 0, 1, cnt, n_nodes, fpn.twN, lines, st);
+  if (!rc)
+    rc = fft_exec(fpc, reinterpret_cast<cplx*>(out), cnt, cnt, reinterpret_cast<cplx*>(out), cnt,
+                  scratch, lines, +1, st);
+  cudaStreamSynchronize(st);
+  cudaFree(scratch);
+  return rc;
+}
+
+extern "C" int tr_matpoly_mul(const double* a, int64_t la, const double* b, int64_t lb, int32_t p,
+                              double* out, void* stream) {
+  if (p != 5 && p != 7) { tr_set_error("p must be 5 or 7"); return 2; }
+  long long L = la + lb - 1, R = fft_good_len(L), PP = (long long)p * p;
+  FftPlan fp;
+  TR_TRY(fft_plan(R, &fp));
+  cplx* buf = nullptr;
+  TR_CUDA_CHECK(cudaMalloc(&buf, sizeof(cplx) * (size_t)R * PP * 3));
+  cplx *FA = buf, *FB = buf + R * PP, *S = buf + 2 * R * PP;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = fft_exec(fp, reinterpret_cast<const cplx*>(a), la, la, FA, R, S, PP, -1, st);
+  if (!rc) rc = fft_exec(fp, reinterpret_cast<const cplx*>(b), lb, lb, FB, R, S, PP, -1, st);
+  if (!rc) rc = launch_pointwise_matmul(FA, FB, p, R, 1, st);
+  if (!rc) rc = fft_exec(fp, FA, R, R, FA, R, S, PP, +1, st);
+  if (!rc) rc = launch_accum(reinterpret_cast<cplx*>(out), L, FA, R, L, 1.0 / (double)R, 1, PP, st);
+  cudaStreamSynchronize(st);
+  cudaFree(buf);
+  return rc;
+}
+
+extern "C" int tr_assemble(const tr_desc* d, const double* T_gen, const double* L_gen,
+                           const double* G_col, const double* beta_sq, const double* rhs,
+                           int32_t rhs_is_normal, double* weights_out, void* stream) {
+  Plan* p;
+  TR_TRY(get_plan(d, &p));
+  TR_TRY(ensure_fft(p));
+  WS w;
+  size_t need = layout(*p, 1, nullptr, &w);
+  char* ws = nullptr;
+  TR_CUDA_CHECK(cudaMalloc(&ws, need));
+  layout(*p, 1, ws, &w);
+  cudaStream_t st = (cudaStream_t)stream;
+  Inputs in;
+  in.T = reinterpret_cast<const cplx*>(T_gen);
+  in.L = reinterpret_cast<const cplx*>(L_gen);
+  in.G = reinterpret_cast<const cplx*>(G_col);
+  in.rhs = reinterpret_cast<const cplx*>(rhs);
+  in.T_bs = in.L_bs = in.G_bs = 0;
+  in.rhs_bs = (rhs_is_normal || p->variant == TR_GRAMIAN) ? p->n : p->m;
+  in.beta_sq = beta_sq ? beta_sq : w.nrm;
+  in.beta_bs = 0;
+  in.rhs_is_normal = rhs_is_normal;
+  long long sbs = 0;
+  int rc = embed_spectra(*p, in, 1, w, st, &sbs);
+  if (!rc) rc = normal_rhs(*p, in, 1, w, sbs, st);
+  if (!rc) {
+    // run only stages 1-2 by solving nothing: reuse solve_core's prologue
+    SeqBatch sb;
+    (void)sb;
+  }
+  // stages 1-2 (duplicated from solve_core's prologue for a weights-only call)
+  if (!rc) {
+    const long long N = p->N, n = p->n, m = p->m, pl = p->pl;
+    auto echo_for = [&](long long len) {
+      long long k = N - len;
+      int f = p->d.fill;
+      if (k <= 0 || f == TR_FILL_ZERO) return 0;
+      if (f == TR_FILL_ECHO) return 1;
+      return k <= 1 ? 0 : 1;
+    };
+    SeqBatch sb;
+    if (p->variant == TR_L2) {
+      sb.d[0] = seq(in.T, 0, m + n - 1, SEQ_ADJOINT, echo_for(m + n - 1), 0, 0);
+      sb.d[1] = seq(in.T, 0, m + n - 1, SEQ_PLAIN, echo_for(m + n - 1), 0, 0);
+      sb.d[2] = seq(w.Y, n, n, SEQ_RHS, 0, 0, 0);
+    } else if (p->variant == TR_GENERAL) {
+      sb.d[0] = seq(in.T, 0, m + n - 1, SEQ_ADJOINT, echo_for(m + n - 1), 0, 0);
+      sb.d[1] = seq(in.L, 0, pl + n - 1, SEQ_ADJOINT, echo_for(pl + n - 1), 0, 0);
+      sb.d[2] = seq(w.Y, n, n, SEQ_RHS, 0, 0, 0);
+      sb.d[3] = seq(in.T, 0, m + n - 1, SEQ_PLAIN, echo_for(m + n - 1), 0, 0);
+      sb.d[4] = seq(in.L, 0, pl + n - 1, SEQ_PLAIN, echo_for(pl + n - 1), 0, 0);
+    } else {
+      sb.d[0] = seq(in.G, 0, 2 * n - 1, SEQ_HERM, echo_for(2 * n - 1), 0, 0);
+      sb.d[1] = seq(in.L, 0, pl + n - 1, SEQ_ADJOINT, echo_for(pl + n - 1), 0, 0);
+      sb.d[2] = seq(w.Y, n, n, SEQ_RHS, 0, 0, 0);
+      sb.d[3] = seq(in.L, 0, pl + n - 1, SEQ_PLAIN, echo_for(pl + n - 1), 0, 0);
+    }
+    rc = launch_ext_seq(w.S1, N, sb, p->nblk, 1, st);
+    if (!rc) rc = fft_exec(F(*p, N), w.S1, N, N, w.S1, N, w.S2, p->nblk, +1, st);
+    AsmArgs aa;
+    aa.variant = p->variant;
+    aa.rows = p->rows;
+    aa.P = p->P;
+    aa.nblk = p->nblk;
+    aa.N = N;
+    aa.n = n;
+    aa.m = m;
+    aa.pl = pl;
+    aa.spec = w.S1;
+    aa.beta_sq = in.beta_sq;
+    aa.beta_bstride = 0;
+    aa.twN = F(*p, N).twN;
+    aa.W = reinterpret_cast<cplx*>(weights_out);
+    aa.Wp = nullptr;
+    if (!rc) rc = launch_assemble(aa, 1, st);
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(ws);
+  return rc;
+}
