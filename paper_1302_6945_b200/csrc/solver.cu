@@ -704,7 +704,7 @@ int normal_rhs(const Plan& p, const Inputs& in, long long nsys, const WS& w, lon
   return 0;
 }
 
-int solve_chunk(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx* x_out,
+int solve_chunk(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx* x_out, int refine,
                 cudaStream_t st, tr_diag* diag_host) {
   const long long n = p.n;
   long long sbs = 0;
@@ -712,7 +712,7 @@ int solve_chunk(const Plan& p, const Inputs& in, long long nsys, const WS& w, cp
   TR_TRY(normal_rhs(p, in, nsys, w, sbs, st));
   TR_TRY(solve_core(p, in, nsys, w, w.Y, w.X, st));
   const int add_ridge = p.variant == TR_L2;
-  for (int r = 0; r < p.d.refine; ++r) {
+  for (int r = 0; r < refine; ++r) {
     // r = y - A x ; solve A d = r ; x += d
     TR_TRY(normal_apply(p, nsys, w, sbs, w.X, st));
     TR_TRY(launch_residual(w.Rv, w.AX, w.X, w.Y, n, in.beta_sq, in.beta_bs, add_ridge, nsys, st));
@@ -813,7 +813,7 @@ extern "C" int tr_solve_batch(const tr_desc* d, int64_t batch, const double* T_g
   // beta_sq is only read for l2; point others at the workspace norm slot
   if (!in.beta_sq) { in.beta_sq = w.nrm; in.beta_bs = 0; }
   cudaStream_t st = (cudaStream_t)stream;
-  TR_TRY(solve_chunk(*p, in, batch, w, reinterpret_cast<cplx*>(x_out), st, diag_host));
+  TR_TRY(solve_chunk(*p, in, batch, w, reinterpret_cast<cplx*>(x_out), d->refine, st, diag_host));
   if (diag_host) {
     for (long long s = 0; s < batch; ++s) {
       if (diag_host[s].status == 3) return 3;
