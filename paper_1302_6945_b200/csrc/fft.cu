@@ -1,5 +1,6 @@
 // Batched complex128 multi-pass Stockham FFT (see fft.cuh).
 #include "fft.cuh"
+#include "fft_fast.cuh"
 
 #include <math.h>
 #include <map>
@@ -301,31 +302,33 @@ int fft_plan(long long n, FftPlan* out) {
   if (n <= FFT_TILE) {
     radices.push_back(n);
   } else {
-    // passes of radix <= 1024 (so T >= 4); the odd factor rides in the first
+    // passes of radix <= 1024 (tiles of >= 4 sub-transforms keep global
+    // accesses in >= 64 B runs).  Leading passes are powers of two so every
+    // pass's Ns is a power of two; the odd factor rides in the last pass.
     int a = 0;
-    while ((p2 >> a) > 1) ++a;           // p2 = 2^a
+    while ((p2 >> a) > 1) ++a;  // p2 = 2^a
     int npass = (n <= 1024LL * 1024LL) ? 2 : 3;
-    // later passes take powers of two, balanced, each <= 2^10
-    int lg = 0;
-    while ((1LL << lg) < n) ++lg;
-    int b_each = (lg + npass - 1) / npass;
-    if (b_each > 10) b_each = 10;
-    std::vector<long long> tail;
-    int used = 0;
-    for (int i = 1; i < npass; ++i) {
-      int b = b_each;
-      if (used + b > a) b = a - used;
-      tail.push_back(1LL << b);
-      used += b;
+    int lgq = 0;
+    while ((1LL << lgq) < q) ++lgq;
+    int lg = a + lgq;
+    int share = (lg + npass - 1) / npass;
+    int b_last = share - lgq;
+    if (b_last < 0) b_last = 0;
+    int rest = a - b_last;
+    std::vector<long long> lead;
+    for (int i = 0; i < npass - 1; ++i) {
+      int left = npass - 1 - i;
+      int b = (rest + left - 1) / left;
+      if (b > 10) b = 10;
+      lead.push_back(1LL << b);
+      rest -= b;
     }
-    long long first = q << (a - used);
-    // rebalance if the first pass is too large
-    for (size_t i = 0; first > 1024 && i < tail.size(); ++i) {
-      while (first > 1024 && tail[i] < 1024 && (first % 2 == 0)) { tail[i] *= 2; first /= 2; }
-    }
-    if (first > 1024) { tr_set_error("fft length %lld cannot be split", n); return 2; }
-    radices.push_back(first);
-    for (long long t : tail) radices.push_back(t);
+    b_last += rest;  // whatever the leading passes could not take
+    long long last = q << b_last;
+    if (last > 1024 && q == 1) { tr_set_error("fft length %lld cannot be split", n); return 2; }
+    if (last > FFT_TILE) { tr_set_error("fft length %lld cannot be split", n); return 2; }
+    for (long long t : lead) radices.push_back(t);
+    radices.push_back(last);
   }
   (void)p2;
   if (radices.size() > 3) { tr_set_error("fft length %lld needs too many passes", n); return 2; }
@@ -350,6 +353,10 @@ int fft_plan(long long n, FftPlan* out) {
       ps.T = (int)T;
     }
     split_pow2(ps.R, ps.rad, &ps.nst);
+    ps.q = (int)odd_part(ps.R);
+    ps.log2 = 0;
+    while ((ps.q << ps.log2) < ps.R) ++ps.log2;
+    ps.fast = fast_supported(ps.log2, ps.q) && ((Ns & (Ns - 1)) == 0);
     ps.twR = twiddle_table(ps.R);
     if (!ps.twR) { tr_set_error("twiddle table allocation failed (R=%d)", ps.R); return 4; }
     Ns *= ps.R;
@@ -361,6 +368,24 @@ int fft_plan(long long n, FftPlan* out) {
 static int launch_pass(const FftPlan& p, int i, const cplx* in, long long in_ls, long long in_len,
                        cplx* out, long long out_ls, long long lines, int sign, cudaStream_t st) {
   const FftPass& ps = p.pass[i];
+  if (ps.fast) {
+    FastArgs f;
+    f.in = in;
+    f.in_ls = in_ls;
+    f.in_len = (int)in_len;
+    f.out = out;
+    f.out_ls = out_ls;
+    f.J = (int)(p.n / ps.R);
+    f.nsub = lines * (long long)f.J;
+    f.Ns = ps.Ns;
+    f.log2Ns = 0;
+    while ((1 << f.log2Ns) < ps.Ns) ++f.log2Ns;
+    f.tws = (int)(p.n / ((long long)ps.Ns * ps.R));
+    f.twN = p.twN;
+    f.twR = ps.twR;
+    f.sign = sign;
+    if (fast_launch(ps.log2, ps.q, f, st) == 0) return 0;
+  }
   PassArgs a;
   a.n = p.n;
   a.R = ps.R;

@@ -19,6 +19,8 @@ struct FftPass {
   int nst;     // number of in-smem stages
   int rad[16]; // in-smem stage radices (first the odd one, then 8/4/2)
   const cplx* twR;  // table exp(2 pi i k / R)
+  int log2, q;      // R = q * 2^log2
+  bool fast;        // compile-time-shaped kernel available (fft_fast.cu)
 };
 
 struct FftPlan {

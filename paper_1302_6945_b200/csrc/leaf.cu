@@ -32,7 +32,7 @@ TR_D long long leaf_node(const LeafArgs& a, int p) {
 
 TR_D int leaf_perm(int i, int s, int rev, int count) {
   if (rev) i = count - 1 - i;
-  return (int)(((long long)i * s) % count);
+  return (int)(((unsigned)i * (unsigned)s) % (unsigned)count);
 }
 
 TR_D double warp_max(double v) {
@@ -71,8 +71,43 @@ TR_D void step_body(cplx (&c)[D][P], cplx (&r)[P], const cplx (&mu)[P], cplx msi
   }
 }
 
-template <int P, int D, int J>
-TR_D cplx top_of(const cplx (&c)[D][P]) { return c[D - 1][J]; }
+// Pivot rule of the reference (ref tanint.py:193-211): among the columns of
+// lowest degree take the first with the largest |phi|; defer when it is below
+// thr * max|phi|.  Compared on squared moduli; mu = -phi / phi_j.
+template <int P>
+TR_D void pivot_publish(const cplx (&phi)[P], const int (&cd)[P], double thr, cplx* mu_out,
+                        int* j_out, int* small_out) {
+  double a2[P], amax2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    a2[i] = cabs2(phi[i]);
+    amax2 = fmax(amax2, a2[i]);
+  }
+  int small = amax2 == 0.0;
+  int j = 0;
+  if (!small) {
+    int dmin = cd[0];
+#pragma unroll
+    for (int i = 1; i < P; ++i) dmin = min(dmin, cd[i]);
+    double bm = -1.0;
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      if (cd[i] == dmin && a2[i] > bm) { bm = a2[i]; j = i; }
+    small = bm < thr * thr * amax2;
+  }
+  if (!small) {
+    cplx pj = cmk(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      if (i == j) pj = phi[i];
+    const double inv2 = 1.0 / cabs2(pj);
+    const cplx inv = cmk(pj.x * inv2, -pj.y * inv2);
+#pragma unroll
+    for (int i = 0; i < P; ++i) mu_out[i] = cneg(cmul(phi[i], inv));
+  }
+  *j_out = j;
+  *small_out = small;
+}
 
 template <int P, int D>
 TR_D cplx top_dyn(const cplx (&c)[D][P], int j) {
@@ -95,6 +130,7 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
   double* red = reinterpret_cast<double*>(bvb + P * P * a.M);  // [NW][P]
   int2* dcur = reinterpret_cast<int2*>(red + NW * P);     // [K]
   int2* dbest = dcur + a.K;                               // [K]
+  int* pubi = reinterpret_cast<int*>(dbest + a.K);        // [2] pivot, [2] deferral flag
 
   const int sys = blockIdx.x;
   const int tid = threadIdx.x;
@@ -157,10 +193,7 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
 #pragma unroll
       for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
     }
-    if (tid == 0) {
-#pragma unroll
-      for (int i = 0; i < P; ++i) phib[i] = r[i];
-    }
+    if (tid == 0) pivot_publish<P>(r, cd, a.thr, phib, pubi, pubi + 2);
     if (lane == 31) {
 #pragma unroll
       for (int i = 0; i < P; ++i) halo[warp * P + i] = c[D - 1][i];
@@ -169,36 +202,20 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
 
     for (int t = 0; t < K; ++t) {
       const int cur = t & 1, nxt = cur ^ 1;
-      cplx phi[P];
-#pragma unroll
-      for (int i = 0; i < P; ++i) phi[i] = phib[cur * P + i];
+      // pivot j, deferral flag and multipliers of condition t were computed
+      // once by the thread owning condition t (ref tanint.py:193-211)
+      const int j = pubi[cur];
+      const bool small = pubi[2 + cur] != 0;
       const int pos_t = leaf_perm(t / rows, ostr, orev, count);
       const long long node_t = leaf_node(a, pos_t);
       const cplx sig_t = __ldg(&a.twN[node_t]);
-      // pivot among the lowest columns, first max (ref tanint.py:193-200)
-      double amax = 0.0;
-      double ab[P];
-#pragma unroll
-      for (int i = 0; i < P; ++i) { ab[i] = cabs(phi[i]); amax = fmax(amax, ab[i]); }
-      bool small = (amax == 0.0);
-      int j = 0;
-      if (!small) {
-        int dmin = cd[0];
-#pragma unroll
-        for (int i = 1; i < P; ++i) dmin = min(dmin, cd[i]);
-        double bm = -1.0;
-#pragma unroll
-        for (int i = 0; i < P; ++i)
-          if (cd[i] == dmin && ab[i] > bm) { bm = ab[i]; j = i; }
-        small = bm < a.thr * amax;
-      }
       if (small) {
         if (tid == 0) dcur[ndef] = make_int2((int)node_t, t % rows);
         ++ndef;
       } else {
         cplx mu[P];
 #pragma unroll
-        for (int i = 0; i < P; ++i) mu[i] = cdiv_np(cneg(phi[i]), phi[j]);
+        for (int i = 0; i < P; ++i) mu[i] = phib[cur * P + i];
         const cplx msig = cneg(sig_t);
         // neighbour's old top coefficient of column j
         cplx mytop = top_dyn<P, D>(c, j);
@@ -228,7 +245,7 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
           for (int i = 0; i < P; ++i) {
             double m = 0.0;
 #pragma unroll
-            for (int d = 0; d < D; ++d) m = fmax(m, cabs(c[d][i]));
+            for (int d = 0; d < D; ++d) m = fmax(m, cabs2(c[d][i]));
             loc[i] = warp_max(m);
           }
           if (lane == 0) {
@@ -240,6 +257,7 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
           for (int i = 0; i < P; ++i) {
             double m = red[i];
             for (int w = 1; w < NW; ++w) m = fmax(m, red[w * P + i]);
+            m = sqrt(m);
             if (m > RESCALE_TRIGGER) {
               double inv = 1.0 / m;
 #pragma unroll
@@ -250,11 +268,9 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
           }
         }
       }
-      // publish phi_{t+1} and this warp's top coefficients
-      if (owner && tid == t + 1) {
-#pragma unroll
-        for (int i = 0; i < P; ++i) phib[nxt * P + i] = r[i];
-      }
+      // the owner of condition t+1 decides its pivot; publish the warp's
+      // top coefficients for the next shift
+      if (owner && tid == t + 1) pivot_publish<P>(r, cd, a.thr, phib + nxt * P, pubi + nxt, pubi + 2 + nxt);
       if (lane == 31) {
 #pragma unroll
         for (int i = 0; i < P; ++i) halo[(nxt * NW + warp) * P + i] = c[D - 1][i];
@@ -270,7 +286,7 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
       for (int i = 0; i < P; ++i) {
         double m = 0.0;
 #pragma unroll
-        for (int d = 0; d < D; ++d) m = fmax(m, cabs(c[d][i]));
+        for (int d = 0; d < D; ++d) m = fmax(m, cabs2(c[d][i]));
         loc[i] = warp_max(m);
       }
       if (lane == 0) {
@@ -283,6 +299,7 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
       for (int i = 0; i < P; ++i) {
         double m = red[i];
         for (int w = 1; w < NW; ++w) m = fmax(m, red[w * P + i]);
+        m = sqrt(m);
         double safe = m > 0.0 ? m : 1.0;
         double inv = 1.0 / safe;
 #pragma unroll
@@ -400,7 +417,7 @@ int launch_t(const LeafArgs& a, int nsys, cudaStream_t st) {
     return 2;
   }
   size_t smem = sizeof(cplx) * (2 * P + 2 * NW * P + 2 * (size_t)P * P * a.M) +
-                sizeof(double) * NW * P + sizeof(int2) * 2 * (size_t)a.K;
+                sizeof(double) * NW * P + sizeof(int2) * 2 * (size_t)a.K + 4 * sizeof(int);
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(leaf_kernel<P, D, TPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
