@@ -120,6 +120,14 @@ int tr_assemble(const tr_desc* d, const double* T_gen, const double* L_gen, cons
                 const double* beta_sq, const double* rhs, int32_t rhs_is_normal,
                 double* weights_out, void* stream);
 
+/* One leaf sweep ~ tanint._Engine._serial_leaf (:395-434): the
+ * `leaf_index`-th leaf of the plan on device weights [N][rows][p] with the
+ * degree ledger col_degrees[p] (host, in/out).  basis_out (device) receives
+ * the normalised p x p x cap coefficient cube (cap >= conditions + 1). */
+int tr_leaf(const tr_desc* d, const double* weights, int64_t leaf_index, int64_t* col_degrees,
+            double* basis_out, int64_t cap, int32_t* ndeferred, double* self_residual,
+            int32_t* attempts, void* stream);
+
 /* Last error message of the calling thread. */
 const char* tr_last_error(void);
 

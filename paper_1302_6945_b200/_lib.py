@@ -65,6 +65,8 @@ SIGNATURES = {
     "tr_grid_eval": (C.c_int, [_P, _I64, _I64, _I64, _I64, _I64, _P, _P]),
     "tr_matpoly_mul": (C.c_int, [_P, _I64, _P, _I64, _I32, _P, _P]),
     "tr_assemble": (C.c_int, [C.POINTER(TrDesc), _P, _P, _P, _P, _P, _I32, _P, _P]),
+    "tr_leaf": (C.c_int, [C.POINTER(TrDesc), _P, _I64, C.POINTER(_I64), _P, _I64,
+                          C.POINTER(_I32), C.POINTER(C.c_double), C.POINTER(_I32), _P]),
     "tr_last_error": (C.c_char_p, []),
 }
 

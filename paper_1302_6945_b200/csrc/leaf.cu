@@ -17,7 +17,16 @@
 //    skipped on deferred ones), normalisation, the self-residual check
 //    (here by coset fold + DFT rather than powers) and the retry orders are
 //    the reference's.
+#include <stdlib.h>
+
 #include "leaf.cuh"
+#include "leaf_split.cuh"
+
+#define TR_TRY_LEAF(expr) \
+  do {                    \
+    int _rc = (expr);     \
+    if (_rc) return _rc;  \
+  } while (0)
 
 namespace {
 
@@ -125,7 +134,8 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* phib = reinterpret_cast<cplx*>(smem_raw);        // [2][P]
   cplx* halo = phib + 2 * P;                              // [2][NW][P]
-  cplx* gbuf = halo + 2 * NW * P;                         // [P*P][M]
+  cplx* sigb = halo + 2 * NW * P;                         // [2] node of condition t
+  cplx* gbuf = sigb + 2;                                  // [P*P][M]
   cplx* bvb = gbuf + P * P * a.M;                         // [P*P][M]
   double* red = reinterpret_cast<double*>(bvb + P * P * a.M);  // [NW][P]
   int2* dcur = reinterpret_cast<int2*>(red + NW * P);     // [K]
@@ -133,6 +143,7 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
   int* pubi = reinterpret_cast<int*>(dbest + a.K);        // [2] pivot, [2] deferral flag
 
   const int sys = blockIdx.x;
+  if (a.only && a.only[sys] != -2) return;  // exact fallback for flagged systems only
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int krow = tid / TPR, u = tid % TPR;
@@ -193,7 +204,10 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
 #pragma unroll
       for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
     }
-    if (tid == 0) pivot_publish<P>(r, cd, a.thr, phib, pubi, pubi + 2);
+    if (tid == 0) {
+      pivot_publish<P>(r, cd, a.thr, phib, pubi, pubi + 2);
+      sigb[0] = sig_s;
+    }
     if (lane == 31) {
 #pragma unroll
       for (int i = 0; i < P; ++i) halo[warp * P + i] = c[D - 1][i];
@@ -206,11 +220,12 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
       // once by the thread owning condition t (ref tanint.py:193-211)
       const int j = pubi[cur];
       const bool small = pubi[2 + cur] != 0;
-      const int pos_t = leaf_perm(t / rows, ostr, orev, count);
-      const long long node_t = leaf_node(a, pos_t);
-      const cplx sig_t = __ldg(&a.twN[node_t]);
+      const cplx sig_t = sigb[cur];
       if (small) {
-        if (tid == 0) dcur[ndef] = make_int2((int)node_t, t % rows);
+        if (tid == 0) {
+          const long long node_t = leaf_node(a, leaf_perm(t / rows, ostr, orev, count));
+          dcur[ndef] = make_int2((int)node_t, t % rows);
+        }
         ++ndef;
       } else {
         cplx mu[P];
@@ -270,7 +285,10 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
       }
       // the owner of condition t+1 decides its pivot; publish the warp's
       // top coefficients for the next shift
-      if (owner && tid == t + 1) pivot_publish<P>(r, cd, a.thr, phib + nxt * P, pubi + nxt, pubi + 2 + nxt);
+      if (owner && tid == t + 1) {
+        pivot_publish<P>(r, cd, a.thr, phib + nxt * P, pubi + nxt, pubi + 2 + nxt);
+        sigb[nxt] = sig_s;
+      }
       if (lane == 31) {
 #pragma unroll
         for (int i = 0; i < P; ++i) halo[(nxt * NW + warp) * P + i] = c[D - 1][i];
@@ -416,7 +434,7 @@ int launch_t(const LeafArgs& a, int nsys, cudaStream_t st) {
     tr_set_error("leaf of %d conditions does not fit the P=%d kernel", a.K, P);
     return 2;
   }
-  size_t smem = sizeof(cplx) * (2 * P + 2 * NW * P + 2 * (size_t)P * P * a.M) +
+  size_t smem = sizeof(cplx) * (2 * P + 2 * NW * P + 2 + 2 * (size_t)P * P * a.M) +
                 sizeof(double) * NW * P + sizeof(int2) * 2 * (size_t)a.K + 4 * sizeof(int);
   static bool set = false;
   if (!set) {
@@ -440,8 +458,16 @@ bool leaf_supported(int P, int K) {
   return false;
 }
 
-int leaf_launch(const LeafArgs& a, int nsys, cudaStream_t st) {
+int leaf_launch(const LeafArgs& a_in, int nsys, cudaStream_t st, const SplitState* split) {
   if (nsys <= 0) return 0;
+  // TR_LEAF_MODE=exact forces the coupled kernel everywhere (diagnostic)
+  static const char* mode = getenv("TR_LEAF_MODE");
+  const bool exact_only = mode && mode[0] == 'e';
+  LeafArgs a = a_in;
+  if (split && !exact_only && leaf_split_supported(a)) {
+    TR_TRY_LEAF(leaf_split_launch(a, *split, nsys, st));
+    a.only = split->need;  // re-run leaves whose rescale speculation failed
+  }
   int rc;
   if (a.P == 5) rc = launch_t<5, 3, 96>(a, nsys, st);
   else if (a.P == 7) rc = launch_t<7, 4, 64>(a, nsys, st);

@@ -38,9 +38,13 @@ struct LeafArgs {
   int* status;          // [sys]
   double* res_out;      // [sys] best self residual (diagnostic), may be null
   int* len_out;         // [sys] basis length (diagnostic), may be null
+  long long* dbg = nullptr;  // [sys][16] clock64 trace (diagnostic), may be null
+  const int* only = nullptr; // when set: only systems with only[sys] == -2 run (exact fallback)
 };
 
-// Launch the register-resident sweep for every system of the batch.
-int leaf_launch(const LeafArgs& a, int nsys, cudaStream_t st);
+struct SplitState;
+// Launch the leaf sweep for every system of the batch (split kernels when a
+// SplitState is given and the shape fits, else the exact coupled kernel).
+int leaf_launch(const LeafArgs& a, int nsys, cudaStream_t st, const SplitState* split = nullptr);
 // Whether a (P, K) leaf fits the register kernels.
 bool leaf_supported(int P, int K);

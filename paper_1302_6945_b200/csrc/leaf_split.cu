@@ -1,0 +1,542 @@
+// Split leaf sweep: pivot chain -> basis replay -> self-check, per attempt.
+//
+// The reference absorbs a leaf's K conditions one at a time (ref:
+// pkg/src/toepreg/tanint.py:189-217 _serial_core).  The decisions it takes
+// (pivot column, deferral, mu) depend on the basis only through the residual
+// rows r_s = w_s . B(sigma_s), which obey r_i += mu_i r_j, r_j *= (sigma_s -
+// sigma_t) at every absorbed step.  So one attempt splits into:
+//
+//   A  leaf_pivot_kernel   the sequential chain on residual rows only (a few
+//                          warps, one __syncthreads per step), writing the
+//                          per-step log (pivot j_t or -1, mu_t) to HBM;
+//   B  leaf_build_kernel   replays the log on the P x P x (K+1) coefficient
+//                          cube held in registers (no decisions left), then
+//                          normalises and writes the basis;
+//   C  leaf_check_kernel   the reference's self-residual check (coset fold +
+//                          DFT), best-attempt bookkeeping and the decision to
+//                          retry with the next absorption order (ref :395-434).
+//
+// The reference's mid-sweep rescale (columns above 1e8, every 8th listed
+// condition, ref :214-217) changes later decisions, so A assumes it does not
+// fire and B verifies that no coefficient ever exceeded the trigger at a
+// check point; a leaf that violates it is re-run by the exact coupled kernel
+// (leaf.cu).  Attempts are rounds: systems that passed exit immediately.
+#include "leaf.cuh"
+#include "leaf_split.cuh"
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr double RESCALE_TRIGGER = 1e8;
+constexpr int RESCALE_PERIOD = 8;
+
+TR_D long long node_of(const LeafArgs& a, int p) {
+  if (a.noff == 1) return a.o0 + a.stride * (long long)p;
+  return ((p & 1) ? a.o1 : a.o0) + a.stride * (long long)(p >> 1);
+}
+TR_D int perm_of(int i, int s, int rev, int count) {
+  if (rev) i = count - 1 - i;
+  return (int)(((unsigned)i * (unsigned)s) % (unsigned)count);
+}
+TR_D long long cond_node(const LeafArgs& a, int s, int att) {
+  return node_of(a, perm_of(s / a.rows, a.ord_stride[att], a.ord_reverse[att], a.count));
+}
+TR_D double wmax(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+
+// ref tanint.py:193-211 on squared moduli; returns pivot or -1 (deferred)
+template <int P>
+TR_D int decide(const cplx (&phi)[P], const int (&cd)[P], double thr, cplx* mu_out) {
+  double a2[P], amax2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    a2[i] = cabs2(phi[i]);
+    amax2 = fmax(amax2, a2[i]);
+  }
+  if (amax2 == 0.0) return -1;
+  int dmin = cd[0];
+#pragma unroll
+  for (int i = 1; i < P; ++i) dmin = min(dmin, cd[i]);
+  double bm = -1.0;
+  int j = 0;
+  cplx pj = phi[0];
+#pragma unroll
+  for (int i = 0; i < P; ++i)
+    if (cd[i] == dmin && a2[i] > bm) { bm = a2[i]; j = i; pj = phi[i]; }
+  if (bm < thr * thr * amax2) return -1;
+  const double inv2 = 1.0 / cabs2(pj);
+  const cplx inv = cmk(pj.x * inv2, -pj.y * inv2);
+#pragma unroll
+  for (int i = 0; i < P; ++i) mu_out[i] = cneg(cmul(phi[i], inv));
+  return j;
+}
+
+#define TR_SWITCH_J(P, CALL)                     \
+  switch (j) {                                   \
+    case 0: CALL(0); break;                      \
+    case 1: CALL(1); break;                      \
+    case 2: CALL(2); break;                      \
+    case 3: CALL(3); break;                      \
+    case 4: CALL(4); break;                      \
+    case 5: if constexpr (P > 5) CALL(5); break; \
+    case 6: if constexpr (P > 6) CALL(6); break; \
+    default: break;                              \
+  }
+
+template <int P, int J>
+TR_D void row_step(cplx (&r)[P], const cplx* mu, cplx dsig) {
+  const cplx rj = r[J];
+#pragma unroll
+  for (int i = 0; i < P; ++i)
+    if (i != J) r[i] = cfma(mu[i], rj, r[i]);
+  r[J] = cmul(rj, dsig);
+}
+
+// ------------------------------------------------------------------ A
+template <int P, int NW, int QMAX>
+__global__ void __launch_bounds__(NW * 32) leaf_pivot_kernel(LeafArgs a, SplitState s, int round) {
+  constexpr int NT = NW * 32;
+  const int sys = blockIdx.x;
+  if (s.need[sys] != round) return;
+  __shared__ cplx pmu[2][P];
+  __shared__ cplx psig[2];
+  __shared__ int pj[2];
+  __shared__ int nd_s;
+  const int tid = threadIdx.x;
+  const int K = a.K, rows = a.rows;
+  const int att = round;
+  const cplx* W = a.W + (long long)sys * a.w_sys;
+  const long long rowstride = (long long)rows * P;
+  cplx* mulog = s.mu + (long long)sys * s.kcap * P;
+  int* jlog = s.jl + (long long)sys * s.kcap;
+  int2* dlog = s.def_try + (long long)sys * s.kcap;
+
+  int cd[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
+  cplx r[QMAX][P];
+  cplx sg[QMAX];
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q) {
+    const int c = tid + NT * q;
+    sg[q] = cmk(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < P; ++i) r[q][i] = cmk(0.0, 0.0);
+    if (c < K) {
+      const long long node = cond_node(a, c, att);
+      sg[q] = __ldg(&a.twN[node]);
+      const cplx* wr = W + node * rowstride + (c % rows) * P;
+#pragma unroll
+      for (int i = 0; i < P; ++i) r[q][i] = wr[i];
+    }
+  }
+  if (tid == 0) {
+    nd_s = 0;
+    const int j0 = decide<P>(r[0], cd, a.thr, pmu[0]);
+    pj[0] = j0;
+    psig[0] = sg[0];
+    jlog[0] = j0;
+    if (j0 >= 0) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) mulog[i] = pmu[0][i];
+    } else {
+      dlog[0] = make_int2((int)cond_node(a, 0, att), 0);
+      nd_s = 1;
+    }
+  }
+  __syncthreads();
+  for (int t = 0; t < K; ++t) {
+    const int cur = t & 1;
+    const int j = pj[cur];
+    const int tn = t + 1;
+    if (j >= 0) {
+      const cplx sig_t = psig[cur];
+      cplx mu[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) mu[i] = pmu[cur][i];
+#pragma unroll
+      for (int i = 0; i < P; ++i) cd[i] += (i == j);
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) {
+        const int c = tid + NT * q;
+        if (c > t && c < K) {
+          const cplx dsig = csub(sg[q], sig_t);
+#define TR_R(J) row_step<P, J>(r[q], mu, dsig)
+          TR_SWITCH_J(P, TR_R)
+#undef TR_R
+        }
+      }
+    }
+    // owner of condition t+1 decides it (rows are current)
+    if (tn < K && (tn % NT) == tid) {
+      const int qo = tn / NT;
+      cplx rr[P];
+      cplx so = sg[0];
+#pragma unroll
+      for (int i = 0; i < P; ++i) rr[i] = r[0][i];
+#pragma unroll
+      for (int q = 1; q < QMAX; ++q)
+        if (q == qo) {
+#pragma unroll
+          for (int i = 0; i < P; ++i) rr[i] = r[q][i];
+          so = sg[q];
+        }
+      const int nxt = cur ^ 1;
+      const int jn = decide<P>(rr, cd, a.thr, pmu[nxt]);
+      pj[nxt] = jn;
+      psig[nxt] = so;
+      jlog[tn] = jn;
+      if (jn >= 0) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) mulog[(long long)tn * P + i] = pmu[nxt][i];
+      } else {
+        dlog[nd_s] = make_int2((int)cond_node(a, tn, att), tn % rows);
+        nd_s += 1;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    s.ndef_try[sys] = nd_s;
+    int len = 1;
+    for (int t = 0; t < K; ++t) len += jlog[t] >= 0;
+    s.len_try[sys] = len;
+  }
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cd[i];
+  }
+}
+
+// ------------------------------------------------------------------ B
+template <int P, int D, int J>
+TR_D void basis_step(cplx (&c)[D][P], const cplx* mu_s, cplx msig, cplx up) {
+  cplx oj[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) oj[d] = c[d][J];
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    if (i == J) continue;
+    const cplx m = mu_s[i];
+#pragma unroll
+    for (int d = 0; d < D; ++d) c[d][i] = cfma(m, oj[d], c[d][i]);
+  }
+#pragma unroll
+  for (int d = 0; d < D; ++d) c[d][J] = cfma(msig, oj[d], d > 0 ? oj[d - 1] : up);
+}
+
+template <int P, int D>
+TR_D cplx pick_top(const cplx (&c)[D][P], int j) {
+  cplx v = c[D - 1][0];
+#pragma unroll
+  for (int i = 1; i < P; ++i)
+    if (j == i) v = c[D - 1][i];
+  return v;
+}
+
+template <int P, int D, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) leaf_build_kernel(LeafArgs a, SplitState s, int round,
+                                                             int TPR) {
+  const int sys = blockIdx.x;
+  if (s.need[sys] != round) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = a.K;
+  const int NT = blockDim.x, NW = NT / 32;
+  cplx* musm = reinterpret_cast<cplx*>(smem_raw);  // [K][P]
+  cplx* sgsm = musm + (size_t)K * P;               // [K]
+  cplx* halo = sgsm + K;                           // [2][NW][P]
+  double* red = reinterpret_cast<double*>(halo + 2 * NW * P);  // [NW][P]
+  int* jsm = reinterpret_cast<int*>(red + NW * P); // [K]
+  int* viol = jsm + K;                             // [1]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int krow = tid / TPR, u = tid % TPR;
+  const bool brow = krow < P;
+  const int att = round;
+  const cplx* mulog = s.mu + (long long)sys * s.kcap * P;
+  const int* jlog = s.jl + (long long)sys * s.kcap;
+  for (int e = tid; e < K; e += NT) {
+    const int j = jlog[e];
+    jsm[e] = j;
+    sgsm[e] = __ldg(&a.twN[cond_node(a, e, att)]);
+    if (j >= 0)
+#pragma unroll
+      for (int i = 0; i < P; ++i) musm[e * P + i] = mulog[(long long)e * P + i];
+  }
+  if (tid == 0) *viol = 0;
+  cplx c[D][P];
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      c[d][i] = (brow && u * D + d == 0 && i == krow) ? cmk(1.0, 0.0) : cmk(0.0, 0.0);
+  if (lane == 31) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) halo[warp * P + i] = c[D - 1][i];
+  }
+  __syncthreads();
+  int len = 1;
+  int cur = 0;
+  bool big = false;
+  for (int t = 0; t < K; ++t) {
+    const int j = jsm[t];
+    if (j < 0) continue;  // deferred: nothing changes (uniform branch)
+    const cplx* mu_s = musm + t * P;
+    const cplx msig = cneg(sgsm[t]);
+    const cplx mytop = pick_top<P, D>(c, j);
+    cplx up;
+    up.x = __shfl_up_sync(FULL, mytop.x, 1);
+    up.y = __shfl_up_sync(FULL, mytop.y, 1);
+    if (lane == 0 && warp > 0) up = halo[(cur * NW + warp - 1) * P + j];
+    if (u == 0) up = cmk(0.0, 0.0);
+    if (brow && u * D <= len) {
+#define TR_B(J) basis_step<P, D, J>(c, mu_s, msig, up)
+      TR_SWITCH_J(P, TR_B)
+#undef TR_B
+    }
+    ++len;
+    if (((t + 1) % RESCALE_PERIOD) == 0) {
+      // speculation check: the reference would rescale when any coefficient
+      // of a column exceeds the trigger at this point
+#pragma unroll
+      for (int d = 0; d < D; ++d)
+#pragma unroll
+        for (int i = 0; i < P; ++i) big |= cabs2(c[d][i]) > RESCALE_TRIGGER * RESCALE_TRIGGER;
+    }
+    cur ^= 1;
+    if (lane == 31) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) halo[(cur * NW + warp) * P + i] = c[D - 1][i];
+    }
+    __syncthreads();
+  }
+  if (big) *viol = 1;
+  // normalize columns (ref tanint.py:179-183)
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    double m = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) m = fmax(m, cabs2(c[d][i]));
+    m = wmax(m);
+    if (lane == 0) red[warp * P + i] = m;
+  }
+  __syncthreads();
+  double factor = 1.0;
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    double m = 0.0;
+    for (int w = 0; w < NW; ++w) m = fmax(m, red[w * P + i]);
+    m = sqrt(m);
+    const double safe = m > 0.0 ? m : 1.0;
+    const double inv = 1.0 / safe;
+#pragma unroll
+    for (int d = 0; d < D; ++d) c[d][i] = cscale(c[d][i], inv);
+    factor = fmax(factor, safe);
+  }
+  cplx* dst = (round == 0 ? a.out : a.scratch) + (long long)sys * a.out_sys;
+  if (brow) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int l = u * D + d;
+      if (l < a.cap) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) dst[(long long)(krow * P + i) * a.cap + l] = c[d][i];
+      }
+    }
+  }
+  const int covered = TPR * D;
+  if (a.cap > covered) {
+    const int tail = a.cap - covered;
+    for (long long e = tid; e < (long long)P * P * tail; e += NT)
+      dst[(e / tail) * a.cap + covered + e % tail] = cmk(0.0, 0.0);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    s.factor_try[sys] = factor;
+    s.viol[sys] = *viol;
+  }
+}
+
+// ------------------------------------------------------------------ C
+constexpr int CK = 256;
+
+template <int P>
+__global__ void __launch_bounds__(CK) leaf_check_kernel(LeafArgs a, SplitState s, int round) {
+  const int sys = blockIdx.x;
+  if (s.need[sys] != round) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int M = a.M, rows = a.rows, K = a.K;
+  cplx* wtab = reinterpret_cast<cplx*>(smem_raw);  // [M]
+  cplx* gbuf = wtab + M;                           // [P*P][M]
+  cplx* bvb = gbuf + P * P * M;                    // [P*P][M]
+  __shared__ double red[CK / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const cplx* W = a.W + (long long)sys * a.w_sys;
+  const long long rowstride = (long long)rows * P;
+  const cplx* src = (round == 0 ? a.out : a.scratch) + (long long)sys * a.out_sys;
+  const int len = s.len_try[sys];
+  for (int e = tid; e < M; e += CK) wtab[e] = __ldg(&a.twN[(long long)e * a.stride]);
+  // scale = max |w_in| over the leaf's conditions
+  double sc = 0.0;
+  for (int e = tid; e < K * P; e += CK) {
+    const int pos = e / (rows * P), rem = e % (rows * P);
+    sc = fmax(sc, cabs2(W[node_of(a, pos) * rowstride + rem]));
+  }
+  sc = wmax(sc);
+  if (lane == 0) red[warp] = sc;
+  __syncthreads();
+  double scale = 0.0;
+  for (int w = 0; w < CK / 32; ++w) scale = fmax(scale, red[w]);
+  scale = sqrt(scale);
+  __syncthreads();
+  double resm = 0.0;
+  for (int cs = 0; cs < a.noff; ++cs) {
+    const long long oc = cs ? a.o1 : a.o0;
+    for (int e = tid; e < P * P * M; e += CK) {
+      const int ee = e / M, q = e % M;
+      cplx acc = cmk(0.0, 0.0);
+      for (int l = q; l < len; l += M)
+        acc = cfma(src[(long long)ee * a.cap + l], __ldg(&a.twN[(oc * l) % a.N]), acc);
+      gbuf[ee * M + q] = acc;
+    }
+    __syncthreads();
+    for (int e = tid; e < P * P * M; e += CK) {
+      const int ee = e / M, tt = e % M;
+      const cplx* g = gbuf + ee * M;
+      cplx acc = cmk(0.0, 0.0);
+      int k = 0;
+      for (int q = 0; q < M; ++q) {
+        acc = cfma(g[q], wtab[k], acc);
+        k += tt;
+        if (k >= M) k -= M;
+      }
+      bvb[ee * M + tt] = acc;
+    }
+    __syncthreads();
+    for (int e = tid; e < M * rows * P; e += CK) {
+      const int tt = e / (rows * P), rem = e % (rows * P);
+      const int rr = rem / P, jj = rem % P;
+      const cplx* wrow = W + (oc + a.stride * (long long)tt) * rowstride + rr * P;
+      cplx acc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc = cfma(wrow[i], bvb[(i * P + jj) * M + tt], acc);
+      resm = fmax(resm, cabs2(acc));
+    }
+    __syncthreads();
+  }
+  resm = wmax(resm);
+  if (lane == 0) red[warp] = resm;
+  __syncthreads();
+  double res = 0.0;
+  for (int w = 0; w < CK / 32; ++w) res = fmax(res, red[w]);
+  res = (scale == 0.0) ? 0.0 : sqrt(res) / scale;
+  const bool better = round == 0 || res < s.res_best[sys];
+  const int nd = s.ndef_try[sys];
+  if (better) {
+    if (round > 0) {
+      cplx* o = a.out + (long long)sys * a.out_sys;
+      for (long long e = tid; e < (long long)P * P * a.cap; e += CK) o[e] = src[e];
+    }
+    int2* db = s.def_best + (long long)sys * s.kcap;
+    const int2* dt = s.def_try + (long long)sys * s.kcap;
+    for (int e = tid; e < nd; e += CK) db[e] = dt[e];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (better) {
+      s.res_best[sys] = res;
+      s.ndef_best[sys] = nd;
+      s.factor_best[sys] = s.factor_try[sys];
+      s.len_best[sys] = s.len_try[sys];
+      for (int i = 0; i < P; ++i) s.cd_best[sys * 8 + i] = s.cd_try[sys * 8 + i];
+    }
+    const bool done = s.res_best[sys] <= a.check_tol || round + 1 >= a.nattempts;
+    if (s.viol[sys]) {
+      s.need[sys] = SPLIT_EXACT;  // speculation failed: exact coupled kernel
+    } else if (!done) {
+      s.need[sys] = round + 1;
+    } else {
+      // commit (ref tanint.py:430-434)
+      for (int i = 0; i < P; ++i) a.cd[sys * 8 + i] = s.cd_best[sys * 8 + i];
+      const int base = a.dcount[sys];
+      const int nb = s.ndef_best[sys];
+      const int room = a.dmax - base;
+      const int nput = nb < room ? nb : room;
+      const int2* db = s.def_best + (long long)sys * s.kcap;
+      for (int e = 0; e < nput; ++e) a.defer[(long long)sys * a.dmax + base + e] = db[e];
+      a.dcount[sys] = base + nb;
+      if (nb > room) a.status[sys] = 5;
+      a.max_scale[sys] = fmax(a.max_scale[sys], s.factor_best[sys]);
+      if (round > 0) a.retried[sys] += 1;
+      if (a.res_out) a.res_out[sys] = s.res_best[sys];
+      if (a.len_out) a.len_out[sys] = s.len_best[sys];
+      s.need[sys] = SPLIT_DONE;
+    }
+  }
+}
+
+__global__ void need_reset_kernel(int* need, int nsys) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nsys) need[i] = 0;
+}
+
+template <int P, int D, int MAXT>
+int launch_build(const LeafArgs& a, const SplitState& s, int round, int nsys, cudaStream_t st) {
+  const int TPR = (a.K + 1 + D - 1) / D;
+  const int NB = P * TPR, NT = (NB + 31) & ~31;
+  if (NT > MAXT) return -1;
+  const int NW = NT / 32;
+  size_t smem = sizeof(cplx) * ((size_t)a.K * P + a.K + 2 * (size_t)NW * P) +
+                sizeof(double) * NW * P + sizeof(int) * (a.K + 1);
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(leaf_build_kernel<P, D, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         160 * 1024);
+    set = true;
+  }
+  leaf_build_kernel<P, D, MAXT><<<nsys, NT, smem, st>>>(a, s, round, TPR);
+  return 0;
+}
+
+}  // namespace
+
+// basis builder shapes: P=5 -> D=3 (<= 480 threads), P=7 -> D=4 (<= 352)
+bool leaf_split_supported(const LeafArgs& a) {
+  const size_t csm = sizeof(cplx) * ((size_t)a.M + 2 * (size_t)a.P * a.P * a.M);
+  if (csm > 200 * 1024) return false;
+  if (a.P == 5) return a.K + 1 <= 96 * 3 && a.K <= 4 * 32 * 2;
+  if (a.P == 7) return a.K + 1 <= 50 * 4 && a.K <= 4 * 32 * 2;
+  return false;
+}
+
+int leaf_split_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t st) {
+  need_reset_kernel<<<(nsys + 255) / 256, 256, 0, st>>>(s.need, nsys);
+  const size_t csm = sizeof(cplx) * ((size_t)a.M + 2 * (size_t)a.P * a.P * a.M);
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(leaf_check_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(leaf_check_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    set = true;
+  }
+  for (int round = 0; round < a.nattempts; ++round) {
+    int rc;
+    if (a.P == 5) {
+      leaf_pivot_kernel<5, 4, 2><<<nsys, 128, 0, st>>>(a, s, round);
+      rc = launch_build<5, 3, 480>(a, s, round, nsys, st);
+      if (!rc) leaf_check_kernel<5><<<nsys, CK, csm, st>>>(a, s, round);
+    } else {
+      leaf_pivot_kernel<7, 4, 2><<<nsys, 128, 0, st>>>(a, s, round);
+      rc = launch_build<7, 4, 352>(a, s, round, nsys, st);
+      if (!rc) leaf_check_kernel<7><<<nsys, CK, csm, st>>>(a, s, round);
+    }
+    if (rc) {
+      tr_set_error("leaf split shape unsupported (K=%d, P=%d)", a.K, a.P);
+      return 2;
+    }
+  }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}

@@ -1,0 +1,27 @@
+// Split leaf sweep (pivot chain / basis replay / check), see leaf_split.cu.
+#pragma once
+#include "leaf.cuh"
+
+enum { SPLIT_DONE = -1, SPLIT_EXACT = -2 };
+
+struct SplitState {
+  int* need;           // [sys] round the system is waiting for, DONE or EXACT
+  int kcap;            // >= conditions per leaf
+  cplx* mu;            // [sys][kcap][P] per-step multipliers
+  int* jl;             // [sys][kcap] per-step pivot (-1 = deferred)
+  int2* def_try;       // [sys][kcap]
+  int2* def_best;      // [sys][kcap]
+  int* ndef_try;
+  int* ndef_best;
+  int* len_try;
+  int* len_best;
+  int* cd_try;         // [sys][8]
+  int* cd_best;        // [sys][8]
+  double* factor_try;
+  double* factor_best;
+  double* res_best;
+  int* viol;           // [sys] rescale speculation violated
+};
+
+bool leaf_split_supported(const LeafArgs& a);
+int leaf_split_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t st);

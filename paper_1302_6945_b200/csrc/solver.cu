@@ -25,6 +25,7 @@
 #include "fft.cuh"
 #include "kernels.cuh"
 #include "leaf.cuh"
+#include "leaf_split.cuh"
 
 // ------------------------------------------------------------ error state
 static thread_local std::string g_err;
@@ -356,6 +357,7 @@ struct WS {
   double *max_scale, *partial, *nrm, *res_out;
   int* len_out;
   cplx* clean_tmp;
+  SplitState split;
 };
 
 size_t layout(const Plan& p, long long nsys, char* base, WS* w) {
@@ -400,6 +402,25 @@ size_t layout(const Plan& p, long long nsys, char* base, WS* w) {
   w->partial = c.take<double>((size_t)nsys * NORM_CHUNKS);
   w->nrm = c.take<double>((size_t)nsys * 2);
   w->clean_tmp = c.take<cplx>((size_t)nsys * p.P * p.slot_cap[p.root_slot]);
+  // split-leaf state (pivot logs and best-attempt bookkeeping)
+  const int kcap = (int)std::max<long long>(p.Kmax, 1);
+  SplitState& s = w->split;
+  s.kcap = kcap;
+  s.need = c.take<int>((size_t)nsys);
+  s.mu = c.take<cplx>((size_t)nsys * kcap * p.P);
+  s.jl = c.take<int>((size_t)nsys * kcap);
+  s.def_try = c.take<int2>((size_t)nsys * kcap);
+  s.def_best = c.take<int2>((size_t)nsys * kcap);
+  s.ndef_try = c.take<int>((size_t)nsys);
+  s.ndef_best = c.take<int>((size_t)nsys);
+  s.len_try = c.take<int>((size_t)nsys);
+  s.len_best = c.take<int>((size_t)nsys);
+  s.cd_try = c.take<int>((size_t)nsys * 8);
+  s.cd_best = c.take<int>((size_t)nsys * 8);
+  s.factor_try = c.take<double>((size_t)nsys);
+  s.factor_best = c.take<double>((size_t)nsys);
+  s.res_best = c.take<double>((size_t)nsys);
+  s.viol = c.take<int>((size_t)nsys);
   return c.off + 256;
 }
 
@@ -582,6 +603,7 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
 
   // ---- stage 3: the tree ----
   const long long w_sys = N * rows * P;
+  long long leaf_no = 0;
   for (const Op& op : p.ops) {
     if (op.kind == OP_LEAF) {
       LeafArgs la;
@@ -618,7 +640,33 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
       la.status = w.status;
       la.res_out = w.res_out;
       la.len_out = w.len_out;
-      TR_TRY(leaf_launch(la, (int)nsys, st));
+      // TR_LEAF_TRACE=<file>: per-leaf clock64 traces of every CTA (diagnostic)
+      static const char* trace_path = getenv("TR_LEAF_TRACE");
+      static long long* trace_buf = nullptr;
+      static long long trace_cap = 0;
+      if (trace_path) {
+        long long need = (long long)p.leaves * nsys * 16;
+        if (need > trace_cap) {
+          if (trace_buf) cudaFree(trace_buf);
+          TR_CUDA_CHECK(cudaMalloc(&trace_buf, sizeof(long long) * need));
+          trace_cap = need;
+        }
+        la.dbg = trace_buf + leaf_no * nsys * 16;
+        TR_CUDA_CHECK(cudaMemsetAsync(la.dbg, 0, sizeof(long long) * nsys * 16, st));
+      }
+      TR_TRY(leaf_launch(la, (int)nsys, st, &w.split));
+      ++leaf_no;
+      if (trace_path && leaf_no == p.leaves) {
+        std::vector<long long> h((size_t)p.leaves * nsys * 16);
+        TR_CUDA_CHECK(cudaMemcpyAsync(h.data(), trace_buf, sizeof(long long) * h.size(),
+                                      cudaMemcpyDeviceToHost, st));
+        TR_CUDA_CHECK(cudaStreamSynchronize(st));
+        FILE* f = fopen(trace_path, "wb");
+        if (f) {
+          fwrite(h.data(), sizeof(long long), h.size(), f);
+          fclose(f);
+        }
+      }
     } else if (op.kind == OP_UPDATE) {
       long long cnt = N / op.stride;
       long long scap = p.slot_cap[op.slot_a];
@@ -928,6 +976,98 @@ extern "C" int tr_matpoly_mul(const double* a, int64_t la, const double* b, int6
   cudaStreamSynchronize(st);
   cudaFree(buf);
   return rc;
+}
+
+// One leaf sweep (the `leaf_index`-th leaf of the plan) on caller-provided
+// weights [N][rows][P] (device) and degree ledger (host, in/out): the stage
+// the reference runs in _serial_leaf (ref tanint.py:395-434).
+extern "C" int tr_leaf(const tr_desc* d, const double* weights, int64_t leaf_index,
+                       int64_t* col_degrees, double* basis_out, int64_t cap, int32_t* ndeferred,
+                       double* self_residual, int32_t* attempts, void* stream) {
+  Plan* p;
+  TR_TRY(get_plan(d, &p));
+  TR_TRY(ensure_fft(p));
+  const Op* op = nullptr;
+  long long li = 0;
+  for (const Op& o : p->ops)
+    if (o.kind == OP_LEAF && li++ == leaf_index) { op = &o; break; }
+  if (!op) { tr_set_error("no leaf %lld", (long long)leaf_index); return 2; }
+  if (cap < op->K + 1) { tr_set_error("cap must be >= %d", op->K + 1); return 2; }
+  const int P = p->P;
+  char* buf = nullptr;
+  size_t bytes = sizeof(cplx) * (size_t)P * P * cap + 4096 + sizeof(int2) * DMAX;
+  TR_CUDA_CHECK(cudaMalloc(&buf, bytes));
+  cplx* scratch = reinterpret_cast<cplx*>(buf);
+  int* ints = reinterpret_cast<int*>(buf + sizeof(cplx) * (size_t)P * P * cap);
+  int *cd = ints, *dcount = ints + 8, *retried = ints + 9, *status = ints + 10, *len = ints + 11;
+  double* ms = reinterpret_cast<double*>(ints + 16);
+  double* res = ms + 1;
+  int2* defer = reinterpret_cast<int2*>(ints + 64);
+  int hcd[8] = {0};
+  for (int i = 0; i < P; ++i) hcd[i] = (int)col_degrees[i];
+  int hz[8] = {0};
+  double one = 1.0;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemcpyAsync(cd, hcd, sizeof hcd, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(dcount, hz, sizeof(int) * 4, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(ms, &one, sizeof(double), cudaMemcpyHostToDevice, st);
+  LeafArgs la;
+  la.W = reinterpret_cast<const cplx*>(weights);
+  la.w_sys = p->N * p->rows * P;
+  la.N = p->N;
+  la.rows = p->rows;
+  la.P = P;
+  la.o0 = op->o0;
+  la.o1 = op->o1;
+  la.noff = op->noff;
+  la.stride = op->stride;
+  la.M = op->M;
+  la.count = op->count;
+  la.K = op->K;
+  la.nattempts = op->nattempts;
+  for (int i = 0; i < 4; ++i) {
+    la.ord_stride[i] = op->ord_stride[i];
+    la.ord_reverse[i] = op->ord_rev[i];
+  }
+  la.twN = F(*p, p->N).twN;
+  la.thr = p->d.pivot_threshold;
+  la.check_tol = LEAF_CHECK_TOL;
+  la.cd = cd;
+  la.out = reinterpret_cast<cplx*>(basis_out);
+  la.out_sys = (long long)P * P * cap;
+  la.cap = (int)cap;
+  la.scratch = scratch;
+  la.defer = defer;
+  la.dcount = dcount;
+  la.dmax = DMAX;
+  la.max_scale = ms;
+  la.retried = retried;
+  la.status = status;
+  la.res_out = res;
+  la.len_out = len;
+  WS wsp;
+  char* wsbuf = nullptr;
+  const size_t wsb = layout(*p, 1, nullptr, &wsp);
+  TR_CUDA_CHECK(cudaMalloc(&wsbuf, wsb));
+  layout(*p, 1, wsbuf, &wsp);
+  int rc = leaf_launch(la, 1, st, &wsp.split);
+  cudaStreamSynchronize(st);
+  cudaFree(wsbuf);
+  int hout[4];
+  double hres = 0;
+  if (!rc) {
+    cudaMemcpyAsync(hcd, cd, sizeof hcd, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hout, dcount, sizeof hout, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&hres, res, sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) rc = 4;
+  }
+  cudaFree(buf);
+  if (rc) return rc;
+  for (int i = 0; i < P; ++i) col_degrees[i] = hcd[i];
+  if (ndeferred) *ndeferred = hout[0];
+  if (attempts) *attempts = 1 + hout[1];
+  if (self_residual) *self_residual = hres;
+  return 0;
 }
 
 extern "C" int tr_assemble(const tr_desc* d, const double* T_gen, const double* L_gen,
