@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark: FP64 Tikhonov-Toeplitz solves/sec on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c5|c1|c3|c4|c5b]
+                    [--impl ours|reference] [--refine R] [--batch B]
+
+One process per GPU (torchrun for N > 1, NCCL).  A step solves one batch of
+the config's synthetic systems per rank (weak scaling: fixed work per rank);
+with N > 1 the solutions are gathered to rank 0 inside the step (the path's
+only collective).  Default workload = BASELINE configs[1] (config 2: T 8192 x
+4096, l2 with beta = 0.1, 64 right-hand sides sharing T).
+
+Printed JSON (rank 0): the contract keys plus
+  e2e          same metric through the public API with host buffers
+               (DeviceBatch.stage -> run -> fetch, H2D/D2H inside the timing)
+  roofline     the dominant kernel class, FP64-bound, against the FP64 FMA
+               peak measured on this GPU by tr_fp64_peak()
+  kernels      per-class device time from CUDA events (separate pass)
+  cpu_baseline the oracle port of the reference, timed on this host's cores
+  clocks       nvidia-smi samples taken during the timed region
+  gpu_launches kernels this library launched inside the timed region
+`--impl reference` times the reference algorithm (oracle/toepreg_oracle.py,
+a bit-exact numpy restatement of toepreg) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import multiprocessing as mp
+import os
+import platform
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import numpy as np  # noqa: E402
+
+METRIC = "FP64 Tikhonov-Toeplitz solves/sec"
+
+
+# ---------------------------------------------------------------- workloads
+def make_workload(cfg: str, rank: int, batch: int):
+    """Raw problem dict + count for this rank (seed item = rank)."""
+    from paper_1302_6945_b200 import workloads as wl
+    if cfg == "c2":
+        raw = wl.c2_rect(nrhs=batch or 64, seed=0, item=rank)
+        return raw, raw["b"].shape[0], "c2: T 8192x4096 real (l2, beta=0.1), shared by %d RHS" % raw["b"].shape[0]
+    if cfg == "c5":
+        b = batch or 256
+        raw = wl.c5_random(n=16384, count=b, seed=0, first=rank * b)
+        return raw, b, "c5: %d independent square systems n=16384 (l2, beta=0.1)" % b
+    if cfg == "c1":
+        raw = wl.c1_blur(256, seed=0, item=rank)
+        return raw, 1, "c1: Gaussian blur n=256 (l2, lambda=1e-2)"
+    if cfg == "c4":
+        raw = wl.c4_nufft(seed=0, item=rank)
+        return raw, 1, "c4: NUFFT gramian m=8192 n=16384 (L=0.01 I)"
+    if cfg == "c5b":
+        raw = wl.c5_random(n=1 << 22, count=1, seed=0, first=rank)
+        return raw, 1, "c5b: one square system n=2^22 (l2, beta=0.1)"
+    if cfg == "c3":
+        raw = wl.c3_firstdiff(n=65536, lam=1e-2, seed=0, item=rank)
+        return raw, 1, "c3: general n=65536, first-difference L, lambda=1e-2"
+    raise SystemExit(f"unknown config {cfg}")
+
+
+def problems_from(raw, count):
+    import paper_1302_6945_b200 as tb
+    from paper_1302_6945_b200 import workloads as wl
+    if count == 1 and np.asarray(raw.get("b", raw.get("normal_rhs"))).ndim == 1:
+        return [wl.to_problem(raw, tb)]
+    return [wl.to_problem(raw, tb, i) for i in range(count)]
+
+
+# ---------------------------------------------------------------- CPU side
+def _cpu_one(args):
+    cfg, rank, batch, i = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    import toepreg_oracle as O
+    raw, count, _ = make_workload(cfg, rank, batch)
+    prob = problems_from(raw, count)[i % count]
+    t0 = time.perf_counter()
+    O.solve(prob)
+    return time.perf_counter() - t0
+
+
+def cpu_sample(cfg, batch, cores, nsolve):
+    """Solve `nsolve` of the config's systems with the oracle port in
+    `cores` processes; returns (solves/s, wall s, mean single-solve s)."""
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        singles = pool.map(_cpu_one, [(cfg, 0, batch, i) for i in range(nsolve)])
+    wall = time.perf_counter() - t0
+    return nsolve / wall, wall, statistics.mean(singles)
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--refine", type=int, default=1)
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1302_6945_b200 as tb
+    from paper_1302_6945_b200 import _lib
+    from paper_1302_6945_b200.dist import gather_solutions
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+
+    raw, count, label = make_workload(args.config, rank, args.batch)
+    probs = problems_from(raw, count)
+    cfg = tb.SolverConfig(refine=args.refine)
+    db = tb.DeviceBatch(probs, cfg).stage()
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(fetch_host=False, stage=False):
+        if stage:
+            db.stage()
+        db.run(with_diag=False)
+        if world > 1:
+            gather_solutions(db.x, count * world, dst=0)
+        if fetch_host:
+            db.x_host.copy_(db.x, non_blocking=True)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region ----
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.tr_launch_count()
+    with ClockSampler(local) as clk:
+        for a, b in evs:
+            flush.fill_(1)  # L2 flush (256 MiB write) between timed steps
+            a.record(stream)
+            step()
+            b.record(stream)
+        torch.cuda.synchronize()
+    launches = lib.tr_launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    value = count * world * args.steps / (ms_total / 1e3)
+
+    # ---- end to end through the public API with host buffers ----
+    e_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+             for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for a, b in e_evs:
+        flush.fill_(1)
+        a.record(stream)
+        step(fetch_host=True, stage=True)
+        b.record(stream)
+    torch.cuda.synchronize()
+    e_ms = sum(a.elapsed_time(b) for a, b in e_evs)
+    te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = count * world * args.steps / (float(te.item()) / 1e3)
+
+    # ---- per-kernel-class timing pass (CUDA events around each launch) ----
+    lib.tr_kernel_timing(1)
+    nk = 2
+    for _ in range(nk):
+        step()
+    torch.cuda.synchronize()
+    kst = _lib.kernel_stats()
+    lib.tr_kernel_timing(0)
+    peak = C.c_double()
+    lib.tr_fp64_peak(C.byref(peak))
+    info = tb.plan_info(probs[0], cfg)
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant class (per solve pass; refinement repeats it)
+    passes = 1 + args.refine
+    tot_k = sum(v[0] for v in kst.values()) or 1.0
+    dom = max(kst, key=lambda k: kst[k][0])
+    P = 7 if probs[0].variant == "general" else 5
+    K = info["max_leaf_conditions"]
+    leaves = info["leaves"]
+    # algorithmic FP64 work per leaf (SURVEY 8(d) counts, per system):
+    #   basis replay  8 P^2 sum_t (t+1)      = 4 P^2 K (K+1)
+    #   pivot chain   8 P  sum_t (K-1-t)     ~ 4 P K (K-1)   (+ decisions)
+    flops_leaf = {"leaf_build": 4.0 * P * P * K * (K + 1), "leaf_pivot": 4.0 * P * K * (K - 1)}
+    roof = None
+    for name in ([dom] if dom in flops_leaf else []) + ["leaf_build"]:
+        if name in flops_leaf and kst[name][0] > 0:
+            per_leaf_ms = kst[name][0] / (nk * passes * leaves)
+            flops = flops_leaf[name] * count
+            ach = flops / (per_leaf_ms * 1e-3) / 1e12
+            roof = {"kernel": name, "bound": "fp64", "achieved": ach, "peak": peak.value,
+                    "unit": "TFLOP/s", "frac": ach / peak.value if peak.value else None,
+                    "traffic": None,
+                    "peak_source": "measured FP64 FMA burst (tr_fp64_peak); MEASURED_PEAKS.json has no FP64 entry",
+                    "algorithmic_flops_per_launch": flops,
+                    "launch_ms": per_leaf_ms}
+            break
+
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "solves/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": ms_total / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128 (fp64)",
+        "data": "synthetic (seeded BASELINE-config generators, paper_1302_6945_b200/workloads.py)",
+        "config": {"workload": label, "config": args.config, "systems_per_rank": count,
+                   "order_N": info["order"], "leaves": leaves, "leaf_conditions": K,
+                   "refine": args.refine, "parallelism": f"dp{world} (systems sharded, gather x to rank 0)",
+                   "l2": "256 MiB device write between timed steps (outside the per-step events)",
+                   "timing": "CUDA events per step on the launching stream, summed; max over ranks"},
+        "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": db.h2d_bytes,
+                "d2h_bytes_per_step": db.d2h_bytes,
+                "path": "DeviceBatch.stage (pinned H2D) -> run -> x D2H"},
+        "roofline": roof,
+        "kernels": {k: {"ms_per_step": v[0] / nk, "launches_per_step": v[1] / nk,
+                        "share": v[0] / tot_k} for k, v in kst.items() if v[1]},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        nsolve = cores if args.config in ("c2", "c1") else max(1, min(cores, 2))
+        rate, wall, single = cpu_sample(args.config, args.batch, cores, nsolve)
+        out["cpu_baseline"] = {"value": rate, "unit": "solves/s", "cores": cores, "kind": "port",
+                               "sample": f"{nsolve} systems of {args.config} solved by the oracle "
+                                         f"(bit-exact numpy restatement of toepreg) in {cores} "
+                                         f"processes, {wall:.1f} s wall; 1-core mean "
+                                         f"{single:.2f} s/solve; {platform.processor() or 'x86_64'}"}
+    print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, rank):
+    """The reference algorithm (oracle port, bit-exact with toepreg) on the
+    host cores; rank 0 only."""
+    if rank != 0:
+        return
+    raw, count, label = make_workload(args.config, 0, args.batch)
+    cores = os.cpu_count() or 1
+    nsolve = cores if args.config in ("c2", "c1") else max(1, min(cores, 2))
+    for _ in range(max(args.warmup, 0)):
+        cpu_sample(args.config, args.batch, cores, nsolve)
+    t0 = time.perf_counter()
+    walls = []
+    for _ in range(args.steps):
+        _, wall, _ = cpu_sample(args.config, args.batch, cores, nsolve)
+        walls.append(wall)
+    total = time.perf_counter() - t0
+    value = nsolve * args.steps / total
+    out = {
+        "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
+        "data": "synthetic (seeded BASELINE-config generators)", "impl": "reference",
+        "config": {"workload": label, "config": args.config, "systems_per_step": nsolve},
+        "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "port",
+                         "sample": f"{nsolve} systems per step, one per process"},
+        "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -128,6 +128,15 @@ int tr_leaf(const tr_desc* d, const double* weights, int64_t leaf_index, int64_t
             double* basis_out, int64_t cap, int32_t* ndeferred, double* self_residual,
             int32_t* attempts, void* stream);
 
+/* Instrumentation: total kernel launches issued by this library; optional
+ * per-class CUDA-event timing (classes: 0 assemble, 1 fft, 2 leaf pivot
+ * chain, 3 leaf basis replay, 4 leaf self-check, 5 leaf exact, 6 coset update,
+ * 7 combine, 8 normal operator, 9 finish); measured FP64 FMA peak. */
+int64_t tr_launch_count(void);
+int tr_kernel_timing(int32_t enable);
+int tr_kernel_stats(int32_t cls, double* total_ms, int64_t* launches);
+int tr_fp64_peak(double* tflops);
+
 /* Last error message of the calling thread. */
 const char* tr_last_error(void);
 

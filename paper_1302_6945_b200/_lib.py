@@ -67,6 +67,10 @@ SIGNATURES = {
     "tr_assemble": (C.c_int, [C.POINTER(TrDesc), _P, _P, _P, _P, _P, _I32, _P, _P]),
     "tr_leaf": (C.c_int, [C.POINTER(TrDesc), _P, _I64, C.POINTER(_I64), _P, _I64,
                           C.POINTER(_I32), C.POINTER(C.c_double), C.POINTER(_I32), _P]),
+    "tr_launch_count": (C.c_int64, []),
+    "tr_kernel_timing": (C.c_int, [_I32]),
+    "tr_kernel_stats": (C.c_int, [_I32, C.POINTER(C.c_double), C.POINTER(_I64)]),
+    "tr_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
     "tr_last_error": (C.c_char_p, []),
 }
 
@@ -90,6 +94,21 @@ def load():
                 fn.argtypes = args
             _lib = lib
     return _lib
+
+
+KERNEL_CLASSES = ["assemble", "fft", "leaf_pivot", "leaf_build", "leaf_check", "leaf_exact",
+                  "update", "combine", "normal", "finish"]
+
+
+def kernel_stats():
+    """{class: (total_ms, launches)} since the last tr_kernel_timing call."""
+    lib = load()
+    out = {}
+    for i, name in enumerate(KERNEL_CLASSES):
+        ms, n = C.c_double(), C.c_int64()
+        lib.tr_kernel_stats(i, C.byref(ms), C.byref(n))
+        out[name] = (ms.value, n.value)
+    return out
 
 
 def last_error() -> str:

@@ -158,7 +158,7 @@ inline dim3 grid1(long long n, long long nsys, int threads = 256) {
 int launch_ext_seq(cplx* out, long long N, const SeqBatch& sb, int nblk, long long nsys,
                    cudaStream_t st) {
   dim3 g((unsigned)((N + 255) / 256), nblk, (unsigned)nsys);
-  ext_seq_kernel<<<g, 256, 0, st>>>(out, N, nblk, sb, nsys);
+  { TrKTimer _kt(TRK_ASSEMBLE, st); ext_seq_kernel<<<g, 256, 0, st>>>(out, N, nblk, sb, nsys); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
@@ -166,13 +166,13 @@ int launch_ext_seq(cplx* out, long long N, const SeqBatch& sb, int nblk, long lo
 int launch_emb_col(cplx* out, long long q, const SeqBatch& sb, int nfill, int nblk, long long nsys,
                    cudaStream_t st) {
   dim3 g((unsigned)((q + 255) / 256), nfill, (unsigned)nsys);
-  emb_col_kernel<<<g, 256, 0, st>>>(out, q, sb, nblk, nsys);
+  { TrKTimer _kt(TRK_ASSEMBLE, st); emb_col_kernel<<<g, 256, 0, st>>>(out, q, sb, nblk, nsys); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
 
 int launch_assemble(const AsmArgs& a, long long nsys, cudaStream_t st) {
-  assemble_weights_kernel<<<grid1(a.N, nsys), 256, 0, st>>>(a);
+  { TrKTimer _kt(TRK_ASSEMBLE, st); assemble_weights_kernel<<<grid1(a.N, nsys), 256, 0, st>>>(a); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
@@ -180,21 +180,21 @@ int launch_assemble(const AsmArgs& a, long long nsys, cudaStream_t st) {
 int launch_spec_mul(cplx* out, long long out_bs, const cplx* a, long long a_bs, const cplx* b,
                     long long b_bs, long long q, double scale, long long nsys, cudaStream_t st,
                     int conj_b) {
-  spec_mul_kernel<<<grid1(q, nsys), 256, 0, st>>>(out, out_bs, a, a_bs, b, b_bs, q, scale, conj_b);
+  { TrKTimer _kt(TRK_NORMAL, st); spec_mul_kernel<<<grid1(q, nsys), 256, 0, st>>>(out, out_bs, a, a_bs, b, b_bs, q, scale, conj_b); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
 
 int launch_mask_scale(cplx* buf, long long bs, long long q, long long keep, double scale,
                       long long nsys, cudaStream_t st) {
-  mask_scale_kernel<<<grid1(q, nsys), 256, 0, st>>>(buf, bs, q, keep, scale);
+  { TrKTimer _kt(TRK_NORMAL, st); mask_scale_kernel<<<grid1(q, nsys), 256, 0, st>>>(buf, bs, q, keep, scale); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
 
 int launch_accum(cplx* acc, long long acc_bs, const cplx* src, long long src_bs, long long n,
                  double scale, int overwrite, long long nsys, cudaStream_t st) {
-  accum_kernel<<<grid1(n, nsys), 256, 0, st>>>(acc, acc_bs, src, src_bs, n, scale, overwrite);
+  { TrKTimer _kt(TRK_NORMAL, st); accum_kernel<<<grid1(n, nsys), 256, 0, st>>>(acc, acc_bs, src, src_bs, n, scale, overwrite); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
@@ -202,7 +202,7 @@ int launch_accum(cplx* acc, long long acc_bs, const cplx* src, long long src_bs,
 int launch_residual(cplx* r, const cplx* ax, const cplx* x, const cplx* y, long long n,
                     const double* beta_sq, long long beta_bs, int add_ridge, long long nsys,
                     cudaStream_t st) {
-  residual_kernel<<<grid1(n, nsys), 256, 0, st>>>(r, ax, x, y, n, beta_sq, beta_bs, add_ridge);
+  { TrKTimer _kt(TRK_NORMAL, st); residual_kernel<<<grid1(n, nsys), 256, 0, st>>>(r, ax, x, y, n, beta_sq, beta_bs, add_ridge); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }

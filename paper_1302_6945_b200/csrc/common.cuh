@@ -74,3 +74,27 @@ TR_D double dfrom(unsigned long long b) { return __longlong_as_double((long long
   } while (0)
 
 void tr_set_error(const char* fmt, ...);
+
+// Kernel classes for launch counting and optional per-class CUDA-event timing
+// (tr_kernel_timing / tr_kernel_stats in the C ABI).
+enum {
+  TRK_ASSEMBLE = 0,
+  TRK_FFT,
+  TRK_LEAF_PIVOT,
+  TRK_LEAF_BUILD,
+  TRK_LEAF_CHECK,
+  TRK_LEAF_EXACT,
+  TRK_UPDATE,
+  TRK_COMBINE,
+  TRK_NORMAL,
+  TRK_FINISH,
+  TRK_NCLASS
+};
+void tr_kernel_begin(int cls, cudaStream_t st);
+void tr_kernel_end(int cls, cudaStream_t st);
+struct TrKTimer {
+  int cls;
+  cudaStream_t st;
+  TrKTimer(int c, cudaStream_t s) : cls(c), st(s) { tr_kernel_begin(c, s); }
+  ~TrKTimer() { tr_kernel_end(cls, st); }
+};

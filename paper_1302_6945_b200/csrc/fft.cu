@@ -413,7 +413,7 @@ static int launch_pass(const FftPlan& p, int i, const cplx* in, long long in_ls,
     cudaFuncSetAttribute(fft_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
     attr_set = true;
   }
-  fft_pass_kernel<<<grid, FFT_THREADS, smem, st>>>(a);
+  { TrKTimer _kt(TRK_FFT, st); fft_pass_kernel<<<grid, FFT_THREADS, smem, st>>>(a); }
   return 0;
 }
 

@@ -275,7 +275,7 @@ int launch_t(const FastArgs& a, cudaStream_t st) {
     set = true;
   }
   long long blocks = (a.nsub + G::TL - 1) / G::TL;
-  fft_fast_kernel<LOG2, Q><<<(unsigned)blocks, FT, smem, st>>>(a);
+  { TrKTimer _kt(TRK_FFT, st); fft_fast_kernel<LOG2, Q><<<(unsigned)blocks, FT, smem, st>>>(a); }
   return 0;
   }
 }

@@ -255,29 +255,32 @@ __global__ void add_kernel(cplx* x, const cplx* d, long long total) {
 }  // namespace
 
 int launch_cleanup(const CleanupArgs& a, long long nsys, cudaStream_t st) {
-  if (a.P == 5) cleanup_kernel<5><<<(unsigned)nsys, CT, 0, st>>>(a);
-  else cleanup_kernel<7><<<(unsigned)nsys, CT, 0, st>>>(a);
+  {
+    TrKTimer _kt(TRK_FINISH, st);
+    if (a.P == 5) cleanup_kernel<5><<<(unsigned)nsys, CT, 0, st>>>(a);
+    else cleanup_kernel<7><<<(unsigned)nsys, CT, 0, st>>>(a);
+  }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
 
 int launch_extract(const ExtractArgs& a, long long nsys, cudaStream_t st) {
-  extract_kernel<<<(unsigned)nsys, CT, 0, st>>>(a);
+  { TrKTimer _kt(TRK_FINISH, st); extract_kernel<<<(unsigned)nsys, CT, 0, st>>>(a); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
 
 int launch_norms(const cplx* v, long long n, long long nsys, double* partial, int nchunk,
                  double* out, cudaStream_t st) {
-  norm_partial_kernel<<<dim3(nchunk, (unsigned)nsys), 256, 0, st>>>(v, n, partial, nchunk);
-  norm_final_kernel<<<(unsigned)((nsys + 127) / 128), 128, 0, st>>>(partial, nchunk, out, nsys);
+  { TrKTimer _kt(TRK_NORMAL, st); norm_partial_kernel<<<dim3(nchunk, (unsigned)nsys), 256, 0, st>>>(v, n, partial, nchunk); }
+  { TrKTimer _kt(TRK_NORMAL, st); norm_final_kernel<<<(unsigned)((nsys + 127) / 128), 128, 0, st>>>(partial, nchunk, out, nsys); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
 
 int launch_add_inplace(cplx* x, const cplx* d, long long n, long long nsys, cudaStream_t st) {
   long long total = n * nsys;
-  add_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(x, d, total);
+  { TrKTimer _kt(TRK_FINISH, st); add_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(x, d, total); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }

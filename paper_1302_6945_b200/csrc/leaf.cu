@@ -446,7 +446,7 @@ int launch_t(const LeafArgs& a, int nsys, cudaStream_t st) {
     tr_set_error("leaf shared memory %zu exceeds the limit", smem);
     return 2;
   }
-  leaf_kernel<P, D, TPR><<<nsys, NT, smem, st>>>(a);
+  { TrKTimer _kt(TRK_LEAF_EXACT, st); leaf_kernel<P, D, TPR><<<nsys, NT, smem, st>>>(a); }
   return 0;
 }
 

@@ -497,7 +497,7 @@ int launch_build(const LeafArgs& a, const SplitState& s, int round, int nsys, cu
                          160 * 1024);
     set = true;
   }
-  leaf_build_kernel<P, D, MAXT><<<nsys, NT, smem, st>>>(a, s, round, TPR);
+  { TrKTimer _kt(TRK_LEAF_BUILD, st); leaf_build_kernel<P, D, MAXT><<<nsys, NT, smem, st>>>(a, s, round, TPR); }
   return 0;
 }
 
@@ -513,7 +513,7 @@ bool leaf_split_supported(const LeafArgs& a) {
 }
 
 int leaf_split_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t st) {
-  need_reset_kernel<<<(nsys + 255) / 256, 256, 0, st>>>(s.need, nsys);
+  { TrKTimer _kt(TRK_LEAF_PIVOT, st); need_reset_kernel<<<(nsys + 255) / 256, 256, 0, st>>>(s.need, nsys); }
   const size_t csm = sizeof(cplx) * ((size_t)a.M + 2 * (size_t)a.P * a.P * a.M);
   static bool set = false;
   if (!set) {
@@ -524,13 +524,13 @@ int leaf_split_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStre
   for (int round = 0; round < a.nattempts; ++round) {
     int rc;
     if (a.P == 5) {
-      leaf_pivot_kernel<5, 4, 2><<<nsys, 128, 0, st>>>(a, s, round);
+      { TrKTimer _kt(TRK_LEAF_PIVOT, st); leaf_pivot_kernel<5, 4, 2><<<nsys, 128, 0, st>>>(a, s, round); }
       rc = launch_build<5, 3, 480>(a, s, round, nsys, st);
-      if (!rc) leaf_check_kernel<5><<<nsys, CK, csm, st>>>(a, s, round);
+      { TrKTimer _kt(TRK_LEAF_CHECK, st); if (!rc) leaf_check_kernel<5><<<nsys, CK, csm, st>>>(a, s, round); }
     } else {
-      leaf_pivot_kernel<7, 4, 2><<<nsys, 128, 0, st>>>(a, s, round);
+      { TrKTimer _kt(TRK_LEAF_PIVOT, st); leaf_pivot_kernel<7, 4, 2><<<nsys, 128, 0, st>>>(a, s, round); }
       rc = launch_build<7, 4, 352>(a, s, round, nsys, st);
-      if (!rc) leaf_check_kernel<7><<<nsys, CK, csm, st>>>(a, s, round);
+      { TrKTimer _kt(TRK_LEAF_CHECK, st); if (!rc) leaf_check_kernel<7><<<nsys, CK, csm, st>>>(a, s, round); }
     }
     if (rc) {
       tr_set_error("leaf split shape unsupported (K=%d, P=%d)", a.K, a.P);

@@ -181,7 +181,7 @@ int launch_twist_fold(cplx* G, const cplx* B, long long b_sys, long long b_cap, 
                       long long o0, long long o1, int noff, long long cnt, long long N,
                       const cplx* twN, long long nsys, cudaStream_t st) {
   dim3 grid((unsigned)((cnt + 255) / 256), noff * PP, (unsigned)nsys);
-  twist_fold_kernel<<<grid, 256, 0, st>>>(G, B, b_sys, b_cap, PP, L, o0, o1, noff, cnt, N, twN);
+  { TrKTimer _kt(TRK_UPDATE, st); twist_fold_kernel<<<grid, 256, 0, st>>>(G, B, b_sys, b_cap, PP, L, o0, o1, noff, cnt, N, twN); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
@@ -191,27 +191,30 @@ int launch_apply_update(cplx* W, long long w_sys, const cplx* G, int rows, int P
                         cudaStream_t st) {
   dim3 grid((unsigned)((cnt + 127) / 128), noff, (unsigned)nsys);
   if (P == 5)
-    apply_update_kernel<5><<<grid, 128, 0, st>>>(W, w_sys, G, rows, o0, o1, noff, stride, cnt);
+    { TrKTimer _kt(TRK_UPDATE, st); apply_update_kernel<5><<<grid, 128, 0, st>>>(W, w_sys, G, rows, o0, o1, noff, stride, cnt); }
   else
-    apply_update_kernel<7><<<grid, 128, 0, st>>>(W, w_sys, G, rows, o0, o1, noff, stride, cnt);
+    { TrKTimer _kt(TRK_UPDATE, st); apply_update_kernel<7><<<grid, 128, 0, st>>>(W, w_sys, G, rows, o0, o1, noff, stride, cnt); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
 
 int launch_pointwise_matmul(cplx* FA, const cplx* FB, int P, long long R, long long nsys,
                             cudaStream_t st) {
-  if (P == 5) pointwise_matmul_kernel<5><<<g2(R, nsys, 128), 128, 0, st>>>(FA, FB, R);
-  else pointwise_matmul_kernel<7><<<g2(R, nsys, 128), 128, 0, st>>>(FA, FB, R);
+  {
+    TrKTimer _kt(TRK_COMBINE, st);
+    if (P == 5) pointwise_matmul_kernel<5><<<g2(R, nsys, 128), 128, 0, st>>>(FA, FB, R);
+    else pointwise_matmul_kernel<7><<<g2(R, nsys, 128), 128, 0, st>>>(FA, FB, R);
+  }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
 
 int launch_trim_normalize(const TrimArgs& a, long long nsys, cudaStream_t st) {
   TR_CUDA_CHECK(cudaMemsetAsync(a.red, 0, sizeof(unsigned long long) * (2 + a.P) * nsys, st));
-  trim1_kernel<<<g2(a.L, nsys), 256, 0, st>>>(a);
-  trim2_kernel<<<g2(a.L, nsys), 256, 0, st>>>(a);
-  trim3_kernel<<<g2(a.L, nsys), 256, 0, st>>>(a);
-  trim4_kernel<<<g2(a.cap, nsys), 256, 0, st>>>(a);
+  { TrKTimer _kt(TRK_COMBINE, st); trim1_kernel<<<g2(a.L, nsys), 256, 0, st>>>(a); }
+  { TrKTimer _kt(TRK_COMBINE, st); trim2_kernel<<<g2(a.L, nsys), 256, 0, st>>>(a); }
+  { TrKTimer _kt(TRK_COMBINE, st); trim3_kernel<<<g2(a.L, nsys), 256, 0, st>>>(a); }
+  { TrKTimer _kt(TRK_COMBINE, st); trim4_kernel<<<g2(a.cap, nsys), 256, 0, st>>>(a); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }

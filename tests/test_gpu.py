@@ -1,0 +1,282 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden outputs, the oracle, and exact solutions.
+
+Tolerances (relative 2-norm unless stated):
+  * accuracy default (SolverConfig.refine=1): GPU <-> exact <= 1e-12 on
+    well-conditioned fixtures (reference <-> exact <= 1e-9), hence
+    GPU <-> reference == reference <-> exact <= 1e-9; never farther from the
+    exact solution than the reference itself.
+  * single pass (refine=0, the reference's own algorithm): within 3x the
+    reference's distance to the exact solution (an FP64
+    leaf lands at ~sqrt(2) x the reference's floor).
+  * integer outputs (degree ledger, deferred count, recursion depth,
+    condition count) are exact.
+"""
+
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+import toepreg_oracle as O
+from conftest import GOLDEN, case_paths, load_case, rel
+from paper_1302_6945_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+CASES = case_paths()
+ILL = ("c4_mini",)  # the reference itself fails on this one (cond ~ 1e8)
+
+
+def _solve(tb, raw, refine):
+    return tb.solve_tikhonov(wl.to_problem(raw, tb), tb.SolverConfig(refine=refine))
+
+
+@pytest.mark.parametrize("path", CASES, ids=lambda p: os.path.basename(p)[:-4])
+def test_parity_with_reference_refined(gpu, path):
+    tb = gpu
+    raw, d = load_case(path)
+    name = os.path.basename(path)[:-4]
+    rep = _solve(tb, raw, 1)
+    ref_exact = rel(d["x_hat"], d["x_exact"])
+    gpu_exact = rel(rep.x_hat, d["x_exact"])
+    gpu_ref = rel(rep.x_hat, d["x_hat"])
+    assert sorted(rep.final_col_degrees.tolist()) == sorted(d["final_col_degrees"].tolist())
+    assert rep.diagnostics.conditions_total == int(d["conditions_total"])
+    assert rep.diagnostics.recursion_depth == int(d["recursion_depth"])
+    assert rep.x_hat.dtype == np.complex128 and rep.x_hat.shape == d["x_hat"].shape
+    assert gpu_exact <= ref_exact * 1.0001 + 1e-15, (name, gpu_exact, ref_exact)
+    if ref_exact <= 1e-9:
+        assert gpu_exact <= 1e-12, (name, gpu_exact)
+        assert gpu_ref <= 1e-9, (name, gpu_ref)
+        assert rep.relative_residual <= 1e-12
+
+
+@pytest.mark.parametrize("path", CASES, ids=lambda p: os.path.basename(p)[:-4])
+def test_single_pass_matches_reference_error_level(gpu, path):
+    tb = gpu
+    raw, d = load_case(path)
+    name = os.path.basename(path)[:-4]
+    if name in ILL:
+        pytest.skip("reference fails on this conditioning; see the refined test")
+    rep = _solve(tb, raw, 0)
+    ref_exact = rel(d["x_hat"], d["x_exact"])
+    assert rel(rep.x_hat, d["x_exact"]) <= 3 * ref_exact + 1e-13, name
+    assert np.array_equal(np.sort(rep.final_col_degrees), np.sort(d["final_col_degrees"]))
+    assert rep.diagnostics.difficult_points == int(d["difficult_points"])
+    assert rep.relative_residual <= 3 * float(d["relative_residual"]) + 1e-14
+
+
+def test_known_answers(gpu):
+    tb = gpu
+    b = np.array([4.0, 8.0, 12.0, 16.0])
+    p = tb.ProblemSpec.general(tb.identity_spec(4), tb.identity_spec(4), b)
+    assert np.allclose(tb.solve_tikhonov(p).x_hat, b / 2, atol=1e-12)
+    p = tb.ProblemSpec.l2(tb.ToeplitzSpec(1, 1, np.array([2.0])), 1.0, [10.0])
+    assert np.allclose(tb.solve_tikhonov(p).x_hat, [4.0], atol=1e-12)
+    # zero right-hand side -> zero solution
+    p = tb.ProblemSpec.l2(tb.ToeplitzSpec(4, 4, np.arange(1, 8.0)), 1.0, np.zeros(4))
+    r = tb.solve_tikhonov(p)
+    assert not r.x_hat.any() and r.relative_residual == 0.0
+
+
+def test_singular_system_raises(gpu):
+    tb = gpu
+    z = np.zeros(7)
+    p = tb.ProblemSpec.general(tb.ToeplitzSpec(4, 4, z), tb.ToeplitzSpec(4, 4, z), np.ones(4))
+    with pytest.raises(tb.SingularSystemError):
+        tb.solve_tikhonov(p)
+
+
+def test_deterministic_and_batch_invariant(gpu):
+    tb = gpu
+    raw = wl.c5_random(n=1024, count=5, seed=11)
+    probs = [wl.to_problem(raw, tb, i) for i in range(5)]
+    a = tb.solve_tikhonov_batch(probs)
+    b = tb.solve_tikhonov_batch(probs)
+    c = tb.solve_tikhonov(probs[3])
+    assert all(np.array_equal(x.x_hat, y.x_hat) for x, y in zip(a, b))
+    assert np.array_equal(a[3].x_hat, c.x_hat)
+
+
+def test_shared_operator_batch(gpu):
+    tb = gpu
+    raw = wl.c2_rect(m=1024, n=512, nrhs=6, seed=3)
+    probs = [wl.to_problem(raw, tb, i) for i in range(6)]
+    reps = tb.solve_tikhonov_batch(probs)
+    for i, r in enumerate(reps):
+        single = tb.solve_tikhonov(probs[i])
+        assert np.array_equal(r.x_hat, single.x_hat)
+        x = O.dense_solution(probs[i])
+        assert rel(r.x_hat, x) < 1e-12
+
+
+@pytest.mark.parametrize("variant", ["general", "l2", "gramian"])
+def test_small_corpus_against_dense(gpu, variant):
+    """The reference acceptance gate (ref tests/test_acceptance.py:107-113):
+    < 1e-8 vs dense for n in {4..64}."""
+    tb = gpu
+    code = {"general": 0, "l2": 1, "gramian": 2}[variant]
+    for n in (4, 8, 16, 32, 64):
+        for trial in range(4):
+            rng = np.random.default_rng(np.random.SeedSequence((8801, code, n, trial)))
+            raw = wl.random_problem(variant, n, rng)
+            for refine in (0, 1):
+                rep = _solve(tb, raw, refine)
+                x = O.dense_solution(wl.to_problem(raw, tb))
+                assert rel(rep.x_hat, x) < 1e-8
+                assert sorted(rep.final_col_degrees.tolist()) == [0] + [1] * (rep.final_col_degrees.size - 1)
+
+
+@pytest.mark.parametrize("variant", ["general", "l2", "gramian"])
+def test_planted_solution_n512(gpu, variant):
+    """ref tests/test_acceptance.py:116-122: max-abs < 1e-9 at n = 512."""
+    tb = gpu
+    rng = np.random.default_rng(np.random.SeedSequence((2024, 7, 512)))
+    raw = wl.random_problem(variant, 512, rng)
+    base = wl.to_problem(raw, tb)
+    x_true = (rng.standard_normal(512) + 1j * rng.standard_normal(512)) / np.sqrt(2.0)
+    y = O.normal_apply(base, x_true)
+    planted = tb.ProblemSpec(variant=variant, T=base.T, L=base.L, G=base.G, beta=base.beta,
+                             b=None, normal_rhs=y)
+    for refine in (0, 1):
+        rep = tb.solve_tikhonov(planted, tb.SolverConfig(refine=refine))
+        assert np.abs(rep.x_hat - x_true).max() < 1e-9
+
+
+def test_full_size_c5_properties(gpu):
+    """Size-independent checks at BASELINE config-5 size (n = 16384)."""
+    tb = gpu
+    raw = wl.c5_random(n=16384, count=3, seed=5)
+    probs = [wl.to_problem(raw, tb, i) for i in range(3)]
+    reps = tb.solve_tikhonov_batch(probs)
+    for p, r in zip(probs, reps):
+        assert r.relative_residual < 1e-13
+        assert sorted(r.final_col_degrees.tolist()) == [0, 1, 1, 1, 1]
+        # residual recomputed independently on the CPU
+        res = np.linalg.norm(O.normal_apply(p, r.x_hat) - O.normal_rhs(p))
+        assert res / np.linalg.norm(O.normal_rhs(p)) < 1e-12
+
+
+def _dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.complex128).view(np.float64).copy()).cuda()
+
+
+def test_stage_fft_against_numpy(gpu):
+    import torch
+    from paper_1302_6945_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(0)
+    for n in (1, 2, 3, 48, 64, 96, 1024, 12288, 32768, 98304, 1 << 20, 3 << 18, 1 << 21):
+        lines = max(1, min(4, (1 << 21) // n))
+        x = rng.standard_normal((lines, n)) + 1j * rng.standard_normal((lines, n))
+        dx = _dev(x)
+        out = torch.empty_like(dx)
+        for sign in (-1, 1):
+            assert lib.tr_fft(C.c_void_p(dx.data_ptr()), C.c_void_p(out.data_ptr()), n, lines, sign, None) == 0
+            got = out.cpu().numpy().view(np.complex128).reshape(lines, n)
+            ref = np.fft.fft(x, axis=-1) if sign < 0 else n * np.fft.ifft(x, axis=-1)
+            assert rel(got, ref) < 2e-15 * np.log2(max(n, 2))
+
+
+def test_stage_grid_eval_and_product(gpu):
+    import torch
+    from paper_1302_6945_b200 import _lib
+    lib = _lib.load()
+    g = np.load(os.path.join(GOLDEN, "stages", "grid_eval.npz"))
+    cube = g["cube"]
+    lines = cube.shape[0] * cube.shape[1]
+    src = _dev(cube.reshape(lines, -1))
+    for key in g.files:
+        if not key.startswith("N"):
+            continue
+        N, off, st = [int(s[1:]) for s in key.split("_")]
+        out = torch.empty((lines, N // st, 2), dtype=torch.float64, device="cuda")
+        assert lib.tr_grid_eval(C.c_void_p(src.data_ptr()), lines, cube.shape[2], N, off, st,
+                                C.c_void_p(out.data_ptr()), None) == 0
+        got = out.cpu().numpy().view(np.complex128).reshape(g[key].shape)
+        assert rel(got, g[key]) < 1e-14
+    m = np.load(os.path.join(GOLDEN, "stages", "matpoly.npz"))
+    a, b = _dev(m["a"]), _dev(m["b"])
+    L = m["a"].shape[2] + m["b"].shape[2] - 1
+    out = torch.empty((25, L, 2), dtype=torch.float64, device="cuda")
+    assert lib.tr_matpoly_mul(C.c_void_p(a.data_ptr()), m["a"].shape[2], C.c_void_p(b.data_ptr()),
+                              m["b"].shape[2], 5, C.c_void_p(out.data_ptr()), None) == 0
+    got = out.cpu().numpy().view(np.complex128).reshape(5, 5, L)
+    # the reference product is long double; FP64 FFT products carry eps*log(R) error
+    assert np.abs(got - m["ld"]).max() / np.abs(m["ld"]).max() < 1e-14
+
+
+@pytest.mark.parametrize("name", ["assemble_l2_n64", "assemble_general_n32", "assemble_gramian_n32"])
+def test_stage_assembly(gpu, name):
+    import torch
+    tb = gpu
+    from paper_1302_6945_b200 import _lib
+    lib = _lib.load()
+    a = dict(np.load(os.path.join(GOLDEN, "stages", name + ".npz")))
+    W = a["weights"]
+    rows, N, P = W.shape
+    variant = name.split("_")[1]
+    n = 64 if variant == "l2" else 32
+    pl = int(a.get("L_rows", n))
+    d = tb.solver.make_desc(variant, n, n, pl, tb.SolverConfig())
+    out = torch.zeros((N, rows, P, 2), dtype=torch.float64, device="cuda")
+    keep = {}
+    def ptr(key):
+        if key not in a:
+            return None
+        keep[key] = _dev(a[key])
+        return C.c_void_p(keep[key].data_ptr())
+    bsq = None
+    if "beta" in a:
+        keep["beta"] = torch.tensor([abs(float(a["beta"])) ** 2], dtype=torch.float64, device="cuda")
+        bsq = C.c_void_p(keep["beta"].data_ptr())
+    rhs = ptr("normal_rhs") if "normal_rhs" in a else ptr("b")
+    assert lib.tr_assemble(C.byref(d), ptr("T_gen"), ptr("L_gen"), ptr("G_col"), bsq, rhs,
+                           int("normal_rhs" in a), C.c_void_p(out.data_ptr()), None) == 0
+    got = np.transpose(out.cpu().numpy().view(np.complex128).reshape(N, rows, P), (1, 0, 2))
+    assert np.abs(got - W).max() <= 1e-12 * max(1.0, np.abs(W).max())
+
+
+@pytest.mark.parametrize("label", ["c1", "c2", "c3", "general64"])
+def test_stage_leaf_against_oracle(gpu, label):
+    """The first leaf (weights from the oracle's assembly) vs the oracle's
+    serial leaf: same degree ledger and deferrals, basis within FP64 sweep
+    noise."""
+    import torch
+    tb = gpu
+    from paper_1302_6945_b200 import _lib
+    lib = _lib.load()
+    raw = {"c1": lambda: wl.c1_blur(256),
+           "c2": lambda: wl.c2_rect(m=1024, n=512, nrhs=1),
+           "c3": lambda: wl.c3_firstdiff(n=512, lam=1e-2),
+           "general64": lambda: wl.random_problem("general", 64, np.random.default_rng(5))}[label]()
+    idx0 = 0 if np.asarray(raw.get("b", [0])).ndim == 2 else None
+    prob = wl.to_problem(raw, tb, idx0)
+    asm = O.assemble(prob)
+    v, m, n, pl = tb.solver._shape(prob)
+    d = tb.solver.make_desc(v, m, n, pl, tb.SolverConfig())
+    W = asm.weights
+    rows, N, P = W.shape
+    offsets, stride = (0,), 1
+    while rows * len(offsets) * (N // stride) > 256:
+        offsets, _, stride = O.split_rule(N, offsets, stride, True)
+    idx = O.coset_indices(N, offsets, stride)
+    K = rows * idx.size
+    degs = -asm.tau.copy()
+    coeffs, d_ref, deferred, _, _, _ = O.leaf_basis(W, asm.nodes, idx, degs.copy(), 1e-8)
+    Wd = _dev(np.transpose(W, (1, 0, 2)))
+    cd = (C.c_int64 * 8)(*([int(x) for x in degs] + [0] * (8 - P)))
+    out = torch.zeros((P * P * (K + 1) * 2,), dtype=torch.float64, device="cuda")
+    nd, att = C.c_int32(), C.c_int32()
+    rr = C.c_double()
+    assert lib.tr_leaf(C.byref(d), C.c_void_p(Wd.data_ptr()), 0, cd, C.c_void_p(out.data_ptr()),
+                       K + 1, C.byref(nd), C.byref(rr), C.byref(att), None) == 0
+    g = out.cpu().numpy().view(np.complex128).reshape(P, P, K + 1)
+    assert list(cd)[:P] == [int(x) for x in d_ref]
+    assert nd.value == len(deferred)
+    L = coeffs.shape[2]
+    assert np.abs(g[:, :, :L] - coeffs).max() <= 1e-9 * np.abs(coeffs).max()
+    assert rr.value < 1e-11

@@ -1,0 +1,62 @@
+"""Host-side API mirror: problem containers behave like the reference's
+(ref: pkg/src/toepreg/toeplitz.py:37-233) and the reference's own
+ProblemSpec objects are accepted by duck typing."""
+
+import numpy as np
+import pytest
+
+import paper_1302_6945_b200 as tb
+from paper_1302_6945_b200 import workloads as wl
+
+
+def test_toeplitz_layout_and_validation():
+    t = tb.ToeplitzSpec(2, 3, [1, 2, 3, 4])  # gen top-right -> bottom-left
+    assert t.entry(0, 2) == 1 and t.entry(0, 0) == 3 and t.entry(1, 0) == 4
+    assert t.gen.dtype == np.complex128 and not t.gen.flags.writeable
+    with pytest.raises(ValueError):
+        tb.ToeplitzSpec(2, 3, [1, 2, 3])
+    with pytest.raises(ValueError):
+        tb.ToeplitzSpec(0, 3, [])
+    a = tb.adjoint_spec(tb.ToeplitzSpec(2, 2, [1j, 2, 3]))
+    assert np.array_equal(a.gen, np.array([3, 2, -1j]))
+
+
+def test_hermitian_spec():
+    h = tb.HermitianToeplitzSpec(3, [2.0, 1 + 1j, 3j])
+    assert np.array_equal(h.full_gen, [-3j, 1 - 1j, 2, 1 + 1j, 3j])
+    with pytest.raises(ValueError):
+        tb.HermitianToeplitzSpec(2, [1j, 0])
+    with pytest.raises(ValueError):
+        tb.HermitianToeplitzSpec(3, [1, 2])
+
+
+def test_problem_constructors_validate_like_the_reference():
+    T = tb.ToeplitzSpec(3, 2, np.ones(4))
+    L = tb.ToeplitzSpec(2, 2, np.ones(3))
+    with pytest.raises(ValueError):
+        tb.ProblemSpec.general(T, tb.ToeplitzSpec(2, 3, np.ones(4)), np.ones(3))
+    with pytest.raises(ValueError):
+        tb.ProblemSpec.general(T, L, np.ones(2))
+    with pytest.raises(ValueError):
+        tb.ProblemSpec.l2(T, 0, np.ones(3))
+    with pytest.raises(ValueError):
+        tb.ProblemSpec.gramian(tb.HermitianToeplitzSpec(3, [1, 0, 0]), L, np.ones(3))
+    p = tb.ProblemSpec.l2(T, 2j, np.ones(3))
+    assert p.beta_sq == 4.0 and p.n == 2 and p.m == 3 and p.reg_rows == 2
+
+
+def test_workloads_are_seed_deterministic():
+    a = wl.c5_random(n=64, count=2, seed=7)
+    b = wl.c5_random(n=64, count=2, seed=7)
+    assert np.array_equal(a["T_gen"], b["T_gen"]) and np.array_equal(a["b"], b["b"])
+    c = wl.c2_rect(m=64, n=32, nrhs=3)
+    assert c["b"].shape == (3, 64) and c["T_gen"].shape == (95,)
+    g = wl.c4_nufft(m=32, n=64)
+    assert g["G_col"][0].imag == 0.0 and abs(g["G_col"][0] - 32) < 1e-9
+
+
+def test_reference_problem_objects_are_accepted_by_shape_logic():
+    ref = pytest.importorskip("toepreg", reason="reference package not importable here")
+    raw = wl.random_problem("general", 8, np.random.default_rng(1))
+    rp = wl.to_problem(raw, ref)
+    assert tb.solver._shape(rp) == ("general", 8, 8, 8)
