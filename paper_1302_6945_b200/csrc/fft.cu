@@ -384,7 +384,8 @@ static int launch_pass(const FftPlan& p, int i, const cplx* in, long long in_ls,
     f.twN = p.twN;
     f.twR = ps.twR;
     f.sign = sign;
-    if (fast_launch(ps.log2, ps.q, f, st) == 0) return 0;
+    const bool small = p.npass == 1 && ps.R <= 1024;
+    if (fast_launch(ps.log2, ps.q, small, f, st) == 0) return 0;
   }
   PassArgs a;
   a.n = p.n;

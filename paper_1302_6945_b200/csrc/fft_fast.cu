@@ -9,8 +9,9 @@
 
 namespace {
 
-constexpr int FT = 256;      // threads per CTA
-constexpr int TILE = 4096;   // complex values per CTA
+// large tiles: 256 threads x 16 values; small tiles (single-pass R <= 1024):
+// 128 threads x 8 values, so small batches still fill the SMs
+constexpr int TILE = 4096;
 
 __host__ __device__ constexpr int np2(int x) {
   int p = 1;
@@ -34,10 +35,12 @@ __host__ __device__ constexpr int odd_at(int q, int s) {
 __host__ __device__ constexpr int npow2st(int l) { return l / 3 + (l % 3 ? 1 : 0); }
 __host__ __device__ constexpr int pow2_at(int l, int s) { return s < l / 3 ? 8 : (l % 3 == 2 ? 4 : 2); }
 
-template <int LOG2, int Q>
+template <int LOG2, int Q, bool SM>
 struct Geo {
+  static constexpr int FT = SM ? 128 : 256;
+  static constexpr int TV = SM ? 1024 : 4096;
   static constexpr int R = Q << LOG2;
-  static constexpr int TL = np2(R) >= TILE ? 1 : (TILE / np2(R) > 256 ? 256 : TILE / np2(R));
+  static constexpr int TL = np2(R) >= TV ? 1 : (TV / np2(R) > 256 ? 256 : TV / np2(R));
   static constexpr int LS = R + (TL > 1 ? 1 : 0);
   static constexpr int NEL = TL * R;
   static constexpr int NODD = nodd(Q);
@@ -138,7 +141,7 @@ TR_D void bfly(cplx* a, int sign) {
 }
 
 // one Stockham stage over every staged sub-transform
-template <int R, int TL, int LS, int RS, int NSS>
+template <int R, int TL, int LS, int RS, int NSS, int FT>
 TR_D void stage(cplx* sm, const cplx* twR, int sign) {
   constexpr int PER = R / RS;
   constexpr int TOT = PER * TL;
@@ -176,20 +179,20 @@ TR_D void stage(cplx* sm, const cplx* twR, int sign) {
   __syncthreads();
 }
 
-template <int LOG2, int Q, int S, int NSS>
+template <int LOG2, int Q, bool SM, int S, int NSS>
 TR_D void run_stages(cplx* sm, const cplx* twR, int sign) {
-  using G = Geo<LOG2, Q>;
+  using G = Geo<LOG2, Q, SM>;
   if constexpr (S < G::NST) {
     constexpr int RS = G::radix(S);
-    stage<G::R, G::TL, G::LS, RS, NSS>(sm, twR, sign);
-    run_stages<LOG2, Q, S + 1, NSS * RS>(sm, twR, sign);
+    stage<G::R, G::TL, G::LS, RS, NSS, G::FT>(sm, twR, sign);
+    run_stages<LOG2, Q, SM, S + 1, NSS * RS>(sm, twR, sign);
   }
 }
 
-template <int LOG2, int Q>
-__global__ void __launch_bounds__(FT) fft_fast_kernel(FastArgs a) {
-  using G = Geo<LOG2, Q>;
-  constexpr int R = G::R, TL = G::TL, LS = G::LS, NEL = G::NEL;
+template <int LOG2, int Q, bool SM>
+__global__ void __launch_bounds__(SM ? 128 : 256) fft_fast_kernel(FastArgs a) {
+  using G = Geo<LOG2, Q, SM>;
+  constexpr int R = G::R, TL = G::TL, LS = G::LS, NEL = G::NEL, FT = G::FT;
   extern __shared__ __align__(16) unsigned char fsm[];
   cplx* sm = reinterpret_cast<cplx*>(fsm);
   __shared__ long long ib[TL], ob[TL];
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(FT) fft_fast_kernel(FastArgs a) {
     }
   }
   __syncthreads();
-  run_stages<LOG2, Q, 0, 1>(sm, a.twR, a.sign);
+  run_stages<LOG2, Q, SM, 0, 1>(sm, a.twR, a.sign);
   // ---- store ----
   if (a.Ns == 1) {
 #pragma unroll 4
@@ -261,21 +264,21 @@ __global__ void __launch_bounds__(FT) fft_fast_kernel(FastArgs a) {
   }
 }
 
-template <int LOG2, int Q>
+template <int LOG2, int Q, bool SM>
 int launch_t(const FastArgs& a, cudaStream_t st) {
-  if constexpr ((Q << LOG2) > TILE) {
+  if constexpr ((Q << LOG2) > TILE || (SM && (Q << LOG2) > 1024)) {
     return -1;
   } else {
-  using G = Geo<LOG2, Q>;
+  using G = Geo<LOG2, Q, SM>;
   size_t smem = sizeof(cplx) * (size_t)G::TL * G::LS;
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(fft_fast_kernel<LOG2, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(fft_fast_kernel<LOG2, Q, SM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          96 * 1024);
     set = true;
   }
   long long blocks = (a.nsub + G::TL - 1) / G::TL;
-  { TrKTimer _kt(TRK_FFT, st); fft_fast_kernel<LOG2, Q><<<(unsigned)blocks, FT, smem, st>>>(a); }
+  { TrKTimer _kt(TRK_FFT, st); fft_fast_kernel<LOG2, Q, SM><<<(unsigned)blocks, G::FT, smem, st>>>(a); }
   return 0;
   }
 }
@@ -301,11 +304,11 @@ bool fast_supported(int log2, int q) {
   return (q << log2) <= TILE && log2 <= 12;
 }
 
-int fast_launch(int log2, int q, const FastArgs& a, cudaStream_t st) {
+int fast_launch(int log2, int q, bool small, const FastArgs& a, cudaStream_t st) {
   if (!fast_supported(log2, q)) return -1;
 #define TR_L(Q, L) \
   case L:          \
-    return launch_t<L, Q>(a, st);
+    return small ? launch_t<L, Q, true>(a, st) : launch_t<L, Q, false>(a, st);
   switch (q) {
     TR_FAST_CASES(1, 12)
     TR_FAST_CASES(3, 10)

@@ -24,6 +24,19 @@
 #include "leaf.cuh"
 #include "leaf_split.cuh"
 
+#include <stdlib.h>
+
+// pivot-chain clock trace of system 0 (diagnostic, tr_debug_pivot_trace)
+__device__ long long g_pivot_trace[4 * 1024];
+__device__ int g_pivot_trace_on = 0;
+
+extern "C" int tr_debug_pivot_trace(int enable, long long* out, int n) {
+  int on = enable;
+  cudaMemcpyToSymbol(g_pivot_trace_on, &on, sizeof(int));
+  if (out) cudaMemcpyFromSymbol(out, g_pivot_trace, sizeof(long long) * (n < 4096 ? n : 4096));
+  return 0;
+}
+
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -70,8 +83,87 @@ TR_D int decide(const cplx (&phi)[P], const int (&cd)[P], double thr, cplx* mu_o
   const double inv2 = 1.0 / cabs2(pj);
   const cplx inv = cmk(pj.x * inv2, -pj.y * inv2);
 #pragma unroll
-  for (int i = 0; i < P; ++i) mu_out[i] = cneg(cmul(phi[i], inv));
+  for (int i = 0; i < P; ++i) mu_out[i] = i == j ? cmk(0.0, 0.0) : cneg(cmul(phi[i], inv));
   return j;
+}
+
+// 1/x to ~1 ulp: MUFU reciprocal estimate + two Newton steps (DDIV costs ~80
+// cycles of latency on the chain, this ~50)
+TR_D double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// The same rule as decide() with a short dependency chain (it sits on the
+// leaf's critical path once per condition): squared moduli, reciprocals of
+// every candidate computed in parallel, max / first-argmax by trees.
+template <int P>
+TR_D int decide_fast(const cplx (&phi)[P], const int (&cd)[P], double thr, cplx* mu_out) {
+  double a2[P], inv2[P], key[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) a2[i] = cabs2(phi[i]);
+#pragma unroll
+  for (int i = 0; i < P; ++i) inv2[i] = rcp_nr(a2[i]);
+  int dmin = cd[0];
+#pragma unroll
+  for (int i = 1; i < P; ++i) dmin = min(dmin, cd[i]);
+#pragma unroll
+  for (int i = 0; i < P; ++i) key[i] = cd[i] == dmin ? a2[i] : -1.0;
+  // tree: (value, index) with ties to the lower index
+  double v[P];
+  int ix[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) { v[i] = key[i]; ix[i] = i; }
+  double am[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) am[i] = a2[i];
+#pragma unroll
+  for (int w = 1; w < P; w *= 2) {
+#pragma unroll
+    for (int i = 0; i + w < P; i += 2 * w) {
+      const bool take = v[i + w] > v[i];
+      ix[i] = take ? ix[i + w] : ix[i];
+      v[i] = take ? v[i + w] : v[i];
+      am[i] = fmax(am[i], am[i + w]);
+    }
+  }
+  const int j = ix[0];
+  const double bm = v[0], amax2 = am[0];
+  if (amax2 == 0.0 || bm < thr * thr * amax2) return -1;
+  cplx pj = phi[0];
+  double ij = inv2[0];
+#pragma unroll
+  for (int i = 1; i < P; ++i) {
+    pj = (j == i) ? phi[i] : pj;
+    ij = (j == i) ? inv2[i] : ij;
+  }
+  const cplx inv = cmk(pj.x * ij, -pj.y * ij);
+#pragma unroll
+  for (int i = 0; i < P; ++i) mu_out[i] = i == j ? cmk(0.0, 0.0) : cneg(cmul(phi[i], inv));
+  return j;
+}
+
+// Branch-free column selection: a data-dependent switch costs ~200 cycles on
+// B200 (indirect branch), a select chain a few ALU ops.
+template <int P>
+TR_D cplx sel(const cplx (&v)[P], int j) {
+  cplx r = v[0];
+#pragma unroll
+  for (int i = 1; i < P; ++i) r = (j == i) ? v[i] : r;
+  return r;
+}
+
+// r <- r F_t(sigma_s) with mu_j == 0: r_i += mu_i r_j, r_j <- r_j (sigma_s - sigma_t)
+template <int P>
+TR_D void row_update(cplx (&r)[P], int j, const cplx* mu, cplx dsig) {
+  const cplx rj = sel<P>(r, j);
+  const cplx nj = cmul(rj, dsig);
+#pragma unroll
+  for (int i = 0; i < P; ++i) r[i] = (i == j) ? nj : cfma(mu[i], rj, r[i]);
 }
 
 #define TR_SWITCH_J(P, CALL)                     \
@@ -135,6 +227,7 @@ __global__ void __launch_bounds__(NW * 32) leaf_pivot_kernel(LeafArgs a, SplitSt
   }
   if (tid == 0) {
     nd_s = 0;
+    s.viol[sys] = 0;
     const int j0 = decide<P>(r[0], cd, a.thr, pmu[0]);
     pj[0] = j0;
     psig[0] = sg[0];
@@ -206,6 +299,355 @@ __global__ void __launch_bounds__(NW * 32) leaf_pivot_kernel(LeafArgs a, SplitSt
     s.len_try[sys] = len;
   }
   if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cd[i];
+  }
+}
+
+// --------------------------------------------------- A (8 warps, 1 row each)
+// Critical path per step: barrier -> read (j, mu, sigma) -> owner row update
+// -> pivot rule -> publish.  Only the warp holding condition t+1 evaluates
+// the rule (all its lanes SIMT, the owner lane publishes); every update is
+// branch-free.
+template <int P>
+__global__ void __launch_bounds__(256) leaf_pivot3_kernel(LeafArgs a, SplitState s, int round) {
+  const int sys = blockIdx.x;
+  if (s.need[sys] != round) return;
+  __shared__ cplx pmu[2][P];
+  __shared__ cplx psig[2];
+  __shared__ int pj[2];
+  __shared__ int nd_s;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int K = a.K, rows = a.rows;
+  const int att = round;
+  const cplx* W = a.W + (long long)sys * a.w_sys;
+  const long long rowstride = (long long)rows * P;
+  cplx* mulog = s.mu + (long long)sys * s.kcap * P;
+  int* jlog = s.jl + (long long)sys * s.kcap;
+  int2* dlog = s.def_try + (long long)sys * s.kcap;
+
+  int cd[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
+  cplx r[P];
+  cplx sg = cmk(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
+  if (tid < K) {
+    const long long node = cond_node(a, tid, att);
+    sg = __ldg(&a.twN[node]);
+    const cplx* wr = W + node * rowstride + (tid % rows) * P;
+#pragma unroll
+    for (int i = 0; i < P; ++i) r[i] = wr[i];
+  }
+  if (tid == 0) {
+    nd_s = 0;
+    s.viol[sys] = 0;
+    cplx m[P];
+    const int j0 = decide<P>(r, cd, a.thr, m);
+    pj[0] = j0;
+    psig[0] = sg;
+    jlog[0] = j0;
+    if (j0 >= 0) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        pmu[0][i] = m[i];
+        mulog[i] = m[i];
+      }
+    } else {
+      dlog[0] = make_int2((int)cond_node(a, 0, att), 0);
+      nd_s = 1;
+    }
+  }
+  __syncthreads();
+  int len = 1;
+  const bool trace = g_pivot_trace_on && sys == 0;
+  for (int t = 0; t < K; ++t) {
+    const long long c0 = trace ? clock64() : 0;
+    const int cur = t & 1, nxt = cur ^ 1;
+    const int j = pj[cur];
+    const int tn = t + 1;
+    if (j >= 0) {
+      ++len;
+      cplx mu[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) mu[i] = pmu[cur][i];
+      const cplx sig_t = psig[cur];
+#pragma unroll
+      for (int i = 0; i < P; ++i) cd[i] += (i == j);
+      if (tid > t && tid < K) row_update<P>(r, j, mu, csub(sg, sig_t));
+    }
+    const long long c1 = trace ? clock64() : 0;
+    if (tn < K && warp == (tn >> 5)) {
+      cplx m[P];
+      const int jn = decide<P>(r, cd, a.thr, m);
+      if (trace && tid == tn) {
+        const long long c2 = clock64();
+        g_pivot_trace[4 * tn + 0] = c0;
+        g_pivot_trace[4 * tn + 1] = c1;
+        g_pivot_trace[4 * tn + 2] = c2;
+      }
+      if (tid == tn) {
+        pj[nxt] = jn;
+        psig[nxt] = sg;
+        jlog[tn] = jn;
+        if (jn >= 0) {
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            pmu[nxt][i] = m[i];
+            mulog[(long long)tn * P + i] = m[i];
+          }
+        } else {
+          dlog[nd_s] = make_int2((int)cond_node(a, tn, att), tn % rows);
+          nd_s += 1;
+        }
+        if (trace) g_pivot_trace[4 * tn + 3] = clock64();
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    s.ndef_try[sys] = nd_s;
+    s.len_try[sys] = len;
+#pragma unroll
+    for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cd[i];
+  }
+}
+
+// ---------------------------------------------------- A (relay, no barriers)
+// Warp w owns conditions 32w .. 32w+31 (one per lane).  Only the warp that
+// owns the next condition is on the critical path: it applies the newest step
+// to its rows, evaluates the pivot rule (SIMT; the owner lane's result is
+// broadcast by shuffle), appends (j, mu, sigma) to an smem log and bumps a
+// volatile head counter.  Every other warp replays the log on its own rows
+// in the background and is current by the time the chain reaches it.
+TR_D int vload(const int* p) { return *(const volatile int*)p; }
+TR_D cplx shfl_c(cplx v, int src) {
+  return cmk(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src));
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) leaf_pivot_relay_kernel(LeafArgs a, SplitState s, int round) {
+  const int sys = blockIdx.x;
+  if (s.need[sys] != round) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = a.K, rows = a.rows;
+  cplx* lmu = reinterpret_cast<cplx*>(smem_raw);   // [K][P]
+  cplx* lsig = lmu + (size_t)K * P;                // [K]
+  int* lj = reinterpret_cast<int*>(lsig + K);      // [K]
+  int* head = lj + K;                              // [1]
+  int* nd_s = head + 1;                            // [1]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int att = round;
+  const cplx* W = a.W + (long long)sys * a.w_sys;
+  const long long rowstride = (long long)rows * P;
+  int2* dlog = s.def_try + (long long)sys * s.kcap;
+
+  int cd[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
+  cplx r[P];
+  cplx sg = cmk(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
+  if (tid < K) {
+    const long long node = cond_node(a, tid, att);
+    sg = __ldg(&a.twN[node]);
+    const cplx* wr = W + node * rowstride + (tid % rows) * P;
+#pragma unroll
+    for (int i = 0; i < P; ++i) r[i] = wr[i];
+  }
+  if (tid == 0) {
+    *head = 0;
+    *nd_s = 0;
+    s.viol[sys] = 0;
+  }
+  __syncthreads();
+
+  const int first = 32 * warp;            // first condition this warp decides
+  const int last = min(K, first + 32);    // one past its last
+  if (first < K) {
+    int done = 0;                         // log steps applied to these rows
+    // decide condition tn on current rows and publish it (whole warp)
+    auto publish = [&](int tn) {
+      cplx m[P];
+      const int jn = decide_fast<P>(r, cd, a.thr, m);
+      const cplx so = sg;
+      const int ow = tn & 31;
+      if (lane == ow) {
+        lj[tn] = jn;
+        lsig[tn] = so;
+        if (jn >= 0) {
+#pragma unroll
+          for (int i = 0; i < P; ++i) lmu[tn * P + i] = m[i];
+        } else {
+          const int nd = vload(nd_s);
+          dlog[nd] = make_int2((int)cond_node(a, tn, att), tn % rows);
+          *(volatile int*)nd_s = nd + 1;
+        }
+        __threadfence_block();
+        *(volatile int*)head = tn + 1;
+      }
+      __syncwarp();
+    };
+    // apply logged step t to these rows
+    auto apply = [&](int t) {
+      const int j = lj[t];
+      if (j >= 0) {
+        cplx mu[P];
+#pragma unroll
+        for (int i = 0; i < P; ++i) mu[i] = lmu[t * P + i];
+        const cplx sig_t = lsig[t];
+#pragma unroll
+        for (int i = 0; i < P; ++i) cd[i] += (i == j);
+        if (tid > t && tid < K) row_update<P>(r, j, mu, csub(sg, sig_t));
+      }
+    };
+    if (warp == 0) publish(0);
+    // replay until the chain reaches this warp's first condition
+    const int need = first > 0 ? first - 1 : 0;
+    while (done < need) {
+      int h;
+      while ((h = vload(head)) <= done) __nanosleep(32);
+      __threadfence_block();
+      if (h > need) h = need;
+      for (; done < h; ++done) apply(done);
+    }
+    // own the chain for conditions first .. last-1
+    for (int tn = (first > 0 ? first : 1); tn < last; ++tn) {
+      while (vload(head) < tn) {}
+      __threadfence_block();
+      apply(tn - 1);
+      done = tn;
+      publish(tn);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int len = 1;
+    int cdf[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) cdf[i] = a.cd[sys * 8 + i];
+    cplx* mulog = s.mu + (long long)sys * s.kcap * P;
+    int* jlog = s.jl + (long long)sys * s.kcap;
+    for (int t = 0; t < K; ++t) {
+      const int j = lj[t];
+      jlog[t] = j;
+      if (j >= 0) {
+        ++len;
+#pragma unroll
+        for (int i = 0; i < P; ++i) cdf[i] += (i == j);
+      }
+    }
+    s.ndef_try[sys] = *nd_s;
+    s.len_try[sys] = len;
+#pragma unroll
+    for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cdf[i];
+  }
+  // the mu log to HBM for the basis replay (coalesced, all threads)
+  cplx* mulog = s.mu + (long long)sys * s.kcap * P;
+  for (int e = tid; e < K * P; e += blockDim.x) mulog[e] = lmu[e];
+}
+
+// ------------------------------------------------------------- A (1 warp)
+// The chain in a single warp: lane l owns conditions s = l + 32 q.  At each
+// step every lane evaluates the pivot rule on its own row of slot q(t+1)
+// (SIMT, no divergence) and the owner lane's result is broadcast by
+// shuffle; rows already absorbed (s <= t) are skipped a whole slot at a time.
+template <int P, int QMAX>
+__global__ void __launch_bounds__(32) leaf_pivot_warp_kernel(LeafArgs a, SplitState s, int round) {
+  const int sys = blockIdx.x;
+  if (s.need[sys] != round) return;
+  const int lane = threadIdx.x;
+  const int K = a.K, rows = a.rows;
+  const int att = round;
+  const cplx* W = a.W + (long long)sys * a.w_sys;
+  const long long rowstride = (long long)rows * P;
+  cplx* mulog = s.mu + (long long)sys * s.kcap * P;
+  int* jlog = s.jl + (long long)sys * s.kcap;
+  int2* dlog = s.def_try + (long long)sys * s.kcap;
+
+  int cd[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
+  cplx r[QMAX][P];
+  cplx sg[QMAX];
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q) {
+    const int c = lane + 32 * q;
+    sg[q] = cmk(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < P; ++i) r[q][i] = cmk(0.0, 0.0);
+    if (c < K) {
+      const long long node = cond_node(a, c, att);
+      sg[q] = __ldg(&a.twN[node]);
+      const cplx* wr = W + node * rowstride + (c % rows) * P;
+#pragma unroll
+      for (int i = 0; i < P; ++i) r[q][i] = wr[i];
+    }
+  }
+  int nd = 0;
+  if (lane == 0) s.viol[sys] = 0;
+  cplx mu[P];
+  cplx sig;
+  int j;
+  // decide condition tn (slot qo = tn / 32, owner lane tn % 32) and broadcast
+  auto decide_bcast = [&](int tn) {
+    const int qo = tn >> 5, ow = tn & 31;
+    cplx m[P];
+    int jj = -1;
+    cplx so = sg[0];
+#define TR_DQ(Q)                                   \
+  case Q:                                          \
+    if constexpr (Q < QMAX) {                      \
+      jj = decide<P>(r[Q], cd, a.thr, m);          \
+      so = sg[Q];                                  \
+    }                                              \
+    break;
+    switch (qo) { TR_DQ(0) TR_DQ(1) TR_DQ(2) TR_DQ(3) TR_DQ(4) TR_DQ(5) TR_DQ(6) TR_DQ(7) default: break; }
+#undef TR_DQ
+    j = __shfl_sync(FULL, jj, ow);
+    sig = shfl_c(so, ow);
+    if (j >= 0) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) mu[i] = shfl_c(m[i], ow);
+    }
+    if (lane == ow) {
+      jlog[tn] = j;
+      if (j >= 0) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) mulog[(long long)tn * P + i] = m[i];
+      }
+    }
+    if (j < 0) {
+      if (lane == 0) dlog[nd] = make_int2((int)cond_node(a, tn, att), tn % rows);
+      ++nd;
+    }
+  };
+  decide_bcast(0);
+  int len = 1;
+  for (int t = 0; t < K; ++t) {
+    if (j >= 0) {
+      ++len;
+#pragma unroll
+      for (int i = 0; i < P; ++i) cd[i] += (i == j);
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) {
+        if (32 * q + 31 <= t) continue;  // the whole slot is absorbed
+        const int c = lane + 32 * q;
+        if (c > t && c < K) {
+          const cplx dsig = csub(sg[q], sig);
+#define TR_R(J) row_step<P, J>(r[q], mu, dsig)
+          TR_SWITCH_J(P, TR_R)
+#undef TR_R
+        }
+      }
+    }
+    if (t + 1 < K) decide_bcast(t + 1);
+  }
+  if (lane == 0) {
+    s.ndef_try[sys] = nd;
+    s.len_try[sys] = len;
 #pragma unroll
     for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cd[i];
   }
@@ -286,16 +728,25 @@ __global__ void __launch_bounds__(MAXT, 1) leaf_build_kernel(LeafArgs a, SplitSt
     if (j < 0) continue;  // deferred: nothing changes (uniform branch)
     const cplx* mu_s = musm + t * P;
     const cplx msig = cneg(sgsm[t]);
-    const cplx mytop = pick_top<P, D>(c, j);
+    // branch-free: old pivot column per degree, then every column at once
+    cplx oj[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) oj[d] = sel<P>(c[d], j);
     cplx up;
-    up.x = __shfl_up_sync(FULL, mytop.x, 1);
-    up.y = __shfl_up_sync(FULL, mytop.y, 1);
+    up.x = __shfl_up_sync(FULL, oj[D - 1].x, 1);
+    up.y = __shfl_up_sync(FULL, oj[D - 1].y, 1);
     if (lane == 0 && warp > 0) up = halo[(cur * NW + warp - 1) * P + j];
     if (u == 0) up = cmk(0.0, 0.0);
     if (brow && u * D <= len) {
-#define TR_B(J) basis_step<P, D, J>(c, mu_s, msig, up)
-      TR_SWITCH_J(P, TR_B)
-#undef TR_B
+      cplx mu[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) mu[i] = mu_s[i];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const cplx nj = cfma(msig, oj[d], d > 0 ? oj[d - 1] : up);
+#pragma unroll
+        for (int i = 0; i < P; ++i) c[d][i] = (i == j) ? nj : cfma(mu[i], oj[d], c[d][i]);
+      }
     }
     ++len;
     if (((t + 1) % RESCALE_PERIOD) == 0) {
@@ -360,11 +811,130 @@ __global__ void __launch_bounds__(MAXT, 1) leaf_build_kernel(LeafArgs a, SplitSt
   }
 }
 
+// ------------------------------------------------------- B (one row per CTA)
+// Rows of the basis never interact in the replay (B <- B F_t acts on each
+// row separately), so row k of system s is CTA (s, k): P x more, much smaller
+// CTAs with cheap barriers.  Coefficients are written unnormalised together
+// with per-row column maxima; the check kernel normalises.
+template <int P, int D, int MAXT>
+__global__ void __launch_bounds__(MAXT) leaf_build_row_kernel(LeafArgs a, SplitState s, int round,
+                                                              int TPR) {
+  const int sys = blockIdx.x, krow = blockIdx.y;
+  if (s.need[sys] != round) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = a.K;
+  const int NT = blockDim.x, NW = NT / 32;
+  cplx* musm = reinterpret_cast<cplx*>(smem_raw);  // [K][P]
+  cplx* sgsm = musm + (size_t)K * P;               // [K]
+  cplx* halo = sgsm + K;                           // [2][NW][P]
+  double* red = reinterpret_cast<double*>(halo + 2 * NW * P);  // [NW][P]
+  int* jsm = reinterpret_cast<int*>(red + NW * P); // [K]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int u = tid;
+  const bool act = u < TPR;
+  const int att = round;
+  const cplx* mulog = s.mu + (long long)sys * s.kcap * P;
+  const int* jlog = s.jl + (long long)sys * s.kcap;
+  for (int e = tid; e < K; e += NT) {
+    const int j = jlog[e];
+    jsm[e] = j;
+    sgsm[e] = __ldg(&a.twN[cond_node(a, e, att)]);
+    if (j >= 0)
+#pragma unroll
+      for (int i = 0; i < P; ++i) musm[e * P + i] = mulog[(long long)e * P + i];
+  }
+  cplx c[D][P];
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      c[d][i] = (u == 0 && d == 0 && i == krow) ? cmk(1.0, 0.0) : cmk(0.0, 0.0);
+  if (lane == 31) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) halo[warp * P + i] = c[D - 1][i];
+  }
+  __syncthreads();
+  int len = 1, cur = 0;
+  bool big = false;
+  for (int t = 0; t < K; ++t) {
+    const int j = jsm[t];
+    if (j < 0) continue;
+    const cplx* mu_s = musm + t * P;
+    const cplx msig = cneg(sgsm[t]);
+    cplx oj[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) oj[d] = sel<P>(c[d], j);
+    cplx up;
+    up.x = __shfl_up_sync(FULL, oj[D - 1].x, 1);
+    up.y = __shfl_up_sync(FULL, oj[D - 1].y, 1);
+    if (lane == 0 && warp > 0) up = halo[(cur * NW + warp - 1) * P + j];
+    if (u == 0) up = cmk(0.0, 0.0);
+    if (act && u * D <= len) {
+      cplx mu[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) mu[i] = mu_s[i];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const cplx nj = cfma(msig, oj[d], d > 0 ? oj[d - 1] : up);
+#pragma unroll
+        for (int i = 0; i < P; ++i) c[d][i] = (i == j) ? nj : cfma(mu[i], oj[d], c[d][i]);
+      }
+    }
+    ++len;
+    if (((t + 1) % RESCALE_PERIOD) == 0) {
+#pragma unroll
+      for (int d = 0; d < D; ++d)
+#pragma unroll
+        for (int i = 0; i < P; ++i) big |= cabs2(c[d][i]) > RESCALE_TRIGGER * RESCALE_TRIGGER;
+    }
+    cur ^= 1;
+    if (lane == 31) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) halo[(cur * NW + warp) * P + i] = c[D - 1][i];
+    }
+    __syncthreads();
+  }
+  if (big) atomicOr(&s.viol[sys], 1);
+  // per-row column maxima (squared) for the check kernel's normalisation
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    double m = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) m = fmax(m, cabs2(c[d][i]));
+    m = wmax(m);
+    if (lane == 0) red[warp * P + i] = m;
+  }
+  __syncthreads();
+  if (tid < P) {
+    double m = 0.0;
+    for (int w = 0; w < NW; ++w) m = fmax(m, red[w * P + tid]);
+    s.colpart[((long long)sys * 8 + krow) * 8 + tid] = m;
+  }
+  cplx* dst = (round == 0 ? a.out : a.scratch) + (long long)sys * a.out_sys;
+  if (act) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int l = u * D + d;
+      if (l < a.cap) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) dst[(long long)(krow * P + i) * a.cap + l] = c[d][i];
+      }
+    }
+  }
+  const int covered = TPR * D;
+  if (a.cap > covered) {
+    const int tail = a.cap - covered;
+    for (long long e = tid; e < (long long)P * tail; e += NT)
+      dst[(long long)(krow * P + e / tail) * a.cap + covered + e % tail] = cmk(0.0, 0.0);
+  }
+}
+
 // ------------------------------------------------------------------ C
 constexpr int CK = 256;
 
 template <int P>
-__global__ void __launch_bounds__(CK) leaf_check_kernel(LeafArgs a, SplitState s, int round) {
+__global__ void __launch_bounds__(CK) leaf_check_kernel(LeafArgs a, SplitState s, int round,
+                                                        int norm) {
   const int sys = blockIdx.x;
   if (s.need[sys] != round) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -372,13 +942,36 @@ __global__ void __launch_bounds__(CK) leaf_check_kernel(LeafArgs a, SplitState s
   cplx* wtab = reinterpret_cast<cplx*>(smem_raw);  // [M]
   cplx* gbuf = wtab + M;                           // [P*P][M]
   cplx* bvb = gbuf + P * P * M;                    // [P*P][M]
+  cplx* twl = bvb + P * P * M;                     // [cap] twist factors of one coset
   __shared__ double red[CK / 32];
+  __shared__ double csafe[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const cplx* W = a.W + (long long)sys * a.w_sys;
   const long long rowstride = (long long)rows * P;
-  const cplx* src = (round == 0 ? a.out : a.scratch) + (long long)sys * a.out_sys;
+  cplx* src = (round == 0 ? a.out : a.scratch) + (long long)sys * a.out_sys;
   const int len = s.len_try[sys];
   for (int e = tid; e < M; e += CK) wtab[e] = __ldg(&a.twN[(long long)e * a.stride]);
+  if (norm) {
+    // column normalisation of the row-parallel build (ref tanint.py:179-183)
+    if (tid < P) {
+      double m = 0.0;
+      for (int k = 0; k < P; ++k) m = fmax(m, s.colpart[((long long)sys * 8 + k) * 8 + tid]);
+      m = sqrt(m);
+      csafe[tid] = m > 0.0 ? m : 1.0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double f = 1.0;
+      for (int i = 0; i < P; ++i) f = fmax(f, csafe[i]);
+      s.factor_try[sys] = f;
+    }
+    for (long long e = tid; e < (long long)P * P * len; e += CK) {
+      const long long ee = e / len, l = e % len;
+      cplx* p = src + ee * a.cap + l;
+      *p = cscale(*p, 1.0 / csafe[ee % P]);
+    }
+    __syncthreads();
+  }
   // scale = max |w_in| over the leaf's conditions
   double sc = 0.0;
   for (int e = tid; e < K * P; e += CK) {
@@ -395,11 +988,13 @@ __global__ void __launch_bounds__(CK) leaf_check_kernel(LeafArgs a, SplitState s
   double resm = 0.0;
   for (int cs = 0; cs < a.noff; ++cs) {
     const long long oc = cs ? a.o1 : a.o0;
+    // twist factors w_N^(oc l), l < len, generated incrementally per warp-stride
+    for (int l = tid; l < len; l += CK) twl[l] = __ldg(&a.twN[(oc * l) % a.N]);
+    __syncthreads();
     for (int e = tid; e < P * P * M; e += CK) {
       const int ee = e / M, q = e % M;
       cplx acc = cmk(0.0, 0.0);
-      for (int l = q; l < len; l += M)
-        acc = cfma(src[(long long)ee * a.cap + l], __ldg(&a.twN[(oc * l) % a.N]), acc);
+      for (int l = q; l < len; l += M) acc = cfma(src[(long long)ee * a.cap + l], twl[l], acc);
       gbuf[ee * M + q] = acc;
     }
     __syncthreads();
@@ -457,7 +1052,7 @@ __global__ void __launch_bounds__(CK) leaf_check_kernel(LeafArgs a, SplitState s
     if (s.viol[sys]) {
       s.need[sys] = SPLIT_EXACT;  // speculation failed: exact coupled kernel
     } else if (!done) {
-      s.need[sys] = round + 1;
+      s.need[sys] = round + 1;    // retry with the next absorption order
     } else {
       // commit (ref tanint.py:430-434)
       for (int i = 0; i < P; ++i) a.cd[sys * 8 + i] = s.cd_best[sys * 8 + i];
@@ -501,40 +1096,99 @@ int launch_build(const LeafArgs& a, const SplitState& s, int round, int nsys, cu
   return 0;
 }
 
-}  // namespace
-
-// basis builder shapes: P=5 -> D=3 (<= 480 threads), P=7 -> D=4 (<= 352)
-bool leaf_split_supported(const LeafArgs& a) {
-  const size_t csm = sizeof(cplx) * ((size_t)a.M + 2 * (size_t)a.P * a.P * a.M);
-  if (csm > 200 * 1024) return false;
-  if (a.P == 5) return a.K + 1 <= 96 * 3 && a.K <= 4 * 32 * 2;
-  if (a.P == 7) return a.K + 1 <= 50 * 4 && a.K <= 4 * 32 * 2;
-  return false;
+template <int P, int D, int MAXT>
+int launch_build_row(const LeafArgs& a, const SplitState& s, int round, int nsys, cudaStream_t st) {
+  const int TPR = (a.K + 1 + D - 1) / D;
+  const int NT = (TPR + 31) & ~31;
+  if (NT > MAXT) return -1;
+  const int NW = NT / 32;
+  size_t smem = sizeof(cplx) * ((size_t)a.K * P + a.K + 2 * (size_t)NW * P) +
+                sizeof(double) * NW * P + sizeof(int) * (a.K + 1);
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(leaf_build_row_kernel<P, D, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         160 * 1024);
+    set = true;
+  }
+  TrKTimer _kt(TRK_LEAF_BUILD, st);
+  leaf_build_row_kernel<P, D, MAXT><<<dim3(nsys, P), NT, smem, st>>>(a, s, round, TPR);
+  return 0;
 }
 
+size_t check_smem(const LeafArgs& a) {
+  return sizeof(cplx) * ((size_t)a.M + 2 * (size_t)a.P * a.P * a.M + a.cap);
+}
+
+}  // namespace
+
+bool leaf_split_supported(const LeafArgs& a) {
+  if (check_smem(a) > 200 * 1024) return false;
+  if (a.K > 256) return false;
+  return a.P == 5 || a.P == 7;
+}
+
+// One leaf for every system: rounds of (pivot chain, basis replay, check);
+// a system leaves the rounds as soon as its self-check passes.
 int leaf_split_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t st) {
-  { TrKTimer _kt(TRK_LEAF_PIVOT, st); need_reset_kernel<<<(nsys + 255) / 256, 256, 0, st>>>(s.need, nsys); }
-  const size_t csm = sizeof(cplx) * ((size_t)a.M + 2 * (size_t)a.P * a.P * a.M);
+  {
+    TrKTimer _kt(TRK_LEAF_PIVOT, st);
+    need_reset_kernel<<<(nsys + 255) / 256, 256, 0, st>>>(s.need, nsys);
+  }
+  const size_t csm = check_smem(a);
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(leaf_check_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(leaf_check_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     set = true;
   }
+  // diagnostics: TR_PIVOT=warp|block4 (pivot variants), TR_BUILD=block (one-CTA replay)
+  static const char* pv = getenv("TR_PIVOT");
+  static const char* bv = getenv("TR_BUILD");
+  const bool block_build = bv && bv[0] == 'b';
   for (int round = 0; round < a.nattempts; ++round) {
+    {
+      TrKTimer _kt(TRK_LEAF_PIVOT, st);
+      if (pv && pv[0] == 'w') {
+        if (a.P == 5) leaf_pivot_warp_kernel<5, 8><<<nsys, 32, 0, st>>>(a, s, round);
+        else leaf_pivot_warp_kernel<7, 8><<<nsys, 32, 0, st>>>(a, s, round);
+      } else if (pv && pv[0] == 'b') {
+        if (a.P == 5) leaf_pivot_kernel<5, 4, 2><<<nsys, 128, 0, st>>>(a, s, round);
+        else leaf_pivot_kernel<7, 4, 2><<<nsys, 128, 0, st>>>(a, s, round);
+      } else if (pv && pv[0] == '3') {
+        if (a.P == 5) leaf_pivot3_kernel<5><<<nsys, 256, 0, st>>>(a, s, round);
+        else leaf_pivot3_kernel<7><<<nsys, 256, 0, st>>>(a, s, round);
+      } else {
+        const size_t rsm = sizeof(cplx) * (size_t)a.K * (a.P + 1) + sizeof(int) * (a.K + 2);
+        if (a.P == 5) leaf_pivot_relay_kernel<5><<<nsys, 256, rsm, st>>>(a, s, round);
+        else leaf_pivot_relay_kernel<7><<<nsys, 256, rsm, st>>>(a, s, round);
+      }
+    }
     int rc;
-    if (a.P == 5) {
-      { TrKTimer _kt(TRK_LEAF_PIVOT, st); leaf_pivot_kernel<5, 4, 2><<<nsys, 128, 0, st>>>(a, s, round); }
-      rc = launch_build<5, 3, 480>(a, s, round, nsys, st);
-      { TrKTimer _kt(TRK_LEAF_CHECK, st); if (!rc) leaf_check_kernel<5><<<nsys, CK, csm, st>>>(a, s, round); }
+    if (block_build) {
+      rc = a.P == 5 ? launch_build<5, 3, 480>(a, s, round, nsys, st)
+                    : launch_build<7, 4, 352>(a, s, round, nsys, st);
     } else {
-      { TrKTimer _kt(TRK_LEAF_PIVOT, st); leaf_pivot_kernel<7, 4, 2><<<nsys, 128, 0, st>>>(a, s, round); }
-      rc = launch_build<7, 4, 352>(a, s, round, nsys, st);
-      { TrKTimer _kt(TRK_LEAF_CHECK, st); if (!rc) leaf_check_kernel<7><<<nsys, CK, csm, st>>>(a, s, round); }
+      static const int bd = bv ? atoi(bv) : 0;  // TR_BUILD=<degrees per thread>
+      if (bd == 4) {
+        rc = a.P == 5 ? launch_build_row<5, 4, 128>(a, s, round, nsys, st)
+                      : launch_build_row<7, 4, 128>(a, s, round, nsys, st);
+      } else if (bd == 2) {
+        rc = a.P == 5 ? launch_build_row<5, 2, 160>(a, s, round, nsys, st)
+                      : launch_build_row<7, 2, 160>(a, s, round, nsys, st);
+      } else {
+        rc = a.P == 5 ? launch_build_row<5, 1, 288>(a, s, round, nsys, st)
+                      : launch_build_row<7, 1, 288>(a, s, round, nsys, st);
+      }
     }
     if (rc) {
       tr_set_error("leaf split shape unsupported (K=%d, P=%d)", a.K, a.P);
       return 2;
+    }
+    {
+      TrKTimer _kt(TRK_LEAF_CHECK, st);
+      const int norm = block_build ? 0 : 1;
+      if (a.P == 5) leaf_check_kernel<5><<<nsys, CK, csm, st>>>(a, s, round, norm);
+      else leaf_check_kernel<7><<<nsys, CK, csm, st>>>(a, s, round, norm);
     }
   }
   TR_CUDA_CHECK(cudaGetLastError());

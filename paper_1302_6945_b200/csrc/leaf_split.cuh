@@ -21,6 +21,7 @@ struct SplitState {
   double* factor_best;
   double* res_best;
   int* viol;           // [sys] rescale speculation violated
+  double* colpart;     // [sys][8][8] per-row column max^2 (row-parallel build)
 };
 
 bool leaf_split_supported(const LeafArgs& a);

@@ -547,6 +547,7 @@ size_t layout(const Plan& p, long long nsys, char* base, WS* w) {
   s.factor_best = c.take<double>((size_t)nsys);
   s.res_best = c.take<double>((size_t)nsys);
   s.viol = c.take<int>((size_t)nsys);
+  s.colpart = c.take<double>((size_t)nsys * 64);
   return c.off + 256;
 }
 
@@ -899,7 +900,11 @@ int solve_chunk(const Plan& p, const Inputs& in, long long nsys, const WS& w, cp
   TR_TRY(launch_norms(w.Rv, n, nsys, w.partial, NORM_CHUNKS, w.nrm, st));
   TR_TRY(launch_norms(w.Y, n, nsys, w.partial, NORM_CHUNKS, w.nrm + nsys, st));
   TR_CUDA_CHECK(cudaMemcpyAsync(x_out, w.X, sizeof(cplx) * nsys * n, cudaMemcpyDeviceToDevice, st));
-  if (diag_host) {
+  return 0;
+}
+
+int read_diag(const Plan& p, long long nsys, const WS& w, cudaStream_t st, tr_diag* diag_host) {
+  {
     std::vector<int> cd(nsys * 8), dc(nsys), rt(nsys), stt(nsys), tro(nsys);
     std::vector<double> ms(nsys), nr(2 * nsys);
     TR_CUDA_CHECK(cudaMemcpyAsync(cd.data(), w.cd, sizeof(int) * nsys * 8, cudaMemcpyDeviceToHost, st));
@@ -925,6 +930,79 @@ int solve_chunk(const Plan& p, const Inputs& in, long long nsys, const WS& w, cp
       dg.trim_overflow = tro[s];
     }
   }
+  return 0;
+}
+
+// ---------------------------------------------------------- CUDA graphs
+// The whole solve (tens of thousands of small launches: one per tree node and
+// kernel class) is captured once per (plan, batch, buffers) and replayed with a
+// single cudaGraphLaunch.  First call: eager (also performs one-time setup such
+// as smem attributes); second call: capture + replay; later calls: replay.
+// Work runs on a private stream fenced to the caller's stream by events, so a
+// legacy default stream is fine.  TR_GRAPHS=0 disables; kernel timing and the
+// leaf trace force eager execution.
+struct GraphEntry {
+  int calls = 0;
+  cudaGraphExec_t exec = nullptr;
+  long long nodes = 0;
+};
+std::mutex g_graph_mu;
+std::map<std::string, GraphEntry> g_graphs;
+
+int run_solve(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx* x_out, int refine,
+              cudaStream_t st, void* ws) {
+  static const char* env = getenv("TR_GRAPHS");
+  static const bool trace = getenv("TR_LEAF_TRACE") != nullptr;
+  const bool graphs = !(env && env[0] == '0') && !trace && !g_timing.load();
+  if (!graphs) return solve_chunk(p, in, nsys, w, x_out, refine, st, nullptr);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  char key[512];
+  snprintf(key, sizeof key, "%d|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%d|%p|%p|%d", dev,
+           (const void*)&p, nsys, (const void*)in.T, in.T_bs, (const void*)in.L, in.L_bs,
+           (const void*)in.G, in.G_bs, (const void*)in.beta_sq, in.beta_bs, (const void*)in.rhs,
+           in.rhs_bs, in.rhs_is_normal, (void*)x_out, ws, refine);
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  GraphEntry& e = g_graphs[key];
+  e.calls += 1;
+  if (!e.exec && e.calls < 2) return solve_chunk(p, in, nsys, w, x_out, refine, st, nullptr);
+  static thread_local cudaStream_t gs = nullptr;
+  static thread_local cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  if (!gs) {
+    TR_CUDA_CHECK(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+    TR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    TR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+  }
+  if (!e.exec) {
+    cudaGraph_t g = nullptr;
+    const long long n0 = g_launches.load();
+    TR_CUDA_CHECK(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+    int rc = solve_chunk(p, in, nsys, w, x_out, refine, gs, nullptr);
+    cudaError_t ce = cudaStreamEndCapture(gs, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ce != cudaSuccess) {
+      tr_set_error("graph capture failed: %s", cudaGetErrorString(ce));
+      return 4;
+    }
+    e.nodes = g_launches.load() - n0;
+    g_launches.fetch_sub(e.nodes);  // counted again at each replay below
+    ce = cudaGraphInstantiate(&e.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) {
+      e.exec = nullptr;
+      tr_set_error("graph instantiate failed: %s", cudaGetErrorString(ce));
+      return 4;
+    }
+  }
+  TR_CUDA_CHECK(cudaEventRecord(ev_in, st));
+  TR_CUDA_CHECK(cudaStreamWaitEvent(gs, ev_in, 0));
+  TR_CUDA_CHECK(cudaGraphLaunch(e.exec, gs));
+  TR_CUDA_CHECK(cudaEventRecord(ev_out, gs));
+  TR_CUDA_CHECK(cudaStreamWaitEvent(st, ev_out, 0));
+  g_launches.fetch_add(e.nodes);
   return 0;
 }
 
@@ -987,7 +1065,8 @@ extern "C" int tr_solve_batch(const tr_desc* d, int64_t batch, const double* T_g
   // beta_sq is only read for l2; point others at the workspace norm slot
   if (!in.beta_sq) { in.beta_sq = w.nrm; in.beta_bs = 0; }
   cudaStream_t st = (cudaStream_t)stream;
-  TR_TRY(solve_chunk(*p, in, batch, w, reinterpret_cast<cplx*>(x_out), d->refine, st, diag_host));
+  TR_TRY(run_solve(*p, in, batch, w, reinterpret_cast<cplx*>(x_out), d->refine, st, workspace));
+  if (diag_host) TR_TRY(read_diag(*p, batch, w, st, diag_host));
   if (diag_host) {
     for (long long s = 0; s < batch; ++s) {
       if (diag_host[s].status == 3) return 3;

@@ -171,6 +171,84 @@ __global__ void trim4_kernel(TrimArgs a) {
   }
 }
 
+// All four trim phases in one CTA per system (batches of many systems):
+// profile + global max, last significant index, column maxima over the kept
+// range, scaled write-out.  Same rule as trim1..4 (squared moduli).
+constexpr int TF = 512;
+
+__device__ __forceinline__ double bmax512(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double m = sh[0];
+#pragma unroll
+  for (int w = 1; w < TF / 32; ++w) m = fmax(m, sh[w]);
+  return m;
+}
+
+template <int P>
+__global__ void __launch_bounds__(TF) trim_fused_kernel(TrimArgs a) {
+  __shared__ double sh[TF / 32];
+  const long long sys = blockIdx.x;
+  constexpr int PP = P * P;
+  const cplx* F = a.F + sys * PP * a.R;
+  double* prof = a.prof + sys * a.L;
+  double gm = 0.0;
+  for (long long l = threadIdx.x; l < a.L; l += TF) {
+    double m = 0.0;
+#pragma unroll
+    for (int e = 0; e < PP; ++e) m = fmax(m, cabs2(F[(long long)e * a.R + l]));
+    prof[l] = m;
+    gm = fmax(gm, m);
+  }
+  gm = bmax512(gm, sh);
+  const double thr = 1e-28 * gm;  // (1e-14)^2 on squared moduli
+  double last = 0.0;
+  for (long long l = threadIdx.x; l < a.L; l += TF)
+    if (prof[l] > thr) last = fmax(last, (double)(l + 1));
+  last = bmax512(last, sh);
+  long long lt = (long long)last;
+  if (lt < 1) lt = 1;
+  const long long lw = lt < a.cap_node ? lt : a.cap_node;
+  double cm[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    double m = 0.0;
+    for (long long l = threadIdx.x; l < lt && l < a.L; l += TF)
+#pragma unroll
+      for (int i = 0; i < P; ++i) m = fmax(m, cabs2(F[(long long)(i * P + j) * a.R + l]));
+    cm[j] = sqrt(bmax512(m, sh));
+  }
+  cplx* o = a.out + sys * a.out_sys;
+  for (long long l = threadIdx.x; l < a.cap; l += TF) {
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        cplx v = cmk(0.0, 0.0);
+        if (l < lw) {
+          const double safe = cm[j] > 0.0 ? cm[j] : 1.0;
+          const cplx f = F[(long long)(i * P + j) * a.R + l];
+          v = cmk(f.x / safe, f.y / safe);
+        }
+        o[(long long)(i * P + j) * a.cap + l] = v;
+      }
+  }
+  if (threadIdx.x == 0) {
+    double ms = 1.0;
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const double c = cm[j] / (double)a.R;
+      const double safe = c > 0.0 ? c : 1.0;
+      ms = j == 0 ? safe : fmax(ms, safe);
+    }
+    a.max_scale[sys] = fmax(a.max_scale[sys], ms);
+    if (lt > a.cap_node) a.trim_over[sys] += 1;
+  }
+}
+
 inline dim3 g2(long long n, long long nsys, int th = 256) {
   return dim3((unsigned)((n + th - 1) / th), (unsigned)nsys);
 }
@@ -210,6 +288,15 @@ int launch_pointwise_matmul(cplx* FA, const cplx* FB, int P, long long R, long l
 }
 
 int launch_trim_normalize(const TrimArgs& a, long long nsys, cudaStream_t st) {
+  if (nsys >= 32) {  // enough systems to fill the GPU with one CTA each
+    {
+      TrKTimer _kt(TRK_COMBINE, st);
+      if (a.P == 5) trim_fused_kernel<5><<<(unsigned)nsys, TF, 0, st>>>(a);
+      else trim_fused_kernel<7><<<(unsigned)nsys, TF, 0, st>>>(a);
+    }
+    TR_CUDA_CHECK(cudaGetLastError());
+    return 0;
+  }
   TR_CUDA_CHECK(cudaMemsetAsync(a.red, 0, sizeof(unsigned long long) * (2 + a.P) * nsys, st));
   { TrKTimer _kt(TRK_COMBINE, st); trim1_kernel<<<g2(a.L, nsys), 256, 0, st>>>(a); }
   { TrKTimer _kt(TRK_COMBINE, st); trim2_kernel<<<g2(a.L, nsys), 256, 0, st>>>(a); }
