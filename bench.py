@@ -13,8 +13,9 @@ only collective).  Default workload = BASELINE configs[1] (config 2: T 8192 x
 Printed JSON (rank 0): the contract keys plus
   e2e          same metric through the public API with host buffers
                (DeviceBatch.stage -> run -> fetch, H2D/D2H inside the timing)
-  roofline     the dominant kernel class, FP64-bound, against the FP64 FMA
-               peak measured on this GPU by tr_fp64_peak()
+  roofline     the dominant kernel class: leaf classes FP64-bound against the
+               FP64 FMA peak measured by tr_fp64_peak(); FFT / combine /
+               update HBM-bound against MEASURED_PEAKS.json hbm_gbs
   kernels      per-class device time from CUDA events (separate pass)
   cpu_baseline the oracle port of the reference, timed on this host's cores
   clocks       nvidia-smi samples taken during the timed region
@@ -148,6 +149,30 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def hbm_peak_gbs():
+    """HBM copy bandwidth from the driver-written MEASURED_PEAKS.json, else
+    the profiling recipe's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        for k in ("hbm_gbs", "hbm_copy_gbs", "hbm_GBps"):
+            if k in d:
+                return float(d[k]), f"MEASURED_PEAKS.json:{k}"
+    except (OSError, ValueError):
+        pass
+    return 7700.0, "B200_PROFILING.md fallback"
+
+
+def ncu_traffic(cfg, cls):
+    """dram__bytes_read+write per launch of the class's top kernel from the
+    committed ncu capture (profiles/r1_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            return json.load(f)[cfg][cls]["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 # ---------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -207,6 +232,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = lib.tr_launch_count()
+    torch.cuda.profiler.start()  # ncu --profile-from-start off sees the timed region only
     with ClockSampler(local) as clk:
         for a, b in evs:
             flush.fill_(1)  # L2 flush (256 MiB write) between timed steps
@@ -214,6 +240,7 @@ def main():
             step()
             b.record(stream)
         torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     launches = lib.tr_launch_count() - launches0
     if world > 1:
         dist.barrier()
@@ -261,30 +288,27 @@ def main():
             dist.destroy_process_group()
         return
 
-    # roofline of the dominant class (per solve pass; refinement repeats it)
-    passes = 1 + args.refine
+    # roofline of the dominant class: algorithmic work (the library counts
+    # minimal bytes / useful flops per launch) / its event time
     tot_k = sum(v[0] for v in kst.values()) or 1.0
     dom = max(kst, key=lambda k: kst[k][0])
-    P = 7 if probs[0].variant == "general" else 5
-    K = info["max_leaf_conditions"]
-    leaves = info["leaves"]
-    # algorithmic FP64 work per leaf (SURVEY 8(d) counts, per system):
-    #   basis replay  8 P^2 sum_t (t+1)      = 4 P^2 K (K+1)
-    #   pivot chain   8 P  sum_t (K-1-t)     ~ 4 P K (K-1)   (+ decisions)
-    flops_leaf = {"leaf_build": 4.0 * P * P * K * (K + 1), "leaf_pivot": 4.0 * P * K * (K - 1)}
-    roof = None
-    for name in ([dom] if dom in flops_leaf else []) + ["leaf_build"]:
-        if name in flops_leaf and kst[name][0] > 0:
-            per_leaf_ms = kst[name][0] / (nk * passes * leaves)
-            flops = flops_leaf[name] * count
-            ach = flops / (per_leaf_ms * 1e-3) / 1e12
-            roof = {"kernel": name, "bound": "fp64", "achieved": ach, "peak": peak.value,
-                    "unit": "TFLOP/s", "frac": ach / peak.value if peak.value else None,
-                    "traffic": None,
-                    "peak_source": "measured FP64 FMA burst (tr_fp64_peak); MEASURED_PEAKS.json has no FP64 entry",
-                    "algorithmic_flops_per_launch": flops,
-                    "launch_ms": per_leaf_ms}
-            break
+    hbm_peak, hbm_src = hbm_peak_gbs()
+    ms, nl, by, fl = kst[dom]
+    if dom in ("leaf_pivot", "leaf_build", "leaf_check", "leaf_exact"):
+        ach = fl / (ms * 1e-3) / 1e12
+        roof = {"kernel": dom, "bound": "fp64", "achieved": ach, "peak": peak.value,
+                "unit": "TFLOP/s", "peak_source": "measured FP64 FMA burst (tr_fp64_peak); "
+                                                  "MEASURED_PEAKS.json has no FP64 entry"}
+    else:
+        ach = by / (ms * 1e-3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak,
+                "unit": "GB/s", "peak_source": hbm_src}
+    roof["frac"] = ach / roof["peak"] if roof["peak"] else None
+    roof["traffic"] = ncu_traffic(args.config, dom)
+    roof["algorithmic_bytes_per_launch"] = by / max(nl, 1)
+    roof["algorithmic_flops_per_launch"] = fl / max(nl, 1)
+    roof["avg_launch_ms"] = ms / max(nl, 1)
+    roof["share_of_step"] = ms / tot_k
 
     out = {
         "metric": METRIC,
@@ -300,7 +324,7 @@ def main():
         "dtype": "c128 (fp64)",
         "data": "synthetic (seeded BASELINE-config generators, paper_1302_6945_b200/workloads.py)",
         "config": {"workload": label, "config": args.config, "systems_per_rank": count,
-                   "order_N": info["order"], "leaves": leaves, "leaf_conditions": K,
+                   "order_N": info["order"], "leaves": info["leaves"], "leaf_conditions": info["max_leaf_conditions"],
                    "refine": args.refine, "parallelism": f"dp{world} (systems sharded, gather x to rank 0)",
                    "l2": "256 MiB device write between timed steps (outside the per-step events)",
                    "timing": "CUDA events per step on the launching stream, summed; max over ranks"},
@@ -309,7 +333,10 @@ def main():
                 "path": "DeviceBatch.stage (pinned H2D) -> run -> x D2H"},
         "roofline": roof,
         "kernels": {k: {"ms_per_step": v[0] / nk, "launches_per_step": v[1] / nk,
-                        "share": v[0] / tot_k} for k, v in kst.items() if v[1]},
+                        "share": v[0] / tot_k,
+                        "alg_GBps": v[2] / (v[0] * 1e-3) / 1e9 if v[0] else None,
+                        "alg_TFLOPs": v[3] / (v[0] * 1e-3) / 1e12 if v[0] else None}
+                    for k, v in kst.items() if v[1]},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

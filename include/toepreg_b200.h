@@ -135,6 +135,9 @@ int tr_leaf(const tr_desc* d, const double* weights, int64_t leaf_index, int64_t
 int64_t tr_launch_count(void);
 int tr_kernel_timing(int32_t enable);
 int tr_kernel_stats(int32_t cls, double* total_ms, int64_t* launches);
+/* Algorithmic bytes / flops issued per class while timing was enabled
+ * (minimal HBM traffic and useful FP64 flops, SURVEY 8(d) counting). */
+int tr_kernel_work_stats(int32_t cls, double* alg_bytes, double* alg_flops);
 int tr_fp64_peak(double* tflops);
 
 /* Last error message of the calling thread. */

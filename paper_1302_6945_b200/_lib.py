@@ -70,6 +70,7 @@ SIGNATURES = {
     "tr_launch_count": (C.c_int64, []),
     "tr_kernel_timing": (C.c_int, [_I32]),
     "tr_kernel_stats": (C.c_int, [_I32, C.POINTER(C.c_double), C.POINTER(_I64)]),
+    "tr_kernel_work_stats": (C.c_int, [_I32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "tr_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
     "tr_last_error": (C.c_char_p, []),
 }
@@ -101,13 +102,16 @@ KERNEL_CLASSES = ["assemble", "fft", "leaf_pivot", "leaf_build", "leaf_check", "
 
 
 def kernel_stats():
-    """{class: (total_ms, launches)} since the last tr_kernel_timing call."""
+    """{class: (total_ms, launches, alg_bytes, alg_flops)} since the last
+    tr_kernel_timing call."""
     lib = load()
     out = {}
     for i, name in enumerate(KERNEL_CLASSES):
         ms, n = C.c_double(), C.c_int64()
+        by, fl = C.c_double(), C.c_double()
         lib.tr_kernel_stats(i, C.byref(ms), C.byref(n))
-        out[name] = (ms.value, n.value)
+        lib.tr_kernel_work_stats(i, C.byref(by), C.byref(fl))
+        out[name] = (ms.value, n.value, by.value, fl.value)
     return out
 
 

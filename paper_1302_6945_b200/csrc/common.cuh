@@ -92,6 +92,8 @@ enum {
 };
 void tr_kernel_begin(int cls, cudaStream_t st);
 void tr_kernel_end(int cls, cudaStream_t st);
+// algorithmic work of a launch (counted only while timing is enabled)
+void tr_kernel_work(int cls, double bytes, double flops);
 struct TrKTimer {
   int cls;
   cudaStream_t st;

@@ -1,3 +1,4 @@
+#include <cmath>
 // Batched complex128 multi-pass Stockham FFT (see fft.cuh).
 #include "fft.cuh"
 #include "fft_fast.cuh"
@@ -423,6 +424,8 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
   if (lines <= 0) return 0;
   if (in_len > p.n) in_len = p.n;
   const long long n = p.n;
+  tr_kernel_work(TRK_FFT, 16.0 * lines * (double)(in_len + n),
+                 5.0 * lines * (double)n * std::log2((double)n));
   if (p.npass == 1) {
     launch_pass(p, 0, in, in_ls, in_len, out, out_ls, lines, sign, st);
   } else if (p.npass == 2) {

@@ -1134,6 +1134,13 @@ int leaf_split_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStre
     TrKTimer _kt(TRK_LEAF_PIVOT, st);
     need_reset_kernel<<<(nsys + 255) / 256, 256, 0, st>>>(s.need, nsys);
   }
+  {  // algorithmic work of one attempt (retry rounds are extra work, not counted)
+    const double K = a.K, P = a.P;
+    tr_kernel_work(TRK_LEAF_PIVOT, 16.0 * nsys * K * P, 4.0 * nsys * P * K * (K - 1));
+    tr_kernel_work(TRK_LEAF_BUILD, 16.0 * nsys * P * P * (K + 1), 4.0 * nsys * P * P * K * (K + 1));
+    tr_kernel_work(TRK_LEAF_CHECK, 16.0 * nsys * (P * P * (K + 1) + K * P),
+                   8.0 * nsys * (P * P * (K + 1) + (double)a.noff * P * P * a.M * a.M));
+  }
   const size_t csm = check_smem(a);
   static bool set = false;
   if (!set) {

@@ -53,6 +53,8 @@ std::vector<KEvent> g_kpending;
 std::vector<cudaEvent_t> g_kpool;
 double g_kms[TRK_NCLASS] = {0};
 long long g_kcount[TRK_NCLASS] = {0};
+double g_kbytes[TRK_NCLASS] = {0};
+double g_kflops[TRK_NCLASS] = {0};
 thread_local int g_kcur = -1;
 
 cudaEvent_t kev_get() {
@@ -85,6 +87,13 @@ void tr_kernel_end(int cls, cudaStream_t st) {
   g_kcur = -1;
 }
 
+void tr_kernel_work(int cls, double bytes, double flops) {
+  if (!g_timing.load(std::memory_order_relaxed)) return;
+  std::lock_guard<std::mutex> lk(g_kmu);
+  g_kbytes[cls] += bytes;
+  g_kflops[cls] += flops;
+}
+
 static void kernel_stats_drain() {
   std::lock_guard<std::mutex> lk(g_kmu);
   for (KEvent& k : g_kpending) {
@@ -107,6 +116,8 @@ extern "C" int tr_kernel_timing(int32_t enable) {
   for (int c = 0; c < TRK_NCLASS; ++c) {
     g_kms[c] = 0.0;
     g_kcount[c] = 0;
+    g_kbytes[c] = 0.0;
+    g_kflops[c] = 0.0;
   }
   g_timing.store(enable != 0);
   return 0;
@@ -117,6 +128,14 @@ extern "C" int tr_kernel_stats(int32_t cls, double* total_ms, int64_t* launches)
   kernel_stats_drain();
   if (total_ms) *total_ms = g_kms[cls];
   if (launches) *launches = g_kcount[cls];
+  return 0;
+}
+
+extern "C" int tr_kernel_work_stats(int32_t cls, double* alg_bytes, double* alg_flops) {
+  if (cls < 0 || cls >= TRK_NCLASS) { tr_set_error("kernel class out of range"); return 2; }
+  std::lock_guard<std::mutex> lk(g_kmu);
+  if (alg_bytes) *alg_bytes = g_kbytes[cls];
+  if (alg_flops) *alg_flops = g_kflops[cls];
   return 0;
 }
 

@@ -259,6 +259,7 @@ int launch_twist_fold(cplx* G, const cplx* B, long long b_sys, long long b_cap, 
                       long long o0, long long o1, int noff, long long cnt, long long N,
                       const cplx* twN, long long nsys, cudaStream_t st) {
   dim3 grid((unsigned)((cnt + 255) / 256), noff * PP, (unsigned)nsys);
+  tr_kernel_work(TRK_UPDATE, 16.0 * nsys * PP * (double)(L + noff * cnt), 8.0 * nsys * PP * (double)L);
   { TrKTimer _kt(TRK_UPDATE, st); twist_fold_kernel<<<grid, 256, 0, st>>>(G, B, b_sys, b_cap, PP, L, o0, o1, noff, cnt, N, twN); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
@@ -268,6 +269,8 @@ int launch_apply_update(cplx* W, long long w_sys, const cplx* G, int rows, int P
                         long long o1, int noff, long long stride, long long cnt, long long nsys,
                         cudaStream_t st) {
   dim3 grid((unsigned)((cnt + 127) / 128), noff, (unsigned)nsys);
+  tr_kernel_work(TRK_UPDATE, 16.0 * nsys * noff * (double)cnt * (2.0 * rows * P + P * P),
+                 8.0 * nsys * noff * (double)cnt * rows * P * P);
   if (P == 5)
     { TrKTimer _kt(TRK_UPDATE, st); apply_update_kernel<5><<<grid, 128, 0, st>>>(W, w_sys, G, rows, o0, o1, noff, stride, cnt); }
   else
@@ -278,6 +281,7 @@ int launch_apply_update(cplx* W, long long w_sys, const cplx* G, int rows, int P
 
 int launch_pointwise_matmul(cplx* FA, const cplx* FB, int P, long long R, long long nsys,
                             cudaStream_t st) {
+  tr_kernel_work(TRK_COMBINE, 48.0 * nsys * P * P * (double)R, 8.0 * nsys * P * P * P * (double)R);
   {
     TrKTimer _kt(TRK_COMBINE, st);
     if (P == 5) pointwise_matmul_kernel<5><<<g2(R, nsys, 128), 128, 0, st>>>(FA, FB, R);
@@ -288,6 +292,7 @@ int launch_pointwise_matmul(cplx* FA, const cplx* FB, int P, long long R, long l
 }
 
 int launch_trim_normalize(const TrimArgs& a, long long nsys, cudaStream_t st) {
+  tr_kernel_work(TRK_COMBINE, 16.0 * nsys * a.P * a.P * (double)(a.L + a.cap), 0.0);
   if (nsys >= 32) {  // enough systems to fill the GPU with one CTA each
     {
       TrKTimer _kt(TRK_COMBINE, st);

@@ -221,7 +221,7 @@ class DeviceBatch:
             DeviceBatch._ws_cache[key] = ws
         self.ws = ws
         self.diag = (_lib.TrDiag * self.batch)()
-        self.pinned = {k: torch.from_numpy(np.ascontiguousarray(h).view(np.float64)).pin_memory()
+        self.pinned = {k: torch.from_numpy(np.array(h, copy=True, order="C").view(np.float64)).pin_memory()
                        for k, h in hosts.items()}
         self.x_host = torch.empty((self.batch, self.n, 2), dtype=torch.float64).pin_memory()
 
