@@ -1,0 +1,693 @@
+// Leaf sweep, two kernels per absorption attempt (default path).
+//
+// The reference absorbs a leaf's K conditions one at a time (ref:
+// pkg/src/toepreg/tanint.py:189-217 _serial_core) into a P x P polynomial
+// workspace, then checks the result (:262-270) and retries other orders
+// (:395-434).  Here an attempt is
+//
+//   leaf_chain_kernel  the K sequential pivot decisions.  They depend on the
+//       basis only through the residual rows r_s = w_s . B(sigma_s); one warp
+//       owns the chain for 32 conditions at a time and keeps the row being
+//       decided ("front") and the next one ("pre") replicated in every lane,
+//       so a step is: decide on the front (branch-free argmax), form the
+//       multipliers mu_i = -phi_i / phi_j (MUFU reciprocal + Newton), update
+//       pre into the next front.  The multipliers are logged (smem, then HBM)
+//       for the other warps, which replay them on their own rows and take the
+//       chain over in turn.  Everything on the chain is branch-free: FP64 is
+//       16 lanes/clk per SMSP, so each warp-uniform FP64 instruction costs two
+//       issue cycles and the step time is set by their count.
+//   leaf_basis_kernel  replays the log on the coefficient cube (warp k owns
+//       basis row k, coefficient l = 32 d + lane in registers), skipping the
+//       structurally-zero part of every row (the degree of each entry is
+//       tracked from the log), normalises the columns (ref :179-183), writes
+//       the basis, evaluates it at the leaf's nodes (coset twist, fold,
+//       M-point DFT) for the reference's self-residual and keeps the best
+//       attempt.
+//
+// The reference's mid-sweep rescale (columns above 1e8 at every 8th
+// condition, ref :214-217) would change later decisions; the chain assumes it
+// does not fire and the basis kernel checks that no coefficient exceeded the
+// trigger at those points.  A leaf that violates this is redone by the exact
+// coupled kernel (leaf.cu).
+#include <stdlib.h>
+
+#include "leaf.cuh"
+#include "leaf_split.cuh"
+
+// chain clock trace of system 0 (diagnostic, tr_debug_chain_trace)
+__device__ long long g_chain_trace[4 * 1024];
+__device__ int g_chain_trace_on = 0;
+#define TR_BTRACE(slot) \
+  if (g_chain_trace_on && sys == 0 && round == 0 && tid == 32) g_chain_trace[3072 + (slot)] = clock64();
+
+extern "C" int tr_debug_chain_trace(int enable, long long* out, int n) {
+  int on = enable;
+  cudaMemcpyToSymbol(g_chain_trace_on, &on, sizeof(int));
+  if (out) cudaMemcpyFromSymbol(out, g_chain_trace, sizeof(long long) * (n < 4096 ? n : 4096));
+  return 0;
+}
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr double RESCALE_TRIGGER = 1e8;
+constexpr int RESCALE_PERIOD = 8;
+constexpr int NT = 256;  // threads per CTA of both kernels
+constexpr int NW = NT / 32;
+
+TR_D long long node_of(const LeafArgs& a, int p) {
+  if (a.noff == 1) return a.o0 + a.stride * (long long)p;
+  return ((p & 1) ? a.o1 : a.o0) + a.stride * (long long)(p >> 1);
+}
+TR_D int perm_of(int i, int s, int rev, int count) {
+  if (rev) i = count - 1 - i;
+  return (int)(((unsigned)i * (unsigned)s) % (unsigned)count);
+}
+TR_D long long cond_node(const LeafArgs& a, int s, int att) {
+  return node_of(a, perm_of(s / a.rows, a.ord_stride[att], a.ord_reverse[att], a.count));
+}
+TR_D double wmax(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+TR_D int vload(const int* p) { return *(const volatile int*)p; }
+TR_D cplx shfl_c(cplx v, int src) {
+  return cmk(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src));
+}
+// 1/x to ~1 ulp: MUFU estimate + two Newton steps
+TR_D double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+// a b - c d, the two products in parallel
+TR_D cplx cmsub(cplx a, cplx b, cplx c, cplx d) {
+  const double ux = fma(a.x, b.x, -a.y * b.y), uy = fma(a.x, b.y, a.y * b.x);
+  const double vx = fma(c.x, d.x, -c.y * d.y), vy = fma(c.x, d.y, c.y * d.x);
+  return cmk(ux - vx, uy - vy);
+}
+template <int P>
+TR_D cplx sel(const cplx (&v)[P], int j) {
+  cplx r = v[0];
+#pragma unroll
+  for (int i = 1; i < P; ++i) r = (j == i) ? v[i] : r;
+  return r;
+}
+template <int P>
+TR_D int sel_i(const int (&v)[P], int j) {
+  int r = v[0];
+#pragma unroll
+  for (int i = 1; i < P; ++i) r = (j == i) ? v[i] : r;
+  return r;
+}
+// r <- r F_t(sigma) with the true multipliers (mu_j = 0)
+template <int P>
+TR_D void row_update(cplx (&r)[P], int j, const cplx* mu, cplx dsig) {
+  const cplx rj = sel<P>(r, j);
+  const cplx nj = cmul(rj, dsig);
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    const cplx v = cfma(mu[i], rj, r[i]);
+    r[i] = (i == j) ? nj : v;
+  }
+}
+
+// The pivot rule of ref tanint.py:193-211 on squared moduli: among the
+// lowest-degree columns the first of largest |phi|; deferred (-1) when that
+// is below thr * max|phi| or the row vanishes.  The argmax tree carries the
+// front and pre entries of the winning column along (fj, qj).
+template <int P>
+TR_D int chain_decide(const cplx (&f)[P], const cplx (&pre)[P], const int (&cd)[P], double thr2,
+                      cplx& fj, cplx& qj) {
+  double v[P], am[P];
+  int ix[P];
+  cplx fv[P], pv[P];
+  int dmin = cd[0];
+#pragma unroll
+  for (int i = 1; i < P; ++i) dmin = min(dmin, cd[i]);
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    am[i] = cabs2(f[i]);
+    v[i] = cd[i] == dmin ? am[i] : -1.0;
+    ix[i] = i;
+    fv[i] = f[i];
+    pv[i] = pre[i];
+  }
+#pragma unroll
+  for (int w = 1; w < P; w *= 2) {
+#pragma unroll
+    for (int i = 0; i + w < P; i += 2 * w) {
+      const bool take = v[i + w] > v[i];
+      ix[i] = take ? ix[i + w] : ix[i];
+      v[i] = take ? v[i + w] : v[i];
+      fv[i] = take ? fv[i + w] : fv[i];
+      pv[i] = take ? pv[i + w] : pv[i];
+      am[i] = fmax(am[i], am[i + w]);
+    }
+  }
+  fj = fv[0];
+  qj = pv[0];
+  if (am[0] == 0.0 || v[0] < thr2 * am[0]) return -1;
+  return ix[0];
+}
+
+// ------------------------------------------------------------ chain kernel
+template <int P>
+__global__ void __launch_bounds__(NT) leaf_chain_kernel(LeafArgs a, SplitState s, int round) {
+  const int sys = blockIdx.x;
+  if (s.need[sys] != round) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = a.K, rows = a.rows;
+  cplx* lmu = reinterpret_cast<cplx*>(smem_raw);   // [K][P] true multipliers
+  cplx* lsig = lmu + (size_t)K * P;                // [K + 2] node of every condition
+  int* lj = reinterpret_cast<int*>(lsig + K + 2);  // [K] pivot or -1
+  int* head = lj + K;                              // steps published
+  int* nd_s = head + 1;                            // deferrals so far (at hand-over)
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(FULL, tid >> 5, 0);  // warp-uniform for ptxas (no collective shuffles)
+  const int att = round;
+  const cplx* W = a.W + (long long)sys * a.w_sys;
+  const long long rowstride = (long long)rows * P;
+  int2* dlog = s.def_try + (long long)sys * s.kcap;
+  const double thr2 = a.thr * a.thr;
+
+  int cd[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
+  cplx r[P];
+  cplx sg = cmk(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
+  if (tid < K) {
+    const long long node = cond_node(a, tid, att);
+    sg = __ldg(&a.twN[node]);
+    lsig[tid] = sg;
+    const cplx* wr = W + node * rowstride + (tid % rows) * P;
+#pragma unroll
+    for (int i = 0; i < P; ++i) r[i] = wr[i];
+  }
+  if (tid < 2) lsig[K + tid] = cmk(0.0, 0.0);
+  if (tid == 0) {
+    *head = 0;
+    *nd_s = 0;
+  }
+  __syncthreads();
+
+  const int first = 32 * warp;
+  const int last = min(K, first + 32);
+  if (first < K) {
+    // replay the published steps until the chain reaches this warp
+    int done = 0;
+    while (done < first) {
+      int h;
+      while ((h = vload(head)) <= done) __nanosleep(20);
+      __threadfence_block();
+      if (h > first) h = first;
+      for (; done < h; ++done) {
+        const int j = lj[done];
+        if (j >= 0) {
+          cplx mu[P];
+#pragma unroll
+          for (int i = 0; i < P; ++i) mu[i] = lmu[done * P + i];
+#pragma unroll
+          for (int i = 0; i < P; ++i) cd[i] += (i == j);
+          row_update<P>(r, j, mu, csub(sg, lsig[done]));
+        }
+      }
+    }
+    // own the chain for conditions first .. last-1
+    cplx f[P], pre[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      f[i] = shfl_c(r[i], 0);
+      pre[i] = shfl_c(r[i], 1);
+    }
+    cplx sf = lsig[first], sp = lsig[first + 1];
+    int nd = vload(nd_s);
+    const bool trace = g_chain_trace_on && sys == 0 && round == 0 && lane == 0;
+    for (int tn = first; tn < last; ++tn) {
+      const int ow = tn - first;
+      cplx fj, qj;
+      if (trace) g_chain_trace[4 * tn] = clock64();
+      const int j = chain_decide<P>(f, pre, cd, thr2, fj, qj);
+      if (trace) g_chain_trace[4 * tn + 1] = clock64() + 0 * j;
+      cplx mu[P];
+      if (j >= 0) {
+        // mu_i = -phi_i / phi_j (mu_j = 0), then branch-free
+        //   next front = pre + mu pre_j,   pre_j (s_p - s_f) in column j
+        //   own rows   = r   + mu r_j,     r_j (s_r - s_f)   in column j
+        const double inv2 = rcp_nr(cabs2(fj));
+        const cplx ci = cmk(-fj.x * inv2, fj.y * inv2);
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const cplx m = cmul(f[i], ci);
+          mu[i] = (i == j) ? cmk(0.0, 0.0) : m;
+        }
+        const cplx nfj = cmul(qj, csub(sp, sf));
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const cplx v = cfma(mu[i], qj, pre[i]);
+          f[i] = (i == j) ? nfj : v;
+        }
+        const cplx rj = sel<P>(r, j);
+        const cplx nrj = cmul(rj, csub(sg, sf));
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const cplx v = cfma(mu[i], rj, r[i]);
+          r[i] = (i == j) ? nrj : v;
+          cd[i] += (i == j);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < P; ++i) f[i] = pre[i];
+      }
+      if (trace) g_chain_trace[4 * tn + 2] = clock64() + 0 * (long long)f[0].x;
+      if (lane == 0) {
+        lj[tn] = j;
+        if (j >= 0) {
+#pragma unroll
+          for (int i = 0; i < P; ++i) lmu[tn * P + i] = mu[i];
+        } else {
+          dlog[nd] = make_int2((int)cond_node(a, tn, att), tn % rows);
+        }
+      }
+      nd += (j < 0);
+      if ((ow & 3) == 3 || tn == last - 1) {
+        if (lane == 0) {
+          if (tn == last - 1) *(volatile int*)nd_s = nd;
+          __threadfence_block();
+          *(volatile int*)head = tn + 1;
+        }
+      }
+      // pre <- row tn+2 through step tn (lane ow+2; unused past the warp's range)
+#pragma unroll
+      for (int i = 0; i < P; ++i) pre[i] = shfl_c(r[i], (ow + 2) & 31);
+      sf = sp;
+      sp = lsig[tn + 2];
+      if (trace) g_chain_trace[4 * tn + 3] = clock64() + 0 * (long long)pre[0].x;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int len = 1;
+    int cdf[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) cdf[i] = a.cd[sys * 8 + i];
+    int* jlog = s.jl + (long long)sys * s.kcap;
+    for (int t = 0; t < K; ++t) {
+      const int j = lj[t];
+      jlog[t] = j;
+      if (j >= 0) {
+        ++len;
+#pragma unroll
+        for (int i = 0; i < P; ++i) cdf[i] += (i == j);
+      }
+    }
+    s.ndef_try[sys] = *nd_s;
+    s.len_try[sys] = len;
+#pragma unroll
+    for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cdf[i];
+  }
+  cplx* mulog = s.mu + (long long)sys * s.kcap * P;
+  for (int e = tid; e < K * P; e += NT) mulog[e] = lmu[e];
+}
+
+// ------------------------------------------------------------ basis kernel
+// One absorbed step on a basis row held as c[d][i] = B[k][i][32 d + lane],
+// straight-line over NB blocks (column J is zero beyond them).  Blocks run
+// high to low so that block d-1 is still unmodified when block d shifts.
+template <int P, int DB, int NB, int J>
+TR_D void basis_step(cplx (&c)[DB][P], const cplx (&mu)[P], cplx msig, int lane) {
+#pragma unroll
+  for (int d = NB - 1; d >= 0; --d) {
+    const cplx oj = c[d][J];
+    const cplx ojm = d > 0 ? c[d - 1][J] : cmk(0.0, 0.0);
+    cplx up = shfl_c(lane == 31 ? ojm : oj, (lane + 31) & 31);
+    if (d == 0) up = lane == 0 ? cmk(0.0, 0.0) : up;
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      if (i != J) c[d][i] = cfma(mu[i], oj, c[d][i]);
+    c[d][J] = cfma(msig, oj, up);
+  }
+}
+
+template <int P, int DB, int NB>
+TR_D void basis_step_j(cplx (&c)[DB][P], int j, const cplx (&mu)[P], cplx msig, int lane) {
+  if (j == 0) basis_step<P, DB, NB, 0>(c, mu, msig, lane);
+  else if (j == 1) basis_step<P, DB, NB, 1>(c, mu, msig, lane);
+  else if (j == 2) basis_step<P, DB, NB, 2>(c, mu, msig, lane);
+  else if (j == 3) basis_step<P, DB, NB, 3>(c, mu, msig, lane);
+  else if constexpr (P == 5) {
+    basis_step<P, DB, NB, 4>(c, mu, msig, lane);
+  } else {
+    if (j == 4) basis_step<P, DB, NB, 4>(c, mu, msig, lane);
+    else if (j == 5) basis_step<P, DB, NB, 5>(c, mu, msig, lane);
+    else basis_step<P, DB, NB, 6>(c, mu, msig, lane);
+  }
+}
+
+struct RowState {
+  int dmax;   // structural degree of the row (max over its entries)
+  bool big;   // a coefficient passed the rescale trigger at a check point
+};
+
+// Steps t.. while the row fits in NB blocks; returns the first step that
+// needs more (or K).  deg[i] = structural degree of B[k][i] (-1: zero).
+template <int P, int DB, int NB>
+TR_D int run_steps(cplx (&c)[DB][P], int (&deg)[P], RowState& st, int t, int K, const int* jsm,
+                   const cplx* musm, const cplx* sgsm, int lane) {
+  for (; t < K; ++t) {
+    const int j = jsm[t];
+    cplx mu[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) mu[i] = musm[t * P + i];
+    const cplx msig = cneg(sgsm[t]);
+    if (j >= 0) {
+      const int dj = sel_i<P>(deg, j);
+      if (dj >= 0) {  // else column j of this row is zero: the step is a no-op here
+        const int nd = max(st.dmax, dj + 1);
+        if (nd / 32 + 1 > NB) return t;
+#pragma unroll
+        for (int i = 0; i < P; ++i) deg[i] = (i == j) ? dj + 1 : max(deg[i], dj);
+        st.dmax = nd;
+        basis_step_j<P, DB, NB>(c, j, mu, msig, lane);
+      }
+    }
+    if (((t + 1) % RESCALE_PERIOD) == 0) {
+      // the reference rescales when a coefficient passes the trigger here
+      bool b = false;
+#pragma unroll
+      for (int d = 0; d < NB; ++d)
+#pragma unroll
+        for (int i = 0; i < P; ++i) b |= cabs2(c[d][i]) > RESCALE_TRIGGER * RESCALE_TRIGGER;
+      st.big |= b;
+    }
+  }
+  return t;
+}
+
+template <int P, int DB>
+TR_D void build_row(cplx (&c)[DB][P], int k, RowState& st, int K, const int* jsm, const cplx* musm,
+                    const cplx* sgsm, int lane) {
+  int deg[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) deg[i] = i == k ? 0 : -1;
+  st.dmax = 0;
+  st.big = false;
+  int t = 0;
+  while (t < K) {
+    int need = st.dmax / 32 + 1;
+    const int j = jsm[t];
+    if (j >= 0) {
+      const int dj = sel_i<P>(deg, j);
+      if (dj >= 0) need = max(need, (dj + 1) / 32 + 1);
+    }
+#define TR_RUN(NB) \
+  case NB: if constexpr (NB <= DB) t = run_steps<P, DB, NB>(c, deg, st, t, K, jsm, musm, sgsm, lane); break;
+    switch (need) {
+      TR_RUN(1) TR_RUN(2) TR_RUN(3) TR_RUN(4) TR_RUN(5) TR_RUN(6) TR_RUN(7) TR_RUN(8) TR_RUN(9)
+      default: t = K; break;  // unreachable: need <= K/32 + 1 <= DB
+    }
+#undef TR_RUN
+  }
+}
+
+struct BasisSmem {
+  static size_t bytes(int K, int P, int M, int DB) {
+    return sizeof(cplx) * ((size_t)K * P + K + M + 32 * (size_t)DB + 2 * (size_t)P * P * M) +
+           sizeof(int) * (size_t)K;
+  }
+};
+
+template <int P, int DB>
+__global__ void __launch_bounds__(NT, 1) leaf_basis_kernel(LeafArgs a, SplitState s, int round) {
+  const int sys = blockIdx.x;
+  if (s.need[sys] != round) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(FULL, tid >> 5, 0);  // warp-uniform for ptxas (no collective shuffles)
+  TR_BTRACE(0);
+  constexpr int CAPR = 32 * DB;
+  const int K = a.K, M = a.M, rows = a.rows, cap = a.cap;
+  constexpr int PP = P * P;
+  cplx* musm = reinterpret_cast<cplx*>(smem_raw);  // [K][P]
+  cplx* sgsm = musm + (size_t)K * P;               // [K]
+  cplx* wtab = sgsm + K;                           // [M] exp(2 pi i q / M)
+  cplx* twl = wtab + M;                            // [CAPR] coset twist w_N^(o l)
+  cplx* gbuf = twl + CAPR;                         // [P*P][M] folded coefficients
+  cplx* vbuf = gbuf + (size_t)PP * M;              // [P*P][M] basis at one coset
+  int* jsm = reinterpret_cast<int*>(vbuf + (size_t)PP * M);  // [K]
+  __shared__ double red[8][8];
+  __shared__ double csafe[8];
+  __shared__ double wred[NW];
+  __shared__ int sviol;
+  const int att = round;
+
+  {
+    const cplx* mulog = s.mu + (long long)sys * s.kcap * P;
+    const int* jlog = s.jl + (long long)sys * s.kcap;
+    for (int e = tid; e < K; e += NT) {
+      jsm[e] = jlog[e];
+      sgsm[e] = __ldg(&a.twN[cond_node(a, e, att)]);
+    }
+    for (int e = tid; e < K * P; e += NT) musm[e] = mulog[e];
+    for (int e = tid; e < M; e += NT) wtab[e] = __ldg(&a.twN[(long long)e * a.stride]);
+    if (tid == 0) sviol = 0;
+  }
+  __syncthreads();
+  TR_BTRACE(1);
+
+  // ---- replay: warp k builds row k of the basis ----
+  cplx c[DB][P];
+#pragma unroll
+  for (int d = 0; d < DB; ++d)
+#pragma unroll
+    for (int i = 0; i < P; ++i) c[d][i] = cmk(0.0, 0.0);
+  if (warp < P) {
+    const int k = warp;
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      if (i == k && lane == 0) c[0][i] = cmk(1.0, 0.0);
+    RowState st;
+    build_row<P, DB>(c, k, st, K, jsm, musm, sgsm, lane);
+    TR_BTRACE(2);
+    if (__any_sync(FULL, st.big) && lane == 0) sviol = 1;
+    // column maxima of this row
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      double m = 0.0;
+#pragma unroll
+      for (int d = 0; d < DB; ++d) m = fmax(m, cabs2(c[d][i]));
+      m = wmax(m);
+      if (lane == 0) red[k][i] = m;
+    }
+  }
+  __syncthreads();
+  if (tid < P) {
+    double m = 0.0;
+    for (int k = 0; k < P; ++k) m = fmax(m, red[k][tid]);
+    m = sqrt(m);
+    csafe[tid] = m > 0.0 ? m : 1.0;
+  }
+  __syncthreads();
+  // normalise (ref tanint.py:179-183) and write the attempt's basis
+  cplx* dst = (round == 0 ? a.out : a.scratch) + (long long)sys * a.out_sys;
+  if (warp < P) {
+    const int k = warp;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const double inv = 1.0 / csafe[i];
+#pragma unroll
+      for (int d = 0; d < DB; ++d) {
+        const int l = 32 * d + lane;
+        if (l < cap) dst[(long long)(k * P + i) * cap + l] = cscale(c[d][i], inv);
+      }
+    }
+  }
+  if (cap > CAPR) {
+    const int tail = cap - CAPR;
+    for (int e = tid; e < PP * tail; e += NT) dst[(long long)(e / tail) * cap + CAPR + e % tail] = cmk(0.0, 0.0);
+  }
+  TR_BTRACE(3);
+
+  // ---- self-residual (ref tanint.py:262-270): fold + M-point DFT, all warps ----
+  const cplx* W = a.W + (long long)sys * a.w_sys;
+  const long long rowstride = (long long)rows * P;
+  double sc = 0.0;
+  for (int e = tid; e < K * P; e += NT) {
+    const int pos = e / (rows * P), rem = e % (rows * P);
+    sc = fmax(sc, cabs2(W[node_of(a, pos) * rowstride + rem]));
+  }
+  sc = wmax(sc);
+  if (lane == 0) wred[warp] = sc;
+  const int len = min(s.len_try[sys], cap);
+  double resm = 0.0;
+  for (int cs = 0; cs < a.noff; ++cs) {
+    const long long oc = cs ? a.o1 : a.o0;
+    for (int l = tid; l < len; l += NT) twl[l] = __ldg(&a.twN[(oc * l) % a.N]);
+    __syncthreads();  // also orders the basis writes above before the reads below
+    for (int e = tid; e < PP * M; e += NT) {
+      const int pq = e / M, q = e % M;
+      const cplx* src = dst + (long long)pq * cap;
+      cplx a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0);
+      int l = q;
+      for (; l + M < len; l += 2 * M) {
+        a0 = cfma(src[l], twl[l], a0);
+        a1 = cfma(src[l + M], twl[l + M], a1);
+      }
+      if (l < len) a0 = cfma(src[l], twl[l], a0);
+      gbuf[e] = cadd(a0, a1);
+    }
+    __syncthreads();
+    for (int e = tid; e < P * M; e += NT) {
+      const int k = e / M, t = e % M;
+      const cplx* g = gbuf + (size_t)k * P * M;
+      cplx acc[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc[i] = cmk(0.0, 0.0);
+      int kk = 0;
+      for (int q = 0; q < M; ++q) {
+        const cplx w = wtab[kk];
+#pragma unroll
+        for (int i = 0; i < P; ++i) acc[i] = cfma(g[i * M + q], w, acc[i]);
+        kk += t;
+        if (kk >= M) kk -= M;
+      }
+#pragma unroll
+      for (int i = 0; i < P; ++i) vbuf[(k * P + i) * M + t] = acc[i];
+    }
+    __syncthreads();
+    for (int e = tid; e < M * rows * P; e += NT) {
+      const int tt = e / (rows * P), rem = e % (rows * P);
+      const int rr = rem / P, jj = rem % P;
+      const cplx* wrow = W + (oc + a.stride * (long long)tt) * rowstride + rr * P;
+      cplx acc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc = cfma(wrow[i], vbuf[(i * P + jj) * M + tt], acc);
+      resm = fmax(resm, cabs2(acc));
+    }
+    __syncthreads();
+  }
+  double scale = 0.0;
+  for (int w = 0; w < NW; ++w) scale = fmax(scale, wred[w]);
+  scale = sqrt(scale);
+  __syncthreads();
+  resm = wmax(resm);
+  if (lane == 0) wred[warp] = resm;
+  __syncthreads();
+  double res = 0.0;
+  for (int w = 0; w < NW; ++w) res = fmax(res, wred[w]);
+  res = (scale == 0.0) ? 0.0 : sqrt(res) / scale;
+  TR_BTRACE(4);
+
+  // ---- best attempt, retry or commit (ref tanint.py:395-434) ----
+  double factor = 1.0;
+  for (int i = 0; i < P; ++i) factor = fmax(factor, csafe[i]);
+  const bool better = round == 0 || res < s.res_best[sys];
+  const int nd = s.ndef_try[sys];
+  if (better) {
+    if (round > 0) {
+      cplx* o = a.out + (long long)sys * a.out_sys;
+      for (long long e = tid; e < (long long)PP * cap; e += NT) o[e] = dst[e];
+    }
+    int2* db = s.def_best + (long long)sys * s.kcap;
+    const int2* dt = s.def_try + (long long)sys * s.kcap;
+    for (int e = tid; e < nd; e += NT) db[e] = dt[e];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    s.viol[sys] = sviol;
+    if (better) {
+      s.res_best[sys] = res;
+      s.ndef_best[sys] = nd;
+      s.factor_best[sys] = factor;
+      s.len_best[sys] = s.len_try[sys];
+      for (int i = 0; i < P; ++i) s.cd_best[sys * 8 + i] = s.cd_try[sys * 8 + i];
+    }
+    const bool done = s.res_best[sys] <= a.check_tol || round + 1 >= a.nattempts;
+    if (sviol) {
+      s.need[sys] = SPLIT_EXACT;  // speculation failed: exact coupled kernel
+    } else if (!done) {
+      s.need[sys] = round + 1;    // retry with the next absorption order
+    } else {
+      for (int i = 0; i < P; ++i) a.cd[sys * 8 + i] = s.cd_best[sys * 8 + i];
+      const int base = a.dcount[sys];
+      const int nb = s.ndef_best[sys];
+      const int room = a.dmax - base;
+      const int nput = nb < room ? nb : room;
+      const int2* db = s.def_best + (long long)sys * s.kcap;
+      for (int e = 0; e < nput; ++e) a.defer[(long long)sys * a.dmax + base + e] = db[e];
+      a.dcount[sys] = base + nb;
+      if (nb > room) a.status[sys] = 5;
+      a.max_scale[sys] = fmax(a.max_scale[sys], s.factor_best[sys]);
+      if (round > 0) a.retried[sys] += 1;
+      if (a.res_out) a.res_out[sys] = s.res_best[sys];
+      if (a.len_out) a.len_out[sys] = s.len_best[sys];
+      s.need[sys] = SPLIT_DONE;
+    }
+  }
+}
+
+__global__ void fast_need_reset_kernel(int* need, int nsys) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nsys) need[i] = 0;
+}
+
+int blocks_for(const LeafArgs& a) { return (a.K + 1 + 31) / 32; }
+constexpr int DB5 = 9, DB7 = 7;  // register blocks: K + 1 <= 288 (P = 5), 224 (P = 7)
+
+template <int P, int DB>
+int launch_basis(const LeafArgs& a, const SplitState& s, int round, int nsys, cudaStream_t st) {
+  const size_t smem = BasisSmem::bytes(a.K, P, a.M, DB);
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(leaf_basis_kernel<P, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    set = true;
+  }
+  TrKTimer _kt(TRK_LEAF_BUILD, st);
+  leaf_basis_kernel<P, DB><<<nsys, NT, smem, st>>>(a, s, round);
+  return 0;
+}
+
+}  // namespace
+
+bool leaf_fast_supported(const LeafArgs& a) {
+  if (a.P != 5 && a.P != 7) return false;
+  if (a.K < 2 || a.K > NT) return false;
+  const int db = a.P == 5 ? DB5 : DB7;
+  if (blocks_for(a) > db) return false;
+  return BasisSmem::bytes(a.K, a.P, a.M, db) <= 220 * 1024;
+}
+
+int leaf_fast_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t st) {
+  {
+    TrKTimer _kt(TRK_LEAF_PIVOT, st);
+    fast_need_reset_kernel<<<(nsys + 255) / 256, 256, 0, st>>>(s.need, nsys);
+  }
+  {  // algorithmic work of one attempt (retry rounds are extra work, not counted)
+    const double K = a.K, P = a.P;
+    tr_kernel_work(TRK_LEAF_PIVOT, 16.0 * nsys * K * P, 4.0 * nsys * P * K * (K - 1));
+    tr_kernel_work(TRK_LEAF_BUILD, 16.0 * nsys * (P * P * (K + 1) + K * P),
+                   4.0 * nsys * P * P * K * (K + 1) + 8.0 * nsys * (double)a.noff * P * P * a.M * a.M);
+  }
+  const size_t csm = sizeof(cplx) * ((size_t)a.K * a.P + a.K + 2) + sizeof(int) * (a.K + 2);
+  for (int round = 0; round < a.nattempts; ++round) {
+    {
+      TrKTimer _kt(TRK_LEAF_PIVOT, st);
+      if (a.P == 5) leaf_chain_kernel<5><<<nsys, NT, csm, st>>>(a, s, round);
+      else leaf_chain_kernel<7><<<nsys, NT, csm, st>>>(a, s, round);
+    }
+    const int rc = a.P == 5 ? launch_basis<5, DB5>(a, s, round, nsys, st)
+                            : launch_basis<7, DB7>(a, s, round, nsys, st);
+    if (rc) {
+      tr_set_error("leaf shape unsupported (K=%d, P=%d)", a.K, a.P);
+      return 2;
+    }
+  }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}

@@ -26,3 +26,7 @@ struct SplitState {
 
 bool leaf_split_supported(const LeafArgs& a);
 int leaf_split_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t st);
+
+// default path (leaf_fast.cu): chain kernel + fused basis / self-check kernel
+bool leaf_fast_supported(const LeafArgs& a);
+int leaf_fast_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t st);
