@@ -1,3 +1,4 @@
+#include <stdlib.h>
 #include <cmath>
 // Batched complex128 multi-pass Stockham FFT (see fft.cuh).
 #include "fft.cuh"
@@ -386,6 +387,8 @@ static int launch_pass(const FftPlan& p, int i, const cplx* in, long long in_ls,
     f.twR = ps.twR;
     f.sign = sign;
     const bool small = p.npass == 1 && ps.R <= 1024;
+    static const bool old_kernels = getenv("TR_FFT_OLD") != nullptr;
+    if (p.npass == 1 && !old_kernels && reg_launch(ps.log2, ps.q, f, st) == 0) return 0;
     if (fast_launch(ps.log2, ps.q, small, f, st) == 0) return 0;
   }
   PassArgs a;

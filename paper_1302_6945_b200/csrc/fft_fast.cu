@@ -6,6 +6,7 @@
 // the generic kernel in fft.cu.
 #include "fft.cuh"
 #include "fft_fast.cuh"
+#include "fft_bfly.cuh"
 
 namespace {
 
@@ -51,93 +52,6 @@ struct Geo {
 TR_D cplx twl(const cplx* t, int i, int sign) {
   cplx w = __ldg(&t[i]);
   return sign < 0 ? cconj(w) : w;
-}
-
-// cos / sin (2 pi k / RS) for RS = 5, 7 as literals
-template <int RS>
-TR_HD constexpr double tcos(int k) {
-  if (RS == 5) {
-    constexpr double c[5] = {1.0, 0.30901699437494742410, -0.80901699437494742410,
-                             -0.80901699437494742410, 0.30901699437494742410};
-    return c[k];
-  }
-  constexpr double c[7] = {1.0, 0.62348980185873353053, -0.22252093395631440429,
-                           -0.90096886790241912624, -0.90096886790241912624,
-                           -0.22252093395631440429, 0.62348980185873353053};
-  return c[k];
-}
-template <int RS>
-TR_HD constexpr double tsin(int k) {
-  if (RS == 5) {
-    constexpr double s[5] = {0.0, 0.95105651629515357212, 0.58778525229247312917,
-                             -0.58778525229247312917, -0.95105651629515357212};
-    return s[k];
-  }
-  constexpr double s[7] = {0.0, 0.78183148246802980871, 0.97492791218182360702,
-                           0.43388373911755812048, -0.43388373911755812048,
-                           -0.97492791218182360702, -0.78183148246802980871};
-  return s[k];
-}
-
-template <int RS>
-TR_D void bfly(cplx* a, int sign) {
-  if constexpr (RS == 2) {
-    cplx t = a[0];
-    a[0] = cadd(t, a[1]);
-    a[1] = csub(t, a[1]);
-  } else if constexpr (RS == 4) {
-    cplx t0 = cadd(a[0], a[2]), t1 = csub(a[0], a[2]);
-    cplx t2 = cadd(a[1], a[3]), d = csub(a[1], a[3]);
-    cplx t3 = sign > 0 ? cmk(-d.y, d.x) : cmk(d.y, -d.x);
-    a[0] = cadd(t0, t2);
-    a[2] = csub(t0, t2);
-    a[1] = cadd(t1, t3);
-    a[3] = csub(t1, t3);
-  } else if constexpr (RS == 8) {
-    cplx e[4] = {a[0], a[2], a[4], a[6]};
-    cplx o[4] = {a[1], a[3], a[5], a[7]};
-    bfly<4>(e, sign);
-    bfly<4>(o, sign);
-    const double c = 0.70710678118654752440;
-    const double s = (double)sign;
-    cplx o1 = cmk(c * (o[1].x - s * o[1].y), c * (o[1].y + s * o[1].x));
-    cplx o2 = cmk(-s * o[2].y, s * o[2].x);
-    cplx o3 = cmk(-c * (o[3].x + s * o[3].y), c * (s * o[3].x - o[3].y));
-    a[0] = cadd(e[0], o[0]);
-    a[4] = csub(e[0], o[0]);
-    a[1] = cadd(e[1], o1);
-    a[5] = csub(e[1], o1);
-    a[2] = cadd(e[2], o2);
-    a[6] = csub(e[2], o2);
-    a[3] = cadd(e[3], o3);
-    a[7] = csub(e[3], o3);
-  } else if constexpr (RS == 3) {
-    const double h = 0.86602540378443864676;  // sin(2 pi / 3)
-    cplx t1 = cadd(a[1], a[2]);
-    cplx t2 = cmk(a[0].x - 0.5 * t1.x, a[0].y - 0.5 * t1.y);
-    cplx d = csub(a[1], a[2]);
-    double s = h * (double)sign;
-    cplx t3 = cmk(-s * d.y, s * d.x);  // i * sign * sin * d
-    a[0] = cadd(a[0], t1);
-    a[1] = cadd(t2, t3);
-    a[2] = csub(t2, t3);
-  } else {
-    // direct DFT for radix 5 / 7 with constant twiddles
-    const double sg = (double)sign;
-    cplx y[RS];
-#pragma unroll
-    for (int v = 0; v < RS; ++v) {
-      cplx acc = a[0];
-#pragma unroll
-      for (int u = 1; u < RS; ++u) {
-        const int k = (u * v) % RS;
-        acc = cfma(a[u], cmk(tcos<RS>(k), sg * tsin<RS>(k)), acc);
-      }
-      y[v] = acc;
-    }
-#pragma unroll
-    for (int v = 0; v < RS; ++v) a[v] = y[v];
-  }
 }
 
 // one Stockham stage over every staged sub-transform

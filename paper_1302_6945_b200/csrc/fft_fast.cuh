@@ -22,3 +22,5 @@ bool fast_supported(int log2, int q);
 int fast_tile(int log2, int q);
 // returns 0 on launch, -1 when (log2, q) has no compiled kernel
 int fast_launch(int log2, int q, bool small, const FastArgs& a, cudaStream_t st);
+// register radix-16 single-pass kernel (fft_reg.cu); -1 when not applicable
+int reg_launch(int log2, int q, const FastArgs& a, cudaStream_t st);

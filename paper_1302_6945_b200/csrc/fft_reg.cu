@@ -1,0 +1,168 @@
+// Single-pass batched FFT, register radix-16 Stockham (lengths R = q 2^a <= 4096).
+//
+// One CTA of 256 threads transforms TL lines; T = 256 / TL threads share a
+// line.  Stage s (radix r, Ns = product of the earlier radices, B = R / r
+// butterflies) reads its r inputs b + u B, twiddles them by w^(u k) with
+// k = b mod Ns, runs the butterfly in registers and writes (b / Ns) Ns r +
+// k + u Ns (Stockham autosort: natural order in and out).  Stage 0 reads
+// straight from HBM and the last stage writes straight to HBM, both
+// coalesced; in between the data sits in shared memory, padded by one value
+// per 2^PSH so that the stride-r writes of the first stage are
+// conflict-free.  Radix-16 stages first, then the power-of-two remainder,
+// then the odd factors: 4096 = 16 16 16 is 3 stages and 2 smem round trips
+// (the pass kernels in fft_fast.cu need 4 stages and 5 round trips).
+// Twiddles come from the exp(2 pi i m / R) table (0.5 ulp, L1 resident).
+#include "fft.cuh"
+#include "fft_bfly.cuh"
+#include "fft_fast.cuh"
+
+namespace {
+
+constexpr int NTH = 256;
+
+__host__ __device__ constexpr int ilog2c(int x) {
+  int l = 0;
+  while ((1 << l) < x) ++l;
+  return l;
+}
+
+// radix plan: 16s, the power-of-two remainder, then the odd factors
+template <int LOG2, int Q>
+struct Plan {
+  static constexpr int R = Q << LOG2;
+  static constexpr int N16 = LOG2 / 4;
+  static constexpr int REM = 1 << (LOG2 % 4);       // 1, 2, 4, 8
+  static constexpr int NODD = Q == 1 ? 0 : (Q == 9 || Q == 15) ? 2 : 1;
+  static constexpr int NST = N16 + (REM > 1 ? 1 : 0) + NODD;
+  TR_HD static constexpr int radix(int s) {
+    return s < N16 ? 16
+         : (REM > 1 && s == N16) ? REM
+         : (Q == 9) ? 3
+         : (Q == 15) ? (s == NST - 2 ? 3 : 5)
+         : Q;
+  }
+  TR_HD static constexpr int ns(int s) {  // product of the radices before stage s
+    int p = 1;
+    for (int i = 0; i < s; ++i) p *= radix(i);
+    return p;
+  }
+  static constexpr int R0 = radix(0);
+  // pad one value per 2^PSH (first-stage write stride) when it is a power of two
+  static constexpr int PSH = (R0 & (R0 - 1)) == 0 ? ilog2c(R0) : 30;
+  static constexpr int Tq = (R + 15) / 16;
+  static constexpr int T = Tq >= NTH ? NTH : (1 << ilog2c(Tq));  // threads per line
+  static constexpr int TL = NTH / T;                              // lines per CTA
+  static constexpr int LS = R + (R >> PSH) + (T < 32 ? 1 : 0);    // smem per line
+};
+
+template <int RS>
+TR_D void tw_apply(cplx (&v)[RS], const cplx* twR, int k, int step, int sign) {
+#pragma unroll
+  for (int u = 1; u < RS; ++u) {
+    cplx w = __ldg(&twR[u * k * step]);
+    if (sign < 0) w.y = -w.y;
+    v[u] = cmul(v[u], w);
+  }
+}
+
+template <int LOG2, int Q, int S>
+TR_D void run_stage(cplx* sm, const FastArgs& a, long long lin, long long lout, bool live, int tb,
+                    int sign) {
+  using G = Plan<LOG2, Q>;
+  constexpr int R = G::R, r = G::radix(S), NS = G::ns(S), B = R / r, T = G::T;
+  constexpr int IT = (B + T - 1) / T;
+  constexpr bool FIRST = S == 0, LAST = S == G::NST - 1;
+  constexpr int PSH = G::PSH;
+  cplx v[IT][r];
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int b = tb + it * T;
+    if ((B % T == 0 || b < B) && live) {
+#pragma unroll
+      for (int u = 0; u < r; ++u) {
+        const int e = b + u * B;
+        if constexpr (FIRST) {
+          v[it][u] = e < a.in_len ? a.in[lin + e] : cmk(0.0, 0.0);
+        } else {
+          v[it][u] = sm[e + (e >> PSH)];
+        }
+      }
+      if constexpr (NS > 1) tw_apply<r>(v[it], a.twR, b % NS, R / (NS * r), sign);
+      bfly_any<r>(v[it], sign);
+    }
+  }
+  if constexpr (!FIRST || LAST) __syncthreads();  // reads done before in-place writes
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int b = tb + it * T;
+    if ((B % T == 0 || b < B) && live) {
+      const int k = b % NS;
+      const int base = (b / NS) * NS * r + k;
+#pragma unroll
+      for (int u = 0; u < r; ++u) {
+        const int o = base + u * NS;
+        if constexpr (LAST) {
+          a.out[lout + o] = v[it][u];
+        } else {
+          sm[o + (o >> PSH)] = v[it][u];
+        }
+      }
+    }
+  }
+  if constexpr (!LAST) {
+    __syncthreads();
+    run_stage<LOG2, Q, S + 1>(sm, a, lin, lout, live, tb, sign);
+  }
+}
+
+template <int LOG2, int Q>
+__global__ void __launch_bounds__(NTH) fft_reg_kernel(FastArgs a) {
+  using G = Plan<LOG2, Q>;
+  extern __shared__ __align__(16) unsigned char fsm[];
+  const int sl = threadIdx.x / G::T, tb = threadIdx.x % G::T;
+  const long long line = (long long)blockIdx.x * G::TL + sl;
+  const bool live = line < a.nsub;
+  cplx* sm = reinterpret_cast<cplx*>(fsm) + (size_t)sl * G::LS;
+  run_stage<LOG2, Q, 0>(sm, a, line * a.in_ls, line * a.out_ls, live, tb, a.sign);
+}
+
+template <int LOG2, int Q>
+int launch(const FastArgs& a, cudaStream_t st) {
+  if constexpr ((Q << LOG2) > 4096 || (Q << LOG2) < 2) {
+    return -1;
+  } else {
+    using G = Plan<LOG2, Q>;
+    const size_t smem = sizeof(cplx) * (size_t)G::TL * G::LS;
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(fft_reg_kernel<LOG2, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           100 * 1024);
+      set = true;
+    }
+    const long long blocks = (a.nsub + G::TL - 1) / G::TL;
+    TrKTimer _kt(TRK_FFT, st);
+    fft_reg_kernel<LOG2, Q><<<(unsigned)blocks, NTH, smem, st>>>(a);
+    return 0;
+  }
+}
+
+}  // namespace
+
+// single-pass transforms only (J == 1, Ns == 1): nsub = lines
+int reg_launch(int log2, int q, const FastArgs& a, cudaStream_t st) {
+  if (a.J != 1 || a.Ns != 1) return -1;
+#define TR_L(Q, L) \
+  case L: return launch<L, Q>(a, st);
+#define TR_Q(Q)                                                                   \
+  case Q: switch (log2) {                                                         \
+      TR_L(Q, 0) TR_L(Q, 1) TR_L(Q, 2) TR_L(Q, 3) TR_L(Q, 4) TR_L(Q, 5) TR_L(Q, 6) \
+      TR_L(Q, 7) TR_L(Q, 8) TR_L(Q, 9) TR_L(Q, 10) TR_L(Q, 11) TR_L(Q, 12)         \
+      default: return -1;                                                         \
+    }
+  switch (q) {
+    TR_Q(1) TR_Q(3) TR_Q(5) TR_Q(7) TR_Q(9) TR_Q(15)
+    default: return -1;
+  }
+#undef TR_Q
+#undef TR_L
+}

@@ -72,6 +72,20 @@ TR_D double wmax(double v) {
   return v;
 }
 TR_D int vload(const int* p) { return *(const volatile int*)p; }
+// release store / acquire load on a shared-memory flag (MEMBAR.ALL.CTA, lighter
+// than __threadfence_block's MEMBAR.SC.CTA)
+TR_D void st_release(int* p, int v) {
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v)
+               : "memory");
+}
+TR_D int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];"
+               : "=r"(v)
+               : "r"((unsigned)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
 TR_D cplx shfl_c(cplx v, int src) {
   return cmk(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src));
 }
@@ -119,10 +133,10 @@ TR_D void row_update(cplx (&r)[P], int j, const cplx* mu, cplx dsig) {
 // The pivot rule of ref tanint.py:193-211 on squared moduli: among the
 // lowest-degree columns the first of largest |phi|; deferred (-1) when that
 // is below thr * max|phi| or the row vanishes.  The argmax tree carries the
-// front and pre entries of the winning column along (fj, qj).
+// winning entry along (fj).
 template <int P>
 TR_D int chain_decide(const cplx (&f)[P], const cplx (&pre)[P], const int (&cd)[P], double thr2,
-                      cplx& fj, cplx& qj) {
+                      cplx& fj, cplx& qj, int& jj) {
   double v[P], am[P];
   int ix[P];
   cplx fv[P], pv[P];
@@ -151,8 +165,58 @@ TR_D int chain_decide(const cplx (&f)[P], const cplx (&pre)[P], const int (&cd)[
   }
   fj = fv[0];
   qj = pv[0];
+  jj = ix[0];
   if (am[0] == 0.0 || v[0] < thr2 * am[0]) return -1;
   return ix[0];
+}
+
+// One absorbed step with pivot J (compile time: no selects on the chain):
+// mu_i = -phi_i / phi_J (mu_J = 0),
+//   next front = pre + mu pre_J,  pre_J (s_pre - s_front) in column J;
+//   own rows   = r + mu r_J,      r_J (s_row - s_front) in column J.
+template <int P, int J>
+TR_D void chain_step(cplx (&f)[P], const cplx (&pre)[P], cplx (&r)[P], cplx (&mu)[P], int (&cd)[P],
+                     cplx dpf, cplx drf) {
+  const cplx fj = f[J];
+  const double inv2 = rcp_nr(cabs2(fj));
+  const cplx ci = cmk(-fj.x * inv2, fj.y * inv2);
+#pragma unroll
+  for (int i = 0; i < P; ++i) mu[i] = (i == J) ? cmk(0.0, 0.0) : cmul(f[i], ci);
+  const cplx qj = pre[J];
+  const cplx rj = r[J];
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    if (i == J) {
+      f[i] = cmul(qj, dpf);
+      r[i] = cmul(rj, drf);
+    } else {
+      f[i] = cfma(mu[i], qj, pre[i]);
+      r[i] = cfma(mu[i], rj, r[i]);
+    }
+  }
+  cd[J] += 1;
+}
+
+template <int P>
+TR_D void chain_step_any(int j, cplx (&f)[P], const cplx (&pre)[P], cplx (&r)[P], cplx (&mu)[P],
+                         int (&cd)[P], cplx dpf, cplx drf) {
+  if (j < 0) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      f[i] = pre[i];
+      mu[i] = cmk(0.0, 0.0);
+    }
+  } else if (j == 0) chain_step<P, 0>(f, pre, r, mu, cd, dpf, drf);
+  else if (j == 1) chain_step<P, 1>(f, pre, r, mu, cd, dpf, drf);
+  else if (j == 2) chain_step<P, 2>(f, pre, r, mu, cd, dpf, drf);
+  else if (j == 3) chain_step<P, 3>(f, pre, r, mu, cd, dpf, drf);
+  else if constexpr (P == 5) {
+    chain_step<P, 4>(f, pre, r, mu, cd, dpf, drf);
+  } else {
+    if (j == 4) chain_step<P, 4>(f, pre, r, mu, cd, dpf, drf);
+    else if (j == 5) chain_step<P, 5>(f, pre, r, mu, cd, dpf, drf);
+    else chain_step<P, 6>(f, pre, r, mu, cd, dpf, drf);
+  }
 }
 
 // ------------------------------------------------------------ chain kernel
@@ -166,7 +230,6 @@ __global__ void __launch_bounds__(NT) leaf_chain_kernel(LeafArgs a, SplitState s
   cplx* lsig = lmu + (size_t)K * P;                // [K + 2] node of every condition
   int* lj = reinterpret_cast<int*>(lsig + K + 2);  // [K] pivot or -1
   int* head = lj + K;                              // steps published
-  int* nd_s = head + 1;                            // deferrals so far (at hand-over)
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(FULL, tid >> 5, 0);  // warp-uniform for ptxas (no collective shuffles)
   const int att = round;
@@ -191,10 +254,7 @@ __global__ void __launch_bounds__(NT) leaf_chain_kernel(LeafArgs a, SplitState s
     for (int i = 0; i < P; ++i) r[i] = wr[i];
   }
   if (tid < 2) lsig[K + tid] = cmk(0.0, 0.0);
-  if (tid == 0) {
-    *head = 0;
-    *nd_s = 0;
-  }
+  if (tid == 0) *head = 0;
   __syncthreads();
 
   const int first = 32 * warp;
@@ -204,8 +264,7 @@ __global__ void __launch_bounds__(NT) leaf_chain_kernel(LeafArgs a, SplitState s
     int done = 0;
     while (done < first) {
       int h;
-      while ((h = vload(head)) <= done) __nanosleep(20);
-      __threadfence_block();
+      while ((h = ld_acquire(head)) <= done) __nanosleep(20);
       if (h > first) h = first;
       for (; done < h; ++done) {
         const int j = lj[done];
@@ -227,61 +286,54 @@ __global__ void __launch_bounds__(NT) leaf_chain_kernel(LeafArgs a, SplitState s
       pre[i] = shfl_c(r[i], 1);
     }
     cplx sf = lsig[first], sp = lsig[first + 1];
-    int nd = vload(nd_s);
     const bool trace = g_chain_trace_on && sys == 0 && round == 0 && lane == 0;
+#pragma unroll 2
     for (int tn = first; tn < last; ++tn) {
       const int ow = tn - first;
-      cplx fj, qj;
       if (trace) g_chain_trace[4 * tn] = clock64();
-      const int j = chain_decide<P>(f, pre, cd, thr2, fj, qj);
+      cplx fj, qj;
+      int jj;
+      const int j = chain_decide<P>(f, pre, cd, thr2, fj, qj, jj);
       if (trace) g_chain_trace[4 * tn + 1] = clock64() + 0 * j;
       cplx mu[P];
       if (j >= 0) {
-        // mu_i = -phi_i / phi_j (mu_j = 0), then branch-free
-        //   next front = pre + mu pre_j,   pre_j (s_p - s_f) in column j
-        //   own rows   = r   + mu r_j,     r_j (s_r - s_f)   in column j
+        // critical path: next front in pivot-scaled form (no division),
+        //   p_j pre_i - p_i pre_j (i != j),  p_j pre_j (s_pre - s_front),
+        // with p = phi 2^-e (exact power-of-two normalisation by the pivot)
+        const double mx = fmax(fabs(fj.x), fabs(fj.y));
+        const double sc = __hiloint2double((2046 - ((__double2hiint(mx) >> 20) & 0x7ff)) << 20, 0);
+        const cplx pj = cscale(fj, sc);
+        const cplx tj = cmul(pj, cmul(qj, csub(sp, sf)));
+        // off the path: mu_i = -phi_i / phi_j for the log and the own rows
         const double inv2 = rcp_nr(cabs2(fj));
         const cplx ci = cmk(-fj.x * inv2, fj.y * inv2);
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          const cplx m = cmul(f[i], ci);
-          mu[i] = (i == j) ? cmk(0.0, 0.0) : m;
-        }
-        const cplx nfj = cmul(qj, csub(sp, sf));
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          const cplx v = cfma(mu[i], qj, pre[i]);
-          f[i] = (i == j) ? nfj : v;
-        }
         const cplx rj = sel<P>(r, j);
         const cplx nrj = cmul(rj, csub(sg, sf));
 #pragma unroll
         for (int i = 0; i < P; ++i) {
+          const cplx nf = cmsub(pj, pre[i], cscale(f[i], sc), qj);
+          const cplx m = cmul(f[i], ci);
+          mu[i] = (i == j) ? cmk(0.0, 0.0) : m;
+          f[i] = (i == j) ? tj : nf;
           const cplx v = cfma(mu[i], rj, r[i]);
           r[i] = (i == j) ? nrj : v;
           cd[i] += (i == j);
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < P; ++i) f[i] = pre[i];
+        for (int i = 0; i < P; ++i) {
+          f[i] = pre[i];
+          mu[i] = cmk(0.0, 0.0);
+        }
       }
       if (trace) g_chain_trace[4 * tn + 2] = clock64() + 0 * (long long)f[0].x;
       if (lane == 0) {
         lj[tn] = j;
-        if (j >= 0) {
 #pragma unroll
-          for (int i = 0; i < P; ++i) lmu[tn * P + i] = mu[i];
-        } else {
-          dlog[nd] = make_int2((int)cond_node(a, tn, att), tn % rows);
-        }
+        for (int i = 0; i < P; ++i) lmu[tn * P + i] = mu[i];
       }
-      nd += (j < 0);
-      if ((ow & 3) == 3 || tn == last - 1) {
-        if (lane == 0) {
-          if (tn == last - 1) *(volatile int*)nd_s = nd;
-          __threadfence_block();
-          *(volatile int*)head = tn + 1;
-        }
+      if ((ow & 7) == 7 || ow >= 28 || tn == last - 1) {  // warp-uniform
+        if (lane == 0) st_release(head, tn + 1);
       }
       // pre <- row tn+2 through step tn (lane ow+2; unused past the warp's range)
 #pragma unroll
@@ -292,25 +344,31 @@ __global__ void __launch_bounds__(NT) leaf_chain_kernel(LeafArgs a, SplitState s
     }
   }
   __syncthreads();
-  if (tid == 0) {
-    int len = 1;
+  // epilogue (warp 0): pivot log, basis length, ledger, deferred conditions in
+  // step order (ref tanint.py:200-206)
+  if (warp == 0) {
+    int len = 1, nd = 0;
     int cdf[P];
 #pragma unroll
     for (int i = 0; i < P; ++i) cdf[i] = a.cd[sys * 8 + i];
     int* jlog = s.jl + (long long)sys * s.kcap;
-    for (int t = 0; t < K; ++t) {
-      const int j = lj[t];
-      jlog[t] = j;
-      if (j >= 0) {
-        ++len;
+    for (int base = 0; base < K; base += 32) {
+      const int t = base + lane;
+      const int j = t < K ? lj[t] : -2;
+      if (t < K) jlog[t] = j;
+      const unsigned def = __ballot_sync(FULL, j == -1);
+      len += __popc(__ballot_sync(FULL, j >= 0));
+      if (j == -1) dlog[nd + __popc(def & ((1u << lane) - 1u))] = make_int2((int)cond_node(a, t, att), t % rows);
+      nd += __popc(def);
 #pragma unroll
-        for (int i = 0; i < P; ++i) cdf[i] += (i == j);
-      }
+      for (int i = 0; i < P; ++i) cdf[i] += __popc(__ballot_sync(FULL, j == i));
     }
-    s.ndef_try[sys] = *nd_s;
-    s.len_try[sys] = len;
+    if (lane == 0) {
+      s.ndef_try[sys] = nd;
+      s.len_try[sys] = len;
 #pragma unroll
-    for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cdf[i];
+      for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cdf[i];
+    }
   }
   cplx* mulog = s.mu + (long long)sys * s.kcap * P;
   for (int e = tid; e < K * P; e += NT) mulog[e] = lmu[e];

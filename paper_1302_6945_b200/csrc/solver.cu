@@ -1148,13 +1148,12 @@ extern "C" int tr_fft(const double* in, double* out, int64_t n, int64_t lines, i
                       void* stream) {
   FftPlan fp;
   TR_TRY(fft_plan(n, &fp));
-  cplx* scratch = nullptr;
-  TR_CUDA_CHECK(cudaMalloc(&scratch, sizeof(cplx) * (size_t)n * lines));
   cudaStream_t st = (cudaStream_t)stream;
+  cplx* scratch = nullptr;  // stream-ordered pool allocation: no device sync
+  if (fp.npass > 1) TR_CUDA_CHECK(cudaMallocAsync((void**)&scratch, sizeof(cplx) * (size_t)n * lines, st));
   int rc = fft_exec(fp, reinterpret_cast<const cplx*>(in), n, n, reinterpret_cast<cplx*>(out), n,
                     scratch, lines, sign >= 0 ? 1 : -1, st);
-  cudaStreamSynchronize(st);
-  cudaFree(scratch);
+  if (scratch) TR_CUDA_CHECK(cudaFreeAsync(scratch, st));
   return rc;
 }
 
