@@ -1,3 +1,4 @@
+#include <tuple>
 #include <stdlib.h>
 #include <cmath>
 // Batched complex128 multi-pass Stockham FFT (see fft.cuh).
@@ -269,6 +270,33 @@ const cplx* twiddle_table(long long n) {
   return d;
 }
 
+// [N2][TL] table exp(2 pi i n2 l / n) (cached)
+const cplx* col_twiddles(long long n, long long N2, int TL) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::map<std::tuple<int, long long, long long, int>, cplx*> cache;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_tuple(dev, n, N2, TL);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  std::vector<cplx> h((size_t)(N2 * TL));
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (long long a = 0; a < N2; ++a)
+    for (int l = 0; l < TL; ++l) {
+      const long long m = (a * l) % n;
+      const long double ang = two_pi * (long double)m / (long double)n;
+      h[(size_t)(a * TL + l)] = cmk((double)cosl(ang), (double)sinl(ang));
+    }
+  cplx* d = nullptr;
+  if (cudaMalloc(&d, sizeof(cplx) * h.size()) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, h.data(), sizeof(cplx) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  cache[key] = d;
+  return d;
+}
+
 bool fft_supported(long long n) {
   if (n < 1) return false;
   return odd_part(n) <= FFT_MAX_ODD;
@@ -363,6 +391,35 @@ int fft_plan(long long n, FftPlan* out) {
     if (!ps.twR) { tr_set_error("twiddle table allocation failed (R=%d)", ps.R); return 4; }
     Ns *= ps.R;
   }
+  // two-pass column plan (fft_col.cu) when n = N1 N2 with both <= 1024
+  if (p.npass >= 2 && !getenv("TR_FFT_OLD")) {
+    int a = 0;
+    while ((p2 >> a) > 1) ++a;
+    int lq = 0;
+    while ((1LL << lq) < q) ++lq;
+    // balanced split first, then the nearest ones whose tiles divide the
+    // sub-transform counts (pass A tile | N2)
+    const int amid = (a + lq + 1) / 2;
+    for (int d = 0; d <= a && !p.col; ++d) {
+      for (int sgn = 0; sgn < 2 && !p.col; ++sgn) {
+        const int a1 = sgn ? amid + d : amid - d;
+        if (d == 0 && sgn) continue;
+        const int a2 = a - a1;
+        if (a1 < 1 || a2 < 0) continue;
+        const long long N1 = 1LL << a1, N2 = q << a2;
+        if (N1 > 1024 || N2 > 1024 || N1 * N2 != n) continue;
+        if (N2 % col_tile((int)N1) || N1 % col_tile((int)N2)) continue;
+        p.col = true;
+        p.a1 = a1;
+        p.a2 = a2;
+        p.q2 = (int)q;
+        p.tw1 = twiddle_table(N1);
+        p.tw2 = twiddle_table(N2);
+        p.twc = col_twiddles(n, N2, col_tile((int)N2));
+        if (!p.tw1 || !p.tw2 || !p.twc) { tr_set_error("twiddle table allocation failed"); return 4; }
+      }
+    }
+  }
   *out = p;
   return 0;
 }
@@ -429,6 +486,39 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
   const long long n = p.n;
   tr_kernel_work(TRK_FFT, 16.0 * lines * (double)(in_len + n),
                  5.0 * lines * (double)n * std::log2((double)n));
+  if (p.col) {
+    const long long N1 = 1LL << p.a1, N2 = (long long)p.q2 << p.a2;
+    ColArgs c;
+    c.in = in;
+    c.in_ls = in_ls;
+    c.in_len = in_len;
+    c.in_es = (int)N2;
+    c.out = scratch;
+    c.out_ls = n;
+    c.out_es = 1;
+    c.subs = (int)N2;
+    c.lines = lines;
+    c.twR = p.tw1;
+    c.twN = p.twN;
+    c.tw2 = p.twc;
+    c.sign = sign;
+    int rc = col_launch(true, p.a1, 1, c, st);
+    if (rc == 0) {
+      c.in = scratch;
+      c.in_ls = n;
+      c.in_len = n;
+      c.in_es = (int)N1;
+      c.out = out;
+      c.out_ls = out_ls;
+      c.out_es = (int)N1;
+      c.subs = (int)N1;
+      c.twR = p.tw2;
+      rc = col_launch(false, p.a2, p.q2, c, st);
+      if (rc) { tr_set_error("fft column plan has no kernel for n=%lld", n); return 2; }
+      TR_CUDA_CHECK(cudaGetLastError());
+      return 0;
+    }
+  }
   if (p.npass == 1) {
     launch_pass(p, 0, in, in_ls, in_len, out, out_ls, lines, sign, st);
   } else if (p.npass == 2) {

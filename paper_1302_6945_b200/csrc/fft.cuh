@@ -28,6 +28,12 @@ struct FftPlan {
   int npass = 0;
   FftPass pass[3];
   const cplx* twN = nullptr;  // table exp(2 pi i k / n)
+  // two-pass column plan n = N1 N2 (fft_col.cu), N1 = 2^a1, N2 = q 2^a2
+  bool col = false;
+  int a1 = 0, a2 = 0, q2 = 1;
+  const cplx* tw1 = nullptr;
+  const cplx* tw2 = nullptr;
+  const cplx* twc = nullptr;  // [N2][TL] exp(2 pi i n2 l / n) for pass B
 };
 
 // Plan (cached per device and length).  Returns 0 on success.

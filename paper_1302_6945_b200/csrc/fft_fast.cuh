@@ -24,3 +24,27 @@ int fast_tile(int log2, int q);
 int fast_launch(int log2, int q, bool small, const FastArgs& a, cudaStream_t st);
 // register radix-16 single-pass kernel (fft_reg.cu); -1 when not applicable
 int reg_launch(int log2, int q, const FastArgs& a, cudaStream_t st);
+
+// two-pass column/row kernels for n = N1 N2 (fft_col.cu)
+struct ColArgs {
+  const cplx* in;
+  long long in_ls, in_len;
+  int in_es;          // element stride inside a sub-transform
+  cplx* out;
+  long long out_ls;
+  int out_es;
+  int subs;           // sub-transforms per line
+  long long lines;
+  const cplx* twR;    // exp(2 pi i k / R)
+  const cplx* twN;    // exp(2 pi i k / n)
+  const cplx* tw2;    // pass B: exp(2 pi i n2 l / n), [N2][TL]
+  int sign;
+};
+// sub-transforms per CTA of the column kernels for transform length R
+inline int col_tile(int R) {
+  int p = 1;
+  while (p < R) p <<= 1;
+  int t = 4096 / p;
+  return t > 16 ? 16 : (t < 4 ? 4 : t);
+}
+int col_launch(bool pass_a, int log2, int q, const ColArgs& a, cudaStream_t st);

@@ -1,7 +1,7 @@
 // Single-pass batched FFT, register radix-16 Stockham (lengths R = q 2^a <= 4096).
 //
-// One CTA of 256 threads transforms TL lines; T = 256 / TL threads share a
-// line.  Stage s (radix r, Ns = product of the earlier radices, B = R / r
+// A CTA transforms TL lines with T threads each (T ~ R / 16, TL chosen at
+// launch).  Stage s (radix r, Ns = product of the earlier radices, B = R / r
 // butterflies) reads its r inputs b + u B, twiddles them by w^(u k) with
 // k = b mod Ns, runs the butterfly in registers and writes (b / Ns) Ns r +
 // k + u Ns (Stockham autosort: natural order in and out).  Stage 0 reads
@@ -51,7 +51,7 @@ struct Plan {
   static constexpr int PSH = (R0 & (R0 - 1)) == 0 ? ilog2c(R0) : 30;
   static constexpr int Tq = (R + 15) / 16;
   static constexpr int T = Tq >= NTH ? NTH : (1 << ilog2c(Tq));  // threads per line
-  static constexpr int TL = NTH / T;                              // lines per CTA
+  static constexpr int TLMAX = NTH / T;                           // lines per CTA (max)
   static constexpr int LS = R + (R >> PSH) + (T < 32 ? 1 : 0);    // smem per line
 };
 
@@ -115,12 +115,14 @@ TR_D void run_stage(cplx* sm, const FastArgs& a, long long lin, long long lout, 
   }
 }
 
+// CTA = TL lines x T threads (TL chosen at launch so small batches still
+// spread over the SMs)
 template <int LOG2, int Q>
-__global__ void __launch_bounds__(NTH) fft_reg_kernel(FastArgs a) {
+__global__ void __launch_bounds__(NTH) fft_reg_kernel(FastArgs a, int TL) {
   using G = Plan<LOG2, Q>;
   extern __shared__ __align__(16) unsigned char fsm[];
   const int sl = threadIdx.x / G::T, tb = threadIdx.x % G::T;
-  const long long line = (long long)blockIdx.x * G::TL + sl;
+  const long long line = (long long)blockIdx.x * TL + sl;
   const bool live = line < a.nsub;
   cplx* sm = reinterpret_cast<cplx*>(fsm) + (size_t)sl * G::LS;
   run_stage<LOG2, Q, 0>(sm, a, line * a.in_ls, line * a.out_ls, live, tb, a.sign);
@@ -132,16 +134,20 @@ int launch(const FastArgs& a, cudaStream_t st) {
     return -1;
   } else {
     using G = Plan<LOG2, Q>;
-    const size_t smem = sizeof(cplx) * (size_t)G::TL * G::LS;
+    // lines per CTA: as many as fit, but keep >= 2 CTAs per SM when the batch allows
+    int TL = G::TLMAX;
+    const int tlmin = G::T >= 32 ? 1 : 32 / G::T;  // whole warps
+    while (TL > tlmin && (a.nsub + TL - 1) / TL < 2 * 148) TL >>= 1;
+    const size_t smem = sizeof(cplx) * (size_t)TL * G::LS;
     static bool set = false;
     if (!set) {
       cudaFuncSetAttribute(fft_reg_kernel<LOG2, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            100 * 1024);
       set = true;
     }
-    const long long blocks = (a.nsub + G::TL - 1) / G::TL;
+    const long long blocks = (a.nsub + TL - 1) / TL;
     TrKTimer _kt(TRK_FFT, st);
-    fft_reg_kernel<LOG2, Q><<<(unsigned)blocks, NTH, smem, st>>>(a);
+    fft_reg_kernel<LOG2, Q><<<(unsigned)blocks, G::T * TL, smem, st>>>(a, TL);
     return 0;
   }
 }

@@ -1150,6 +1150,17 @@ extern "C" int tr_fft(const double* in, double* out, int64_t n, int64_t lines, i
   TR_TRY(fft_plan(n, &fp));
   cudaStream_t st = (cudaStream_t)stream;
   cplx* scratch = nullptr;  // stream-ordered pool allocation: no device sync
+  static bool pool_set = false;
+  if (!pool_set) {  // keep freed pool memory for the next call
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_set = true;
+  }
   if (fp.npass > 1) TR_CUDA_CHECK(cudaMallocAsync((void**)&scratch, sizeof(cplx) * (size_t)n * lines, st));
   int rc = fft_exec(fp, reinterpret_cast<const cplx*>(in), n, n, reinterpret_cast<cplx*>(out), n,
                     scratch, lines, sign >= 0 ? 1 : -1, st);
