@@ -17,6 +17,7 @@ struct LeafArgs {
   int M;                // nodes per coset
   int count;            // leaf nodes = noff * M
   int K;                // conditions = rows * count
+  int dbound = 0;       // planned structural degree of the leaf basis (0: unknown)
   // absorption orders
   int nattempts;
   int ord_stride[4];    // perm[i] = (i * s) % count   (ord_reverse: use reversed)

@@ -219,9 +219,51 @@ TR_D void chain_step_any(int j, cplx (&f)[P], const cplx (&pre)[P], cplx (&r)[P]
   }
 }
 
+// decision only (winning entry carried along)
+template <int P>
+TR_D int chain_decide1(const cplx (&f)[P], const int (&cd)[P], double thr2, cplx& fj) {
+  double v[P], am[P];
+  int ix[P];
+  cplx fv[P];
+  int dmin = cd[0];
+#pragma unroll
+  for (int i = 1; i < P; ++i) dmin = min(dmin, cd[i]);
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    am[i] = cabs2(f[i]);
+    v[i] = cd[i] == dmin ? am[i] : -1.0;
+    ix[i] = i;
+    fv[i] = f[i];
+  }
+#pragma unroll
+  for (int w = 1; w < P; w *= 2) {
+#pragma unroll
+    for (int i = 0; i + w < P; i += 2 * w) {
+      const bool take = v[i + w] > v[i];
+      ix[i] = take ? ix[i + w] : ix[i];
+      v[i] = take ? v[i + w] : v[i];
+      fv[i] = take ? fv[i + w] : fv[i];
+      am[i] = fmax(am[i], am[i + w]);
+    }
+  }
+  fj = fv[0];
+  if (am[0] == 0.0 || v[0] < thr2 * am[0]) return -1;
+  return ix[0];
+}
+
+// decider multipliers for pivot J (compile time): mu_i = -phi_i / phi_J, mu_J = 0
+template <int P, int J>
+TR_D void decider_mu(const cplx (&f)[P], cplx (&mu)[P], int (&cd)[P], cplx fj) {
+  const double inv2 = rcp_nr(cabs2(fj));
+  const cplx ci = cmk(-fj.x * inv2, fj.y * inv2);
+#pragma unroll
+  for (int i = 0; i < P; ++i) mu[i] = (i == J) ? cmk(0.0, 0.0) : cmul(f[i], ci);
+  cd[J] += 1;
+}
+
 // ------------------------------------------------------------ chain kernel
 template <int P>
-__global__ void __launch_bounds__(NT) leaf_chain_kernel(LeafArgs a, SplitState s, int round) {
+__global__ void __launch_bounds__(NT, 2) leaf_chain_kernel(LeafArgs a, SplitState s, int round) {
   const int sys = blockIdx.x;
   if (s.need[sys] != round) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -374,6 +416,232 @@ __global__ void __launch_bounds__(NT) leaf_chain_kernel(LeafArgs a, SplitState s
   for (int e = tid; e < K * P; e += NT) mulog[e] = lmu[e];
 }
 
+// ---------------------------------------------- chain kernel, warp-specialised
+// Warp 0 (the decider) owns the chain: it keeps the row being decided
+// ("front", row t through step t-1) and the next one ("pre", row t+1 through
+// t-1) replicated in its lanes, decides step t, forms mu_t, publishes
+// (j_t, mu_t) and updates pre into the next front.  Warps 1..H (holders) own
+// 32 rows each and apply every published step to their rows; the holder of
+// row t+2 hands it back (through step t) for the decider's next pre.  The
+// hand-offs are named barriers (bar.arrive by the producer, bar.sync by the
+// consumers: ~70 cycles one way, with memory ordering), so the decider never
+// polls and never updates rows it does not need.
+//   barriers 1/3 (step t published, t even/odd): decider + the holders still
+//     needed at step t;
+//   barriers 2/4 (row t+2 handed back after step t): decider + its holder.
+// The decider consumes the hand-back of step t-1 only at the end of step t,
+// so the holders' round trip overlaps a whole decision.
+TR_D void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+TR_D void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Pivot rule on the bit patterns of the squared moduli (non-negative doubles
+// order like their bits): integer compares and selects instead of FP64
+// ones; the winning entry and its squared modulus are carried along.
+template <int P>
+TR_D int decide_bits(const cplx (&f)[P], const int (&cd)[P], double thr2, cplx& fj, double& a2j) {
+  unsigned long long v[P], am[P];
+  int ix[P];
+  cplx fv[P];
+  int dmin = cd[0];
+#pragma unroll
+  for (int i = 1; i < P; ++i) dmin = min(dmin, cd[i]);
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(cabs2(f[i]));
+    am[i] = b;
+    v[i] = cd[i] == dmin ? b : 0ull;
+    ix[i] = i;
+    fv[i] = f[i];
+  }
+#pragma unroll
+  for (int w = 1; w < P; w *= 2) {
+#pragma unroll
+    for (int i = 0; i + w < P; i += 2 * w) {
+      const bool take = v[i + w] > v[i];
+      ix[i] = take ? ix[i + w] : ix[i];
+      v[i] = take ? v[i + w] : v[i];
+      fv[i] = take ? fv[i + w] : fv[i];
+      am[i] = am[i] > am[i + w] ? am[i] : am[i + w];
+    }
+  }
+  fj = fv[0];
+  a2j = __longlong_as_double((long long)v[0]);
+  const double amax = __longlong_as_double((long long)am[0]);
+  if (amax == 0.0 || a2j < thr2 * amax) return -1;
+  return ix[0];
+}
+
+template <int P, bool SPREAD>
+__global__ void __launch_bounds__(SPREAD ? 352 : 288, SPREAD ? 1 : 2) leaf_chain2_kernel(LeafArgs a, SplitState s, int round) {
+  const int sys = blockIdx.x;
+  if (s.need[sys] != round) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = a.K, rows = a.rows;
+  // log of step t: the decided row phi_t (lf), c_t = -conj(phi_j)/|phi_j|^2
+  // (lci) and j_t; the multipliers are mu_i = phi_i c_t (mu_j = 0)
+  cplx* lf = reinterpret_cast<cplx*>(smem_raw);    // [K][P]
+  cplx* lci = lf + (size_t)K * P;                  // [K]
+  cplx* lsig = lci + K;                            // [K + 2] node of every condition
+  cplx* prow = lsig + K + 2;                       // [2][P] handed-back rows
+  int* lj = reinterpret_cast<int*>(prow + 2 * P);  // [K] pivot or -1
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(FULL, tid >> 5, 0);  // warp-uniform for ptxas
+  const int att = round;
+  const cplx* W = a.W + (long long)sys * a.w_sys;
+  const long long rowstride = (long long)rows * P;
+  int2* dlog = s.def_try + (long long)sys * s.kcap;
+  const int H = (K + 31) / 32;  // holder warps
+  // holders live on warps 1, 2, 3, 5, 6, 7, 9, 10 (never warp_id = 0 mod 4, the
+  // decider's scheduler); holder h >= 1 owns conditions 32 (h - 1) + lane
+  // (SPREAD, for one CTA per SM) or on warps 1..H (compact, two CTAs per SM)
+  const int hid = SPREAD ? ((warp & 3) ? warp - warp / 4 : 0) : warp;
+  const int mine = 32 * (hid - 1) + lane;
+  cplx r[P];
+  cplx sg = cmk(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
+  if (hid >= 1 && mine < K) {
+    const long long node = cond_node(a, mine, att);
+    sg = __ldg(&a.twN[node]);
+    lsig[mine] = sg;
+    const cplx* wr = W + node * rowstride + (mine % rows) * P;
+#pragma unroll
+    for (int i = 0; i < P; ++i) r[i] = wr[i];
+  }
+  if (tid < 2) lsig[K + tid] = cmk(0.0, 0.0);
+  __syncthreads();
+
+  // participants of barrier 1 at step t: the decider and holders h >= hmin
+  auto hmin = [&](int t) { return (t + 2) / 32 + 1; };
+  auto nbar1 = [&](int t) { return 32 * (1 + H - hmin(t) + 1); };
+
+  if (warp == 0) {
+    // ---------------- decider ----------------
+    const double thr2 = a.thr * a.thr;
+    int cd[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
+    cplx f[P], pre[P];
+    {
+      const long long n0 = cond_node(a, 0, att);
+      const cplx* w0 = W + n0 * rowstride;
+#pragma unroll
+      for (int i = 0; i < P; ++i) f[i] = w0[i];
+      if (K > 1) {
+        const long long n1 = cond_node(a, 1, att);
+        const cplx* w1 = W + n1 * rowstride + (1 % rows) * P;
+#pragma unroll
+        for (int i = 0; i < P; ++i) pre[i] = w1[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < P; ++i) pre[i] = cmk(0.0, 0.0);
+      }
+    }
+    cplx sf = lsig[0], sp = lsig[1];
+    const bool trace = g_chain_trace_on && sys == 0 && round == 0 && lane == 0;
+    for (int t = 0; t < K; ++t) {
+      if (trace) g_chain_trace[4 * t] = clock64();
+      cplx fj;
+      double a2j;
+      const int j = decide_bits<P>(f, cd, thr2, fj, a2j);
+      const double inv2 = rcp_nr(a2j);
+      const cplx ci = cmk(-fj.x * inv2, fj.y * inv2);
+      if (trace) g_chain_trace[4 * t + 1] = clock64() + 0 * j;
+      if (lane == 0) {
+        lj[t] = j;
+        lci[t] = ci;
+#pragma unroll
+        for (int i = 0; i < P; ++i) lf[t * P + i] = f[i];
+      }
+      // step t to the holders (barrier ids alternate: the decider runs one
+      // step ahead of the hand-back)
+      if (t + 2 < K) bar_arrive(1 + 2 * (t & 1), nbar1(t));
+      if (t + 1 < K) {
+        if (t >= 1) {  // pre <- row t+1 through step t-1 (holder step t-1)
+          bar_sync(2 + 2 * ((t - 1) & 1), 64);
+          if (trace) g_chain_trace[4 * t + 2] = clock64();
+          const cplx* src = prow + ((t - 1) & 1) * P;
+#pragma unroll
+          for (int i = 0; i < P; ++i) pre[i] = src[i];
+        }
+        // next front: row t+1 through step t = pre + phi (c q_j), q_j (s_p - s_f) in column j
+        const cplx qj = sel<P>(pre, j);
+        const cplx c2 = cmul(ci, qj);
+        const cplx nfj = cmul(qj, csub(sp, sf));
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const cplx v = cfma(f[i], c2, pre[i]);
+          f[i] = (j < 0) ? pre[i] : (i == j) ? nfj : v;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < P; ++i) cd[i] += (i == j);
+      sf = sp;
+      sp = lsig[t + 2];
+      if (trace) g_chain_trace[4 * t + 3] = clock64() + 0 * (long long)f[0].x;
+    }
+  } else if (hid >= 1 && hid <= H) {
+    // ---------------- holder ----------------
+    for (int t = 0; t + 2 < K && hid >= hmin(t); ++t) {
+      bar_sync(1 + 2 * (t & 1), nbar1(t));
+      const int j = lj[t];
+      if (j >= 0) {
+        // r <- r + phi (c r_j), r_j (s_r - s_t) in column j
+        const cplx rj = sel<P>(r, j);
+        const cplx c2 = cmul(lci[t], rj);
+        const cplx nj = cmul(rj, csub(sg, lsig[t]));
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const cplx v = cfma(lf[t * P + i], c2, r[i]);
+          r[i] = (i == j) ? nj : v;
+        }
+      }
+      if (hid == hmin(t)) {
+        if (lane == (t + 2) % 32) {
+          cplx* dst = prow + (t & 1) * P;
+#pragma unroll
+          for (int i = 0; i < P; ++i) dst[i] = r[i];
+        }
+        bar_arrive(2 + 2 * (t & 1), 64);
+      }
+    }
+  }
+  __syncthreads();
+  // epilogue (warp 0): pivot log, basis length, ledger, deferred conditions in
+  // step order (ref tanint.py:200-206)
+  if (warp == 0) {
+    int len = 1, nd = 0;
+    int cdf[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) cdf[i] = a.cd[sys * 8 + i];
+    int* jlog = s.jl + (long long)sys * s.kcap;
+    for (int base = 0; base < K; base += 32) {
+      const int t = base + lane;
+      const int j = t < K ? lj[t] : -2;
+      if (t < K) jlog[t] = j;
+      const unsigned def = __ballot_sync(FULL, j == -1);
+      len += __popc(__ballot_sync(FULL, j >= 0));
+      if (j == -1) dlog[nd + __popc(def & ((1u << lane) - 1u))] = make_int2((int)cond_node(a, t, att), t % rows);
+      nd += __popc(def);
+#pragma unroll
+      for (int i = 0; i < P; ++i) cdf[i] += __popc(__ballot_sync(FULL, j == i));
+    }
+    if (lane == 0) {
+      s.ndef_try[sys] = nd;
+      s.len_try[sys] = len;
+#pragma unroll
+      for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cdf[i];
+    }
+  }
+  // multipliers for the basis replay: mu_i = phi_i c (mu_j = 0)
+  cplx* mulog = s.mu + (long long)sys * s.kcap * P;
+  for (int e = tid; e < K * P; e += blockDim.x) {
+    const int t = e / P, i = e - t * P;
+    const int j = lj[t];
+    mulog[e] = (j < 0 || i == j) ? cmk(0.0, 0.0) : cmul(lf[e], lci[t]);
+  }
+}
+
 // ------------------------------------------------------------ basis kernel
 // One absorbed step on a basis row held as c[d][i] = B[k][i][32 d + lane],
 // straight-line over NB blocks (column J is zero beyond them).  Blocks run
@@ -466,9 +734,13 @@ TR_D void build_row(cplx (&c)[DB][P], int k, RowState& st, int K, const int* jsm
     }
 #define TR_RUN(NB) \
   case NB: if constexpr (NB <= DB) t = run_steps<P, DB, NB>(c, deg, st, t, K, jsm, musm, sgsm, lane); break;
+    if (need > DB) {  // the basis outgrew the planned register blocks
+      st.big = true;    // -> exact coupled kernel
+      break;
+    }
     switch (need) {
       TR_RUN(1) TR_RUN(2) TR_RUN(3) TR_RUN(4) TR_RUN(5) TR_RUN(6) TR_RUN(7) TR_RUN(8) TR_RUN(9)
-      default: t = K; break;  // unreachable: need <= K/32 + 1 <= DB
+      default: t = K; break;
     }
 #undef TR_RUN
   }
@@ -482,7 +754,7 @@ struct BasisSmem {
 };
 
 template <int P, int DB>
-__global__ void __launch_bounds__(NT, 1) leaf_basis_kernel(LeafArgs a, SplitState s, int round) {
+__global__ void __launch_bounds__(NT, (DB <= 3 ? 2 : 1)) leaf_basis_kernel(LeafArgs a, SplitState s, int round) {
   const int sys = blockIdx.x;
   if (s.need[sys] != round) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -697,6 +969,14 @@ __global__ void fast_need_reset_kernel(int* need, int nsys) {
 
 int blocks_for(const LeafArgs& a) { return (a.K + 1 + 31) / 32; }
 constexpr int DB5 = 9, DB7 = 7;  // register blocks: K + 1 <= 288 (P = 5), 224 (P = 7)
+// blocks for this leaf: the planned structural degree plus slack (a leaf that
+// outgrows them is redone by the exact kernel), at most what K allows
+int blocks_planned(const LeafArgs& a) {
+  const int full = blocks_for(a);
+  if (a.dbound <= 0) return full;
+  const int b = (a.dbound + 8) / 32 + 1;
+  return b < full ? b : full;
+}
 
 template <int P, int DB>
 int launch_basis(const LeafArgs& a, const SplitState& s, int round, int nsys, cudaStream_t st) {
@@ -711,13 +991,29 @@ int launch_basis(const LeafArgs& a, const SplitState& s, int round, int nsys, cu
   return 0;
 }
 
+template <int P>
+int dispatch_basis(const LeafArgs& a, const SplitState& s, int round, int nsys, cudaStream_t st) {
+  switch (blocks_planned(a)) {
+    case 1: return launch_basis<P, 1>(a, s, round, nsys, st);
+    case 2: return launch_basis<P, 2>(a, s, round, nsys, st);
+    case 3: return launch_basis<P, 3>(a, s, round, nsys, st);
+    case 4: return launch_basis<P, 4>(a, s, round, nsys, st);
+    case 5: return launch_basis<P, 5>(a, s, round, nsys, st);
+    case 6: return launch_basis<P, 6>(a, s, round, nsys, st);
+    case 7: return launch_basis<P, 7>(a, s, round, nsys, st);
+    case 8: if constexpr (P == 5) return launch_basis<P, 8>(a, s, round, nsys, st); else return -1;
+    case 9: if constexpr (P == 5) return launch_basis<P, 9>(a, s, round, nsys, st); else return -1;
+    default: return -1;
+  }
+}
+
 }  // namespace
 
 bool leaf_fast_supported(const LeafArgs& a) {
   if (a.P != 5 && a.P != 7) return false;
   if (a.K < 2 || a.K > NT) return false;
-  const int db = a.P == 5 ? DB5 : DB7;
-  if (blocks_for(a) > db) return false;
+  const int db = blocks_planned(a);
+  if (db > (a.P == 5 ? DB5 : DB7)) return false;
   return BasisSmem::bytes(a.K, a.P, a.M, db) <= 220 * 1024;
 }
 
@@ -733,14 +1029,32 @@ int leaf_fast_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStrea
                    4.0 * nsys * P * P * K * (K + 1) + 8.0 * nsys * (double)a.noff * P * P * a.M * a.M);
   }
   const size_t csm = sizeof(cplx) * ((size_t)a.K * a.P + a.K + 2) + sizeof(int) * (a.K + 2);
+  const size_t csm2 = sizeof(cplx) * ((size_t)a.K * a.P + 2 * a.K + 2 + 2 * a.P) + sizeof(int) * a.K;
+  const int hk = (a.K + 31) / 32;  // holder warps
+  // one CTA per SM when the batch fits the GPU: holders off the decider's
+  // scheduler; otherwise the compact layout, two CTAs per SM
+  const bool spread = nsys <= 148;
+  const int nth2 = 32 * (1 + hk + (spread ? (hk - 1) / 3 : 0));
+  static const char* cv = getenv("TR_CHAIN");  // TR_CHAIN=relay: previous chain kernel
+  const bool relay = cv && cv[0] == 'r';
   for (int round = 0; round < a.nattempts; ++round) {
     {
       TrKTimer _kt(TRK_LEAF_PIVOT, st);
-      if (a.P == 5) leaf_chain_kernel<5><<<nsys, NT, csm, st>>>(a, s, round);
-      else leaf_chain_kernel<7><<<nsys, NT, csm, st>>>(a, s, round);
+      if (relay) {
+        if (a.P == 5) leaf_chain_kernel<5><<<nsys, NT, csm, st>>>(a, s, round);
+        else leaf_chain_kernel<7><<<nsys, NT, csm, st>>>(a, s, round);
+      } else {
+        if (a.P == 5) {
+          if (spread) leaf_chain2_kernel<5, true><<<nsys, nth2, csm2, st>>>(a, s, round);
+          else leaf_chain2_kernel<5, false><<<nsys, nth2, csm2, st>>>(a, s, round);
+        } else {
+          if (spread) leaf_chain2_kernel<7, true><<<nsys, nth2, csm2, st>>>(a, s, round);
+          else leaf_chain2_kernel<7, false><<<nsys, nth2, csm2, st>>>(a, s, round);
+        }
+      }
     }
-    const int rc = a.P == 5 ? launch_basis<5, DB5>(a, s, round, nsys, st)
-                            : launch_basis<7, DB7>(a, s, round, nsys, st);
+    const int rc = a.P == 5 ? dispatch_basis<5>(a, s, round, nsys, st)
+                            : dispatch_basis<7>(a, s, round, nsys, st);
     if (rc) {
       tr_set_error("leaf shape unsupported (K=%d, P=%d)", a.K, a.P);
       return 2;

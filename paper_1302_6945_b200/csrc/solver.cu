@@ -208,6 +208,7 @@ struct Op {
   int slot_out = -1, slot_a = -1, slot_b = -1;
   long long cap_a = 0, cap_b = 0, cap_out = 0, R = 0;
   int K = 0, count = 0, M = 0, depth = 0;
+  int dbound = 0;  // leaf: structural basis degree under water-filling, no deferrals
   int nattempts = 1;
   int ord_stride[4] = {1, 1, 1, 1};
   int ord_rev[4] = {0, 0, 0, 0};
@@ -258,7 +259,32 @@ int opt_extend_detail(long long n_tilde, long long n_lim, int rows, bool paired,
 struct Builder {
   Plan& pl;
   std::vector<int> ms;  // degree multiset (sorted)
+  std::vector<int> deg; // the same degrees per column (pivot: lowest-index minimum)
   explicit Builder(Plan& p) : pl(p) {}
+
+  // Structural degree of a leaf basis: replay the water-filling pivots on the
+  // degree pattern of every basis row (entry degrees, -1 = zero).
+  int leaf_dbound(int K) {
+    const int P = (int)deg.size();
+    std::vector<std::vector<int>> sd(P, std::vector<int>(P, -1));
+    for (int k = 0; k < P; ++k) sd[k][k] = 0;
+    int D = 0;
+    for (int t = 0; t < K; ++t) {
+      int j = 0;
+      for (int i = 1; i < P; ++i)
+        if (deg[i] < deg[j]) j = i;
+      deg[j] += 1;
+      for (int k = 0; k < P; ++k) {
+        const int dj = sd[k][j];
+        if (dj < 0) continue;
+        for (int i = 0; i < P; ++i)
+          if (i != j) sd[k][i] = std::max(sd[k][i], dj);
+        sd[k][j] = dj + 1;
+        D = std::max(D, dj + 1);
+      }
+    }
+    return D;
+  }
 
   void waterfill(long long steps) {
     for (long long s = 0; s < steps; ++s) {
@@ -339,6 +365,7 @@ struct Builder {
         op.ord_stride[3] = s0;
         op.ord_rev[3] = 1;
       }
+      op.dbound = leaf_dbound((int)count);
       pl.ops.push_back(op);
       pl.leaves += 1;
       pl.Kmax = std::max<long long>(pl.Kmax, count);
@@ -439,6 +466,7 @@ int get_plan(const tr_desc* d, Plan** out) {
   }
   Builder b(*p);
   for (long long t : p->tau) b.ms.push_back((int)-t);
+  b.deg = b.ms;
   std::sort(b.ms.begin(), b.ms.end());
   int root = b.slot_for(1, 0);
   p->root_slot = root;
@@ -765,6 +793,7 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
       la.M = op.M;
       la.count = op.count;
       la.K = op.K;
+      la.dbound = op.dbound;
       la.nattempts = op.nattempts;
       for (int i = 0; i < 4; ++i) {
         la.ord_stride[i] = op.ord_stride[i];

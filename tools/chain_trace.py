@@ -22,8 +22,9 @@ f(0, C.addressof(buf), 4096)
 K = tb.plan_info(probs[0])["max_leaf_conditions"]
 a = np.frombuffer(buf, dtype=np.int64).reshape(-1, 4)[:K]
 step = np.diff(a[:, 0])
+a = a[1:K - 1]; step = step[1:K - 2]
 dec = a[:, 1] - a[:, 0]; upd = a[:, 2] - a[:, 1]; pub = a[:, 3] - a[:, 2]
-print("K", K, "mean step cycles %.0f  decide %.0f  update %.0f  publish+shfl %.0f" % (
+print("K", K, "mean step cycles %.0f  decide+ci %.0f  log+arrive+sync-wait %.0f  pre+front %.0f" % (
     step.mean(), dec.mean(), upd.mean(), pub.mean()))
 print("per-step:", step[:40].tolist())
 print("handover steps (32k-1 -> 32k):", [int(step[i]) for i in range(31, K - 1, 32)])
