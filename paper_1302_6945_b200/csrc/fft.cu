@@ -302,16 +302,39 @@ bool fft_supported(long long n) {
   return odd_part(n) <= FFT_MAX_ODD;
 }
 
+// measured cost per element of tr_fft on B200 (tools/fft_sweep.py, 8M-element batches)
+static const struct { long long n; double c; } kFftCost[] = {
+    {16, 0.0145}, {18, 0.0102}, {20, 0.0074}, {24, 0.0091}, {28, 0.0094}, {30, 0.0105},
+    {32, 0.0083}, {36, 0.0075}, {40, 0.0079}, {48, 0.0067}, {56, 0.0077}, {60, 0.0085},
+    {64, 0.0069}, {72, 0.0071}, {80, 0.0067}, {96, 0.0067}, {112, 0.0064}, {120, 0.0079},
+    {128, 0.0057}, {144, 0.0069}, {160, 0.0076}, {192, 0.0069}, {224, 0.0072}, {240, 0.0071},
+    {256, 0.0060}, {288, 0.0084}, {320, 0.0083}, {384, 0.0078}, {448, 0.0082}, {480, 0.0091},
+    {512, 0.0083}, {576, 0.0087}, {640, 0.0091}, {768, 0.0082}, {896, 0.0086}, {960, 0.0091},
+    {1024, 0.0093}, {1152, 0.0096}, {1280, 0.0093}, {1536, 0.0100}, {1792, 0.0090}, {1920, 0.0096},
+    {2048, 0.0106}, {2304, 0.0103}, {2560, 0.0113}, {3072, 0.0113}, {3584, 0.0109}, {3840, 0.0099},
+    {4096, 0.0120}, {4608, 0.0297}, {5120, 0.0304}, {6144, 0.0370}, {7168, 0.0270}, {7680, 0.0267},
+    {8192, 0.0321}, {9216, 0.0246}, {10240, 0.0290}, {12288, 0.0227}, {14336, 0.0252}, {15360, 0.0209},
+    {16384, 0.0233}, {18432, 0.0227}, {20480, 0.0293}, {24576, 0.0221}, {28672, 0.0249}, {30720, 0.0189},
+    {32768, 0.0236}, {36864, 0.0224}, {40960, 0.0196}, {49152, 0.0215}, {57344, 0.0178}, {61440, 0.0185},
+    {65536, 0.0186}, {73728, 0.0225}, {81920, 0.0196}, {98304, 0.0215}, {114688, 0.0177}, {122880, 0.0183},
+    {131072, 0.0184},
+};
+
 long long fft_good_len(long long n) {
   if (n <= 1) return 1;
-  // candidates 2^a * q, q in a small odd set; cost ~ len * (log2 len + q/4)
+  // candidates 2^a * q, q in a small odd set; ranked by the measured cost of
+  // this library's kernels (len * cost per element), else len (log2 len + q / 4)
   static const int qs[] = {1, 3, 5, 7, 9, 15};
   long long best = -1;
   double best_cost = 1e300;
   for (int q : qs) {
     long long len = q;
     while (len < n) len *= 2;
-    double cost = (double)len * (log2((double)len) + 0.25 * q);
+    double per = -1.0;
+    for (const auto& e : kFftCost)
+      if (e.n == len) per = e.c;
+    const double cost = per > 0.0 ? (double)len * per
+                                  : (double)len * (log2((double)len) + 0.25 * q) * 1e-3;
     if (cost < best_cost) { best_cost = cost; best = len; }
   }
   return best;

@@ -123,8 +123,37 @@ TR_D void bfly16(cplx* a, int sign) {
   }
 }
 
+// radix 9 = 3 x 3 with the W9 twiddles in between (output in natural order)
+TR_D void bfly9(cplx* a, int sign) {
+  const double s = (double)sign;
+  // cos / sin (2 pi e / 9), e = 1, 2, 4
+  const double c1 = 0.76604444311897803520, s1 = 0.64278760968653932632;
+  const double c2 = 0.17364817766693034885, s2 = 0.98480775301220805936;
+  const double c4 = -0.93969262078590838405, s4 = 0.34202014332566873304;
+  cplx y[3][3];
+#pragma unroll
+  for (int n2 = 0; n2 < 3; ++n2) {
+    cplx t[3] = {a[n2], a[3 + n2], a[6 + n2]};
+    bfly<3>(t, sign);
+#pragma unroll
+    for (int k1 = 0; k1 < 3; ++k1) y[n2][k1] = t[k1];
+  }
+  y[1][1] = cmul(y[1][1], cmk(c1, s * s1));
+  y[1][2] = cmul(y[1][2], cmk(c2, s * s2));
+  y[2][1] = cmul(y[2][1], cmk(c2, s * s2));
+  y[2][2] = cmul(y[2][2], cmk(c4, s * s4));
+#pragma unroll
+  for (int k1 = 0; k1 < 3; ++k1) {
+    cplx t[3] = {y[0][k1], y[1][k1], y[2][k1]};
+    bfly<3>(t, sign);
+#pragma unroll
+    for (int k2 = 0; k2 < 3; ++k2) a[k1 + 3 * k2] = t[k2];
+  }
+}
+
 template <int RS>
 TR_D void bfly_any(cplx* a, int sign) {
   if constexpr (RS == 16) bfly16(a, sign);
+  else if constexpr (RS == 9) bfly9(a, sign);
   else bfly<RS>(a, sign);
 }

@@ -32,12 +32,11 @@ struct Plan {
   static constexpr int R = Q << LOG2;
   static constexpr int N16 = LOG2 / 4;
   static constexpr int REM = 1 << (LOG2 % 4);       // 1, 2, 4, 8
-  static constexpr int NODD = Q == 1 ? 0 : (Q == 9 || Q == 15) ? 2 : 1;
+  static constexpr int NODD = Q == 1 ? 0 : Q == 15 ? 2 : 1;
   static constexpr int NST = N16 + (REM > 1 ? 1 : 0) + NODD;
   TR_HD static constexpr int radix(int s) {
     return s < N16 ? 16
          : (REM > 1 && s == N16) ? REM
-         : (Q == 9) ? 3
          : (Q == 15) ? (s == NST - 2 ? 3 : 5)
          : Q;
   }

@@ -661,6 +661,25 @@ TR_D void basis_step(cplx (&c)[DB][P], const cplx (&mu)[P], cplx msig, int lane)
   }
 }
 
+// the same step with a run-time pivot: selects instead of a dispatch
+template <int P, int DB, int NB>
+TR_D void basis_step_sel(cplx (&c)[DB][P], int j, const cplx (&mu)[P], cplx msig, int lane) {
+  cplx m[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) m[i] = (i == j) ? msig : mu[i];
+  cplx oj[NB];
+#pragma unroll
+  for (int d = 0; d < NB; ++d) oj[d] = sel<P>(c[d], j);
+#pragma unroll
+  for (int d = NB - 1; d >= 0; --d) {
+    const cplx ojm = d > 0 ? oj[d - 1] : cmk(0.0, 0.0);
+    cplx up = shfl_c(lane == 31 ? ojm : oj[d], (lane + 31) & 31);
+    if (d == 0) up = lane == 0 ? cmk(0.0, 0.0) : up;
+#pragma unroll
+    for (int i = 0; i < P; ++i) c[d][i] = cfma(m[i], oj[d], (i == j) ? up : c[d][i]);
+  }
+}
+
 template <int P, int DB, int NB>
 TR_D void basis_step_j(cplx (&c)[DB][P], int j, const cplx (&mu)[P], cplx msig, int lane) {
   if (j == 0) basis_step<P, DB, NB, 0>(c, mu, msig, lane);
@@ -751,10 +770,13 @@ struct BasisSmem {
     return sizeof(cplx) * ((size_t)K * P + K + M + 32 * (size_t)DB + 2 * (size_t)P * P * M) +
            sizeof(int) * (size_t)K;
   }
+  // + the normalised basis staged for the self-check fold
+  static size_t staged(int P, int DB) { return sizeof(cplx) * (size_t)P * P * 32 * DB; }
 };
 
 template <int P, int DB>
-__global__ void __launch_bounds__(NT, (DB <= 3 ? 2 : 1)) leaf_basis_kernel(LeafArgs a, SplitState s, int round) {
+__global__ void __launch_bounds__(NT, (DB <= 3 ? 2 : 1)) leaf_basis_kernel(LeafArgs a, SplitState s, int round,
+                                                                           int stage) {
   const int sys = blockIdx.x;
   if (s.need[sys] != round) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -771,6 +793,8 @@ __global__ void __launch_bounds__(NT, (DB <= 3 ? 2 : 1)) leaf_basis_kernel(LeafA
   cplx* gbuf = twl + CAPR;                         // [P*P][M] folded coefficients
   cplx* vbuf = gbuf + (size_t)PP * M;              // [P*P][M] basis at one coset
   int* jsm = reinterpret_cast<int*>(vbuf + (size_t)PP * M);  // [K]
+  // [P*P][CAPR] normalised basis (when staged), 16-byte aligned after jsm
+  cplx* cbuf = reinterpret_cast<cplx*>(smem_raw + (((size_t)((unsigned char*)(jsm + K) - smem_raw) + 15) & ~(size_t)15));
   __shared__ double red[8][8];
   __shared__ double csafe[8];
   __shared__ double wred[NW];
@@ -834,7 +858,9 @@ __global__ void __launch_bounds__(NT, (DB <= 3 ? 2 : 1)) leaf_basis_kernel(LeafA
 #pragma unroll
       for (int d = 0; d < DB; ++d) {
         const int l = 32 * d + lane;
-        if (l < cap) dst[(long long)(k * P + i) * cap + l] = cscale(c[d][i], inv);
+        const cplx v = cscale(c[d][i], inv);
+        if (l < cap) dst[(long long)(k * P + i) * cap + l] = v;
+        if (stage) cbuf[(k * P + i) * CAPR + l] = v;
       }
     }
   }
@@ -854,7 +880,9 @@ __global__ void __launch_bounds__(NT, (DB <= 3 ? 2 : 1)) leaf_basis_kernel(LeafA
   }
   sc = wmax(sc);
   if (lane == 0) wred[warp] = sc;
-  const int len = min(s.len_try[sys], cap);
+  // coefficients past the register blocks are zero (an overflow went to the
+  // exact kernel), so the staged fold stops at CAPR
+  const int len = min(min(s.len_try[sys], cap), stage ? CAPR : cap);
   double resm = 0.0;
   for (int cs = 0; cs < a.noff; ++cs) {
     const long long oc = cs ? a.o1 : a.o0;
@@ -862,7 +890,7 @@ __global__ void __launch_bounds__(NT, (DB <= 3 ? 2 : 1)) leaf_basis_kernel(LeafA
     __syncthreads();  // also orders the basis writes above before the reads below
     for (int e = tid; e < PP * M; e += NT) {
       const int pq = e / M, q = e % M;
-      const cplx* src = dst + (long long)pq * cap;
+      const cplx* src = stage ? cbuf + (size_t)pq * CAPR : dst + (long long)pq * cap;
       cplx a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0);
       int l = q;
       for (; l + M < len; l += 2 * M) {
@@ -980,14 +1008,20 @@ int blocks_planned(const LeafArgs& a) {
 
 template <int P, int DB>
 int launch_basis(const LeafArgs& a, const SplitState& s, int round, int nsys, cudaStream_t st) {
-  const size_t smem = BasisSmem::bytes(a.K, P, a.M, DB);
+  size_t smem = BasisSmem::bytes(a.K, P, a.M, DB);
+  // stage the basis in shared memory for the check when it still fits the
+  // kernel's CTAs per SM
+  const size_t limit = DB <= 3 ? 110 * 1024 : 220 * 1024;
+  const size_t with = ((smem + 15) & ~(size_t)15) + BasisSmem::staged(P, DB);
+  const int stage = with <= limit ? 1 : 0;
+  if (stage) smem = with;
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(leaf_basis_kernel<P, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     set = true;
   }
   TrKTimer _kt(TRK_LEAF_BUILD, st);
-  leaf_basis_kernel<P, DB><<<nsys, NT, smem, st>>>(a, s, round);
+  leaf_basis_kernel<P, DB><<<nsys, NT, smem, st>>>(a, s, round, stage);
   return 0;
 }
 

@@ -19,10 +19,17 @@ __global__ void twist_fold_kernel(cplx* G, const cplx* B, long long b_sys, long 
   long long oc = c ? o1 : o0;
   const cplx* src = B + sys * b_sys + (long long)e * b_cap;
   cplx acc = cmk(0.0, 0.0);
-  for (long long l = q; l < L; l += cnt) {
-    cplx v = src[l];
-    if (oc) v = cmul(v, __ldg(&twN[(oc * l) % N]));
-    acc = cadd(acc, v);
+  if (oc == 0) {
+    for (long long l = q; l < L; l += cnt) acc = cadd(acc, src[l]);
+  } else {
+    // twist index oc l mod N, stepped by oc cnt < N (no 64-bit modulo in the loop)
+    long long idx = (oc * q) % N;
+    const long long step = (oc * cnt) % N;
+    for (long long l = q; l < L; l += cnt) {
+      acc = cfma(src[l], __ldg(&twN[idx]), acc);
+      idx += step;
+      if (idx >= N) idx -= N;
+    }
   }
   G[((sys * noff + c) * PP + e) * cnt + q] = acc;
 }
