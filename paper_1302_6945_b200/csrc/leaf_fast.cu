@@ -774,6 +774,177 @@ struct BasisSmem {
   static size_t staged(int P, int DB) { return sizeof(cplx) * (size_t)P * P * 32 * DB; }
 };
 
+// Column normalisation, basis write-out, self-check and best-attempt
+// bookkeeping of one attempt (ref tanint.py:179-183, :262-270, :395-434).
+// Warp `row >= 0` holds basis row `row` in c; every thread of the CTA calls.
+template <int P, int DB>
+TR_D void finish_attempt(const LeafArgs& a, const SplitState& s, int round, int sys, cplx (&c)[DB][P], int row,
+                         int stage, cplx* wtab, cplx* twl, cplx* gbuf, cplx* vbuf, cplx* cbuf,
+                         double (*red)[8], double* csafe, double* wred, int* sviol, int nw) {
+  constexpr int CAPR = 32 * DB;
+  constexpr int PP = P * P;
+  const int K = a.K, M = a.M, rows = a.rows, cap = a.cap;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+  if (row >= 0) {
+    // column maxima of this row
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      double m = 0.0;
+#pragma unroll
+      for (int d = 0; d < DB; ++d) m = fmax(m, cabs2(c[d][i]));
+      m = wmax(m);
+      if (lane == 0) red[row][i] = m;
+    }
+  }
+  __syncthreads();
+  if (tid < P) {
+    double m = 0.0;
+    for (int k = 0; k < P; ++k) m = fmax(m, red[k][tid]);
+    m = sqrt(m);
+    csafe[tid] = m > 0.0 ? m : 1.0;
+  }
+  __syncthreads();
+  // normalise and write the attempt's basis
+  cplx* dst = (round == 0 ? a.out : a.scratch) + (long long)sys * a.out_sys;
+  if (row >= 0) {
+    const int k = row;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const double inv = 1.0 / csafe[i];
+#pragma unroll
+      for (int d = 0; d < DB; ++d) {
+        const int l = 32 * d + lane;
+        const cplx v = cscale(c[d][i], inv);
+        if (l < cap) dst[(long long)(k * P + i) * cap + l] = v;
+        if (stage) cbuf[(k * P + i) * CAPR + l] = v;
+      }
+    }
+  }
+  if (cap > CAPR) {
+    const int tail = cap - CAPR;
+    for (int e = tid; e < PP * tail; e += nt) dst[(long long)(e / tail) * cap + CAPR + e % tail] = cmk(0.0, 0.0);
+  }
+
+  // ---- self-residual: fold + M-point DFT, all warps ----
+  const cplx* W = a.W + (long long)sys * a.w_sys;
+  const long long rowstride = (long long)rows * P;
+  double sc = 0.0;
+  for (int e = tid; e < K * P; e += nt) {
+    const int pos = e / (rows * P), rem = e % (rows * P);
+    sc = fmax(sc, cabs2(W[node_of(a, pos) * rowstride + rem]));
+  }
+  sc = wmax(sc);
+  if (lane == 0) wred[warp] = sc;
+  // coefficients past the register blocks are zero (an overflow went to the
+  // exact kernel), so the staged fold stops at CAPR
+  const int len = min(min(s.len_try[sys], cap), stage ? CAPR : cap);
+  double resm = 0.0;
+  for (int cs = 0; cs < a.noff; ++cs) {
+    const long long oc = cs ? a.o1 : a.o0;
+    for (int l = tid; l < len; l += nt) twl[l] = __ldg(&a.twN[(oc * l) % a.N]);
+    __syncthreads();  // also orders the basis writes above before the reads below
+    for (int e = tid; e < PP * M; e += nt) {
+      const int pq = e / M, q = e % M;
+      const cplx* src = stage ? cbuf + (size_t)pq * CAPR : dst + (long long)pq * cap;
+      cplx a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0);
+      int l = q;
+      for (; l + M < len; l += 2 * M) {
+        a0 = cfma(src[l], twl[l], a0);
+        a1 = cfma(src[l + M], twl[l + M], a1);
+      }
+      if (l < len) a0 = cfma(src[l], twl[l], a0);
+      gbuf[e] = cadd(a0, a1);
+    }
+    __syncthreads();
+    for (int e = tid; e < P * M; e += nt) {
+      const int k = e / M, t = e % M;
+      const cplx* g = gbuf + (size_t)k * P * M;
+      cplx acc[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc[i] = cmk(0.0, 0.0);
+      int kk = 0;
+      for (int q = 0; q < M; ++q) {
+        const cplx w = wtab[kk];
+#pragma unroll
+        for (int i = 0; i < P; ++i) acc[i] = cfma(g[i * M + q], w, acc[i]);
+        kk += t;
+        if (kk >= M) kk -= M;
+      }
+#pragma unroll
+      for (int i = 0; i < P; ++i) vbuf[(k * P + i) * M + t] = acc[i];
+    }
+    __syncthreads();
+    for (int e = tid; e < M * rows * P; e += nt) {
+      const int tt = e / (rows * P), rem = e % (rows * P);
+      const int rr = rem / P, jj = rem % P;
+      const cplx* wrow = W + (oc + a.stride * (long long)tt) * rowstride + rr * P;
+      cplx acc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc = cfma(wrow[i], vbuf[(i * P + jj) * M + tt], acc);
+      resm = fmax(resm, cabs2(acc));
+    }
+    __syncthreads();
+  }
+  double scale = 0.0;
+  for (int w = 0; w < nw; ++w) scale = fmax(scale, wred[w]);
+  scale = sqrt(scale);
+  __syncthreads();
+  resm = wmax(resm);
+  if (lane == 0) wred[warp] = resm;
+  __syncthreads();
+  double res = 0.0;
+  for (int w = 0; w < nw; ++w) res = fmax(res, wred[w]);
+  res = (scale == 0.0) ? 0.0 : sqrt(res) / scale;
+
+  // ---- best attempt, retry or commit ----
+  double factor = 1.0;
+  for (int i = 0; i < P; ++i) factor = fmax(factor, csafe[i]);
+  const bool better = round == 0 || res < s.res_best[sys];
+  const int nd = s.ndef_try[sys];
+  if (better) {
+    if (round > 0) {
+      cplx* o = a.out + (long long)sys * a.out_sys;
+      for (long long e = tid; e < (long long)PP * cap; e += nt) o[e] = dst[e];
+    }
+    int2* db = s.def_best + (long long)sys * s.kcap;
+    const int2* dt = s.def_try + (long long)sys * s.kcap;
+    for (int e = tid; e < nd; e += nt) db[e] = dt[e];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int viol = *sviol;
+    s.viol[sys] = viol;
+    if (better) {
+      s.res_best[sys] = res;
+      s.ndef_best[sys] = nd;
+      s.factor_best[sys] = factor;
+      s.len_best[sys] = s.len_try[sys];
+      for (int i = 0; i < P; ++i) s.cd_best[sys * 8 + i] = s.cd_try[sys * 8 + i];
+    }
+    const bool done = s.res_best[sys] <= a.check_tol || round + 1 >= a.nattempts;
+    if (viol) {
+      s.need[sys] = SPLIT_EXACT;  // speculation failed: exact coupled kernel
+    } else if (!done) {
+      s.need[sys] = round + 1;    // retry with the next absorption order
+    } else {
+      for (int i = 0; i < P; ++i) a.cd[sys * 8 + i] = s.cd_best[sys * 8 + i];
+      const int base = a.dcount[sys];
+      const int nb = s.ndef_best[sys];
+      const int room = a.dmax - base;
+      const int nput = nb < room ? nb : room;
+      const int2* db = s.def_best + (long long)sys * s.kcap;
+      for (int e = 0; e < nput; ++e) a.defer[(long long)sys * a.dmax + base + e] = db[e];
+      a.dcount[sys] = base + nb;
+      if (nb > room) a.status[sys] = 5;
+      a.max_scale[sys] = fmax(a.max_scale[sys], s.factor_best[sys]);
+      if (round > 0) a.retried[sys] += 1;
+      if (a.res_out) a.res_out[sys] = s.res_best[sys];
+      if (a.len_out) a.len_out[sys] = s.len_best[sys];
+      s.need[sys] = SPLIT_DONE;
+    }
+  }
+}
+
 template <int P, int DB>
 __global__ void __launch_bounds__(NT, (DB <= 3 ? 2 : 1)) leaf_basis_kernel(LeafArgs a, SplitState s, int round,
                                                                            int stage) {
@@ -830,164 +1001,274 @@ __global__ void __launch_bounds__(NT, (DB <= 3 ? 2 : 1)) leaf_basis_kernel(LeafA
     build_row<P, DB>(c, k, st, K, jsm, musm, sgsm, lane);
     TR_BTRACE(2);
     if (__any_sync(FULL, st.big) && lane == 0) sviol = 1;
-    // column maxima of this row
-#pragma unroll
-    for (int i = 0; i < P; ++i) {
-      double m = 0.0;
-#pragma unroll
-      for (int d = 0; d < DB; ++d) m = fmax(m, cabs2(c[d][i]));
-      m = wmax(m);
-      if (lane == 0) red[k][i] = m;
+  }
+  finish_attempt<P, DB>(a, s, round, sys, c, warp < P ? warp : -1, stage, wtab, twl, gbuf, vbuf, cbuf, red,
+                        csafe, wred, &sviol, NW);
+}
+
+// ------------------------------------------------- fused attempt (one kernel)
+// For batches that fit the GPU with one CTA per SM: the decider + holder
+// chain of leaf_chain2_kernel plus P basis warps that replay each published
+// step on their basis row (in the shadow of the chain: they sync on the same
+// step barrier), then the normalisation and self-check of finish_attempt.
+// Warps: 0 decider; then on warp ids != 0 mod 4 the H holders and the P basis
+// rows.  Per step a basis row applies mu_i = phi_i c to its coefficient blocks.
+template <int P, int DB, int NB>
+TR_D int fused_steps(cplx (&c)[DB][P], int (&deg)[P], RowState& st, int t, int& synced, int lim, int K,
+                     int H, const int* lj, const cplx* lf, const cplx* lci, const cplx* lsig, int lane) {
+  for (; t < lim; ++t) {
+    if (t + 2 < K && synced <= t) {  // step t published (barrier 1/3)
+      const int hm = (t + 2) / 32 + 1;
+      bar_sync(1 + 2 * (t & 1), 32 * (1 + H - hm + 1 + P));
+      synced = t + 1;
     }
-  }
-  __syncthreads();
-  if (tid < P) {
-    double m = 0.0;
-    for (int k = 0; k < P; ++k) m = fmax(m, red[k][tid]);
-    m = sqrt(m);
-    csafe[tid] = m > 0.0 ? m : 1.0;
-  }
-  __syncthreads();
-  // normalise (ref tanint.py:179-183) and write the attempt's basis
-  cplx* dst = (round == 0 ? a.out : a.scratch) + (long long)sys * a.out_sys;
-  if (warp < P) {
-    const int k = warp;
+    const int j = lj[t];
+    if (j >= 0) {
+      const int dj = sel_i<P>(deg, j);
+      if (dj >= 0) {
+        const int nd = max(st.dmax, dj + 1);
+        if (nd / 32 + 1 > NB) return t;
 #pragma unroll
-    for (int i = 0; i < P; ++i) {
-      const double inv = 1.0 / csafe[i];
+        for (int i = 0; i < P; ++i) deg[i] = (i == j) ? dj + 1 : max(deg[i], dj);
+        st.dmax = nd;
+        const cplx ci = lci[t];
+        cplx mu[P];
 #pragma unroll
-      for (int d = 0; d < DB; ++d) {
-        const int l = 32 * d + lane;
-        const cplx v = cscale(c[d][i], inv);
-        if (l < cap) dst[(long long)(k * P + i) * cap + l] = v;
-        if (stage) cbuf[(k * P + i) * CAPR + l] = v;
+        for (int i = 0; i < P; ++i) mu[i] = cmul(lf[t * P + i], ci);
+        basis_step_j<P, DB, NB>(c, j, mu, cneg(lsig[t]), lane);
       }
     }
+    if (((t + 1) % RESCALE_PERIOD) == 0) {
+      bool b = false;
+#pragma unroll
+      for (int d = 0; d < NB; ++d)
+#pragma unroll
+        for (int i = 0; i < P; ++i) b |= cabs2(c[d][i]) > RESCALE_TRIGGER * RESCALE_TRIGGER;
+      st.big |= b;
+    }
   }
-  if (cap > CAPR) {
-    const int tail = cap - CAPR;
-    for (int e = tid; e < PP * tail; e += NT) dst[(long long)(e / tail) * cap + CAPR + e % tail] = cmk(0.0, 0.0);
-  }
-  TR_BTRACE(3);
+  return t;
+}
 
-  // ---- self-residual (ref tanint.py:262-270): fold + M-point DFT, all warps ----
+template <int P, int DB>
+__global__ void __launch_bounds__(512, 1) leaf_fused_kernel(LeafArgs a, SplitState s, int round, int stage) {
+  const int sys = blockIdx.x;
+  if (s.need[sys] != round) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int CAPR = 32 * DB;
+  const int K = a.K, rows = a.rows, M = a.M;
+  cplx* lf = reinterpret_cast<cplx*>(smem_raw);    // [K][P] decided rows
+  cplx* lci = lf + (size_t)K * P;                  // [K]
+  cplx* lsig = lci + K;                            // [K + 2]
+  cplx* prow = lsig + K + 2;                       // [2][P]
+  cplx* wtab = prow + 2 * P;                       // [M]
+  cplx* twl = wtab + M;                            // [CAPR]
+  cplx* gbuf = twl + CAPR;                         // [P*P][M]
+  cplx* vbuf = gbuf + (size_t)P * P * M;           // [P*P][M]
+  cplx* cbuf = vbuf + (size_t)P * P * M;           // [P*P][CAPR] (stage)
+  int* lj = reinterpret_cast<int*>(cbuf + (stage ? (size_t)P * P * CAPR : 0));  // [K]
+  __shared__ double red[8][8];
+  __shared__ double csafe[8];
+  __shared__ double wred[16];
+  __shared__ int sviol;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(FULL, tid >> 5, 0);
+  const int nw = blockDim.x >> 5;
+  const int att = round;
   const cplx* W = a.W + (long long)sys * a.w_sys;
   const long long rowstride = (long long)rows * P;
-  double sc = 0.0;
-  for (int e = tid; e < K * P; e += NT) {
-    const int pos = e / (rows * P), rem = e % (rows * P);
-    sc = fmax(sc, cabs2(W[node_of(a, pos) * rowstride + rem]));
-  }
-  sc = wmax(sc);
-  if (lane == 0) wred[warp] = sc;
-  // coefficients past the register blocks are zero (an overflow went to the
-  // exact kernel), so the staged fold stops at CAPR
-  const int len = min(min(s.len_try[sys], cap), stage ? CAPR : cap);
-  double resm = 0.0;
-  for (int cs = 0; cs < a.noff; ++cs) {
-    const long long oc = cs ? a.o1 : a.o0;
-    for (int l = tid; l < len; l += NT) twl[l] = __ldg(&a.twN[(oc * l) % a.N]);
-    __syncthreads();  // also orders the basis writes above before the reads below
-    for (int e = tid; e < PP * M; e += NT) {
-      const int pq = e / M, q = e % M;
-      const cplx* src = stage ? cbuf + (size_t)pq * CAPR : dst + (long long)pq * cap;
-      cplx a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0);
-      int l = q;
-      for (; l + M < len; l += 2 * M) {
-        a0 = cfma(src[l], twl[l], a0);
-        a1 = cfma(src[l + M], twl[l + M], a1);
-      }
-      if (l < len) a0 = cfma(src[l], twl[l], a0);
-      gbuf[e] = cadd(a0, a1);
-    }
-    __syncthreads();
-    for (int e = tid; e < P * M; e += NT) {
-      const int k = e / M, t = e % M;
-      const cplx* g = gbuf + (size_t)k * P * M;
-      cplx acc[P];
-#pragma unroll
-      for (int i = 0; i < P; ++i) acc[i] = cmk(0.0, 0.0);
-      int kk = 0;
-      for (int q = 0; q < M; ++q) {
-        const cplx w = wtab[kk];
-#pragma unroll
-        for (int i = 0; i < P; ++i) acc[i] = cfma(g[i * M + q], w, acc[i]);
-        kk += t;
-        if (kk >= M) kk -= M;
-      }
-#pragma unroll
-      for (int i = 0; i < P; ++i) vbuf[(k * P + i) * M + t] = acc[i];
-    }
-    __syncthreads();
-    for (int e = tid; e < M * rows * P; e += NT) {
-      const int tt = e / (rows * P), rem = e % (rows * P);
-      const int rr = rem / P, jj = rem % P;
-      const cplx* wrow = W + (oc + a.stride * (long long)tt) * rowstride + rr * P;
-      cplx acc = cmk(0.0, 0.0);
-#pragma unroll
-      for (int i = 0; i < P; ++i) acc = cfma(wrow[i], vbuf[(i * P + jj) * M + tt], acc);
-      resm = fmax(resm, cabs2(acc));
-    }
-    __syncthreads();
-  }
-  double scale = 0.0;
-  for (int w = 0; w < NW; ++w) scale = fmax(scale, wred[w]);
-  scale = sqrt(scale);
-  __syncthreads();
-  resm = wmax(resm);
-  if (lane == 0) wred[warp] = resm;
-  __syncthreads();
-  double res = 0.0;
-  for (int w = 0; w < NW; ++w) res = fmax(res, wred[w]);
-  res = (scale == 0.0) ? 0.0 : sqrt(res) / scale;
-  TR_BTRACE(4);
+  int2* dlog = s.def_try + (long long)sys * s.kcap;
+  const int H = (K + 31) / 32;
+  const int slot = (warp & 3) ? warp - warp / 4 : 0;  // 1.. on warps != 0 mod 4
+  const int hid = (slot >= 1 && slot <= H) ? slot : 0;
+  const int brow = (slot > H && slot <= H + P) ? slot - H - 1 : -1;
 
-  // ---- best attempt, retry or commit (ref tanint.py:395-434) ----
-  double factor = 1.0;
-  for (int i = 0; i < P; ++i) factor = fmax(factor, csafe[i]);
-  const bool better = round == 0 || res < s.res_best[sys];
-  const int nd = s.ndef_try[sys];
-  if (better) {
-    if (round > 0) {
-      cplx* o = a.out + (long long)sys * a.out_sys;
-      for (long long e = tid; e < (long long)PP * cap; e += NT) o[e] = dst[e];
+  const int mine = 32 * (hid - 1) + lane;
+  cplx r[P];
+  cplx sg = cmk(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
+  if (hid >= 1 && mine < K) {
+    const long long node = cond_node(a, mine, att);
+    sg = __ldg(&a.twN[node]);
+    lsig[mine] = sg;
+    const cplx* wr = W + node * rowstride + (mine % rows) * P;
+#pragma unroll
+    for (int i = 0; i < P; ++i) r[i] = wr[i];
+  }
+  if (tid < 2) lsig[K + tid] = cmk(0.0, 0.0);
+  for (int e = tid; e < M; e += blockDim.x) wtab[e] = __ldg(&a.twN[(long long)e * a.stride]);
+  if (tid == 0) sviol = 0;
+  cplx c[DB][P];
+#pragma unroll
+  for (int d = 0; d < DB; ++d)
+#pragma unroll
+    for (int i = 0; i < P; ++i) c[d][i] = cmk(0.0, 0.0);
+  __syncthreads();
+
+  auto nbar1 = [&](int t) { return 32 * (1 + H - ((t + 2) / 32 + 1) + 1 + P); };
+
+  RowState st;
+  st.dmax = 0;
+  st.big = false;
+  int deg[P];
+  int tb = 0, synced = 0;  // basis rows: next step, steps whose barrier was passed
+  if (warp == 0) {
+    // ---------------- decider (as leaf_chain2_kernel) ----------------
+    const double thr2 = a.thr * a.thr;
+    int cd[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
+    cplx f[P], pre[P];
+    {
+      const cplx* w0 = W + cond_node(a, 0, att) * rowstride;
+#pragma unroll
+      for (int i = 0; i < P; ++i) f[i] = w0[i];
+      if (K > 1) {
+        const cplx* w1 = W + cond_node(a, 1, att) * rowstride + (1 % rows) * P;
+#pragma unroll
+        for (int i = 0; i < P; ++i) pre[i] = w1[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < P; ++i) pre[i] = cmk(0.0, 0.0);
+      }
     }
-    int2* db = s.def_best + (long long)sys * s.kcap;
-    const int2* dt = s.def_try + (long long)sys * s.kcap;
-    for (int e = tid; e < nd; e += NT) db[e] = dt[e];
+    cplx sf = lsig[0], sp = lsig[1];
+    for (int t = 0; t < K; ++t) {
+      cplx fj;
+      double a2j;
+      const int j = decide_bits<P>(f, cd, thr2, fj, a2j);
+      const double inv2 = rcp_nr(a2j);
+      const cplx ci = cmk(-fj.x * inv2, fj.y * inv2);
+      if (lane == 0) {
+        lj[t] = j;
+        lci[t] = ci;
+#pragma unroll
+        for (int i = 0; i < P; ++i) lf[t * P + i] = f[i];
+      }
+      if (t + 2 < K) bar_arrive(1 + 2 * (t & 1), nbar1(t));
+      if (t + 1 < K) {
+        if (t >= 1) {
+          bar_sync(2 + 2 * ((t - 1) & 1), 64);
+          const cplx* src = prow + ((t - 1) & 1) * P;
+#pragma unroll
+          for (int i = 0; i < P; ++i) pre[i] = src[i];
+        }
+        const cplx qj = sel<P>(pre, j);
+        const cplx c2 = cmul(ci, qj);
+        const cplx nfj = cmul(qj, csub(sp, sf));
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const cplx v = cfma(f[i], c2, pre[i]);
+          f[i] = (j < 0) ? pre[i] : (i == j) ? nfj : v;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < P; ++i) cd[i] += (i == j);
+      sf = sp;
+      sp = lsig[t + 2];
+    }
+  } else if (hid >= 1) {
+    // ---------------- holder ----------------
+    for (int t = 0; t + 2 < K && hid >= (t + 2) / 32 + 1; ++t) {
+      bar_sync(1 + 2 * (t & 1), nbar1(t));
+      const int j = lj[t];
+      if (j >= 0) {
+        const cplx rj = sel<P>(r, j);
+        const cplx c2 = cmul(lci[t], rj);
+        const cplx nj = cmul(rj, csub(sg, lsig[t]));
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const cplx v = cfma(lf[t * P + i], c2, r[i]);
+          r[i] = (i == j) ? nj : v;
+        }
+      }
+      if (hid == (t + 2) / 32 + 1) {
+        if (lane == (t + 2) % 32) {
+          cplx* dst = prow + (t & 1) * P;
+#pragma unroll
+          for (int i = 0; i < P; ++i) dst[i] = r[i];
+        }
+        bar_arrive(2 + 2 * (t & 1), 64);
+      }
+    }
+    // holders still needed at the end wait at the barrier below
+  } else if (brow >= 0) {
+    // ---------------- basis row: steps published through barrier 1/3 ----------------
+#pragma unroll
+    for (int i = 0; i < P; ++i) deg[i] = i == brow ? 0 : -1;
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      if (i == brow && lane == 0) c[0][i] = cmk(1.0, 0.0);
+    // steps up to K-3 come with a barrier; the last two after the sync below
+    const int kb = K > 2 ? K - 2 : 0;
+    bool over = false;  // outgrew the register blocks: keep passing the barriers only
+    while (tb < kb) {
+      int need = st.dmax / 32 + 1;
+      if (synced <= tb) {  // the barrier of step tb must be passed before reading it
+        bar_sync(1 + 2 * (tb & 1), nbar1(tb));
+        synced = tb + 1;
+      }
+      if (over) { ++tb; continue; }
+      const int j = lj[tb];
+      if (j >= 0) {
+        const int dj = sel_i<P>(deg, j);
+        if (dj >= 0) need = max(need, (dj + 1) / 32 + 1);
+      }
+      if (need > DB) { st.big = true; over = true; ++tb; continue; }
+#define TR_RUNF(NB, LIM) \
+  case NB: if constexpr (NB <= DB) tb = fused_steps<P, DB, NB>(c, deg, st, tb, synced, LIM, K, H, lj, lf, lci, lsig, lane); break;
+      switch (need) {
+        TR_RUNF(1, kb) TR_RUNF(2, kb) TR_RUNF(3, kb) TR_RUNF(4, kb) TR_RUNF(5, kb) TR_RUNF(6, kb) TR_RUNF(7, kb)
+        default: tb = K; break;
+      }
+    }
   }
   __syncthreads();
-  if (tid == 0) {
-    s.viol[sys] = sviol;
-    if (better) {
-      s.res_best[sys] = res;
-      s.ndef_best[sys] = nd;
-      s.factor_best[sys] = factor;
-      s.len_best[sys] = s.len_try[sys];
-      for (int i = 0; i < P; ++i) s.cd_best[sys * 8 + i] = s.cd_try[sys * 8 + i];
+  if (brow >= 0 && tb < K && !st.big) {  // the last steps (no barrier)
+    synced = K;
+    while (tb < K) {
+      int need = st.dmax / 32 + 1;
+      const int j = lj[tb];
+      if (j >= 0) {
+        const int dj = sel_i<P>(deg, j);
+        if (dj >= 0) need = max(need, (dj + 1) / 32 + 1);
+      }
+      if (need > DB) { st.big = true; break; }
+      switch (need) {
+        TR_RUNF(1, K) TR_RUNF(2, K) TR_RUNF(3, K) TR_RUNF(4, K) TR_RUNF(5, K) TR_RUNF(6, K) TR_RUNF(7, K)
+        default: tb = K; break;
+      }
     }
-    const bool done = s.res_best[sys] <= a.check_tol || round + 1 >= a.nattempts;
-    if (sviol) {
-      s.need[sys] = SPLIT_EXACT;  // speculation failed: exact coupled kernel
-    } else if (!done) {
-      s.need[sys] = round + 1;    // retry with the next absorption order
-    } else {
-      for (int i = 0; i < P; ++i) a.cd[sys * 8 + i] = s.cd_best[sys * 8 + i];
-      const int base = a.dcount[sys];
-      const int nb = s.ndef_best[sys];
-      const int room = a.dmax - base;
-      const int nput = nb < room ? nb : room;
-      const int2* db = s.def_best + (long long)sys * s.kcap;
-      for (int e = 0; e < nput; ++e) a.defer[(long long)sys * a.dmax + base + e] = db[e];
-      a.dcount[sys] = base + nb;
-      if (nb > room) a.status[sys] = 5;
-      a.max_scale[sys] = fmax(a.max_scale[sys], s.factor_best[sys]);
-      if (round > 0) a.retried[sys] += 1;
-      if (a.res_out) a.res_out[sys] = s.res_best[sys];
-      if (a.len_out) a.len_out[sys] = s.len_best[sys];
-      s.need[sys] = SPLIT_DONE;
+#undef TR_RUNF
+  }
+  if (brow >= 0 && __any_sync(FULL, st.big) && lane == 0) sviol = 1;
+  // chain epilogue (warp 0): pivot log, basis length, ledger, deferrals
+  if (warp == 0) {
+    int len = 1, nd = 0;
+    int cdf[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) cdf[i] = a.cd[sys * 8 + i];
+    for (int base = 0; base < K; base += 32) {
+      const int t = base + lane;
+      const int j = t < K ? lj[t] : -2;
+      const unsigned def = __ballot_sync(FULL, j == -1);
+      len += __popc(__ballot_sync(FULL, j >= 0));
+      if (j == -1) dlog[nd + __popc(def & ((1u << lane) - 1u))] = make_int2((int)cond_node(a, t, att), t % rows);
+      nd += __popc(def);
+#pragma unroll
+      for (int i = 0; i < P; ++i) cdf[i] += __popc(__ballot_sync(FULL, j == i));
+    }
+    if (lane == 0) {
+      s.ndef_try[sys] = nd;
+      s.len_try[sys] = len;
+#pragma unroll
+      for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cdf[i];
     }
   }
+  __syncthreads();
+  finish_attempt<P, DB>(a, s, round, sys, c, brow, stage, wtab, twl, gbuf, vbuf, cbuf, red, csafe, wred, &sviol,
+                        nw);
 }
 
 __global__ void fast_need_reset_kernel(int* need, int nsys) {
@@ -1071,6 +1352,54 @@ int leaf_fast_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStrea
   const int nth2 = 32 * (1 + hk + (spread ? (hk - 1) / 3 : 0));
   static const char* cv = getenv("TR_CHAIN");  // TR_CHAIN=relay: previous chain kernel
   const bool relay = cv && cv[0] == 'r';
+  // fused attempt kernel (chain + basis + check in one CTA) when the batch
+  // fits the GPU at one CTA per SM and the basis fits the register blocks
+  static const char* fv = getenv("TR_FUSED");  // TR_FUSED=0: two kernels
+  const int fslots = hk + a.P;
+  const int fwarps = fslots + (fslots - 1) / 3 + 1;
+  const int fdb = blocks_planned(a);
+  const bool fused = !relay && !(fv && fv[0] == '0') && nsys <= 148 && fwarps <= 16 &&
+                     fdb <= (a.P == 5 ? 4 : 3);
+  if (fused) {
+    const int CAPR = 32 * fdb;
+    size_t fs = sizeof(cplx) * ((size_t)a.K * a.P + 2 * a.K + 2 + 2 * a.P + a.M + CAPR +
+                                2 * (size_t)a.P * a.P * a.M) + sizeof(int) * a.K;
+    const size_t fstaged = sizeof(cplx) * (size_t)a.P * a.P * CAPR;
+    const int stage = fs + fstaged <= 200 * 1024 ? 1 : 0;
+    if (stage) fs += fstaged;
+    for (int round = 0; round < a.nattempts; ++round) {
+      TrKTimer _kt(TRK_LEAF_PIVOT, st);
+      int rc = 0;
+#define TR_FUSED_L(PP_, DB_)                                                                       \
+  {                                                                                                \
+    static bool set = false;                                                                       \
+    if (!set) {                                                                                    \
+      cudaFuncSetAttribute(leaf_fused_kernel<PP_, DB_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           200 * 1024);                                                            \
+      set = true;                                                                                  \
+    }                                                                                              \
+    leaf_fused_kernel<PP_, DB_><<<nsys, 32 * fwarps, fs, st>>>(a, s, round, stage);                \
+  }
+      if (a.P == 5) {
+        switch (fdb) {
+          case 1: TR_FUSED_L(5, 1) break;
+          case 2: TR_FUSED_L(5, 2) break;
+          case 3: TR_FUSED_L(5, 3) break;
+          default: TR_FUSED_L(5, 4) break;
+        }
+      } else {
+        switch (fdb) {
+          case 1: TR_FUSED_L(7, 1) break;
+          case 2: TR_FUSED_L(7, 2) break;
+          default: TR_FUSED_L(7, 3) break;
+        }
+      }
+#undef TR_FUSED_L
+      (void)rc;
+    }
+    TR_CUDA_CHECK(cudaGetLastError());
+    return 0;
+  }
   for (int round = 0; round < a.nattempts; ++round) {
     {
       TrKTimer _kt(TRK_LEAF_PIVOT, st);
