@@ -29,6 +29,7 @@
 // does not fire and the basis kernel checks that no coefficient exceeded the
 // trigger at those points.  A leaf that violates this is redone by the exact
 // coupled kernel (leaf.cu).
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "leaf.cuh"
@@ -54,6 +55,9 @@ constexpr double RESCALE_TRIGGER = 1e8;
 constexpr int RESCALE_PERIOD = 8;
 constexpr int NT = 256;  // threads per CTA of both kernels
 constexpr int NW = NT / 32;
+#ifndef TR_SPIN_NS
+#define TR_SPIN_NS 64
+#endif
 
 TR_D long long node_of(const LeafArgs& a, int p) {
   if (a.noff == 1) return a.o0 + a.stride * (long long)p;
@@ -85,6 +89,15 @@ TR_D int ld_acquire(const int* p) {
                : "r"((unsigned)__cvta_generic_to_shared(p))
                : "memory");
   return v;
+}
+// wait until the published step counter passes t (backs off so that spinning
+// warps leave the shared-memory pipe to the decider)
+TR_D int wait_steps(const int* flag, int t, int avail) {
+  while (avail <= t) {
+    avail = ld_acquire(flag);
+    if (avail <= t) __nanosleep(TR_SPIN_NS);
+  }
+  return avail;
 }
 TR_D cplx shfl_c(cplx v, int src) {
   return cmk(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src));
@@ -605,6 +618,163 @@ __global__ void __launch_bounds__(SPREAD ? 352 : 288, SPREAD ? 1 : 2) leaf_chain
         bar_arrive(2 + 2 * (t & 1), 64);
       }
     }
+  }
+  __syncthreads();
+  // epilogue (warp 0): pivot log, basis length, ledger, deferred conditions in
+  // step order (ref tanint.py:200-206)
+  if (warp == 0) {
+    int len = 1, nd = 0;
+    int cdf[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) cdf[i] = a.cd[sys * 8 + i];
+    int* jlog = s.jl + (long long)sys * s.kcap;
+    for (int base = 0; base < K; base += 32) {
+      const int t = base + lane;
+      const int j = t < K ? lj[t] : -2;
+      if (t < K) jlog[t] = j;
+      const unsigned def = __ballot_sync(FULL, j == -1);
+      len += __popc(__ballot_sync(FULL, j >= 0));
+      if (j == -1) dlog[nd + __popc(def & ((1u << lane) - 1u))] = make_int2((int)cond_node(a, t, att), t % rows);
+      nd += __popc(def);
+#pragma unroll
+      for (int i = 0; i < P; ++i) cdf[i] += __popc(__ballot_sync(FULL, j == i));
+    }
+    if (lane == 0) {
+      s.ndef_try[sys] = nd;
+      s.len_try[sys] = len;
+#pragma unroll
+      for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cdf[i];
+    }
+  }
+  // multipliers for the basis replay: mu_i = phi_i c (mu_j = 0)
+  cplx* mulog = s.mu + (long long)sys * s.kcap * P;
+  for (int e = tid; e < K * P; e += blockDim.x) {
+    const int t = e / P, i = e - t * P;
+    const int j = lj[t];
+    mulog[e] = (j < 0 || i == j) ? cmk(0.0, 0.0) : cmul(lf[e], lci[t]);
+  }
+}
+
+// ------------------------------------------ chain kernel, lane-resident front
+// The decider warp holds a block of 32 consecutive conditions, one row per
+// lane, and applies every step to all of them itself: the next front is
+// already in a lane and is broadcast by shuffle, so a step has no barrier and
+// no hand-back on its critical path (shuffle -> decide -> reciprocal -> own
+// row update).  Warps 1..H-1 hold the later blocks, apply the published steps
+// from the shared-memory log as they appear (acquire polling on a step
+// counter) and pass their block to the decider when it reaches it (after the
+// last step of the previous block).  The log and the epilogue are those of
+// leaf_chain2_kernel, and every row update uses the same formulas, so the
+// pivots and multipliers are the same.
+template <int P>
+__global__ void __launch_bounds__(256, 2) leaf_chain3_kernel(LeafArgs a, SplitState s, int round) {
+  const int sys = blockIdx.x;
+  if (s.need[sys] != round) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = a.K, rows = a.rows;
+  cplx* lf = reinterpret_cast<cplx*>(smem_raw);    // [K][P] decided rows
+  cplx* lci = lf + (size_t)K * P;                  // [K] c_t = -conj(phi_j)/|phi_j|^2
+  cplx* lsig = lci + K;                            // [K] node of every condition
+  cplx* xfer = lsig + K;                           // [32][P] block hand-over
+  int* lj = reinterpret_cast<int*>(xfer + 32 * P);  // [K]
+  int* flag = lj + K;                              // [0] published steps, [1] blocks handed over
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(FULL, tid >> 5, 0);
+  const int att = round;
+  const cplx* W = a.W + (long long)sys * a.w_sys;
+  const long long rowstride = (long long)rows * P;
+  int2* dlog = s.def_try + (long long)sys * s.kcap;
+  const int H = (K + 31) / 32;
+  const int mine = 32 * warp + lane;
+  cplx r[P];
+  cplx sg = cmk(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
+  if (warp < H && mine < K) {
+    const long long node = cond_node(a, mine, att);
+    sg = __ldg(&a.twN[node]);
+    lsig[mine] = sg;
+    const cplx* wr = W + node * rowstride + (mine % rows) * P;
+#pragma unroll
+    for (int i = 0; i < P; ++i) r[i] = wr[i];
+  }
+  if (tid < 2) flag[tid] = 0;
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---------------- decider ----------------
+    const double thr2 = a.thr * a.thr;
+    int cd[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
+    const bool trace = g_chain_trace_on && sys == 0 && round == 0 && lane == 0;
+    for (int b = 0; b < H; ++b) {
+      if (b > 0) {  // take over block b (its rows carry steps < 32 b)
+        while (ld_acquire(&flag[1]) < b) {
+        }
+#pragma unroll
+        for (int i = 0; i < P; ++i) r[i] = xfer[lane * P + i];
+        sg = lsig[min(32 * b + lane, K - 1)];
+      }
+      const int tend = min(K, 32 * b + 32);
+      for (int t = 32 * b; t < tend; ++t) {
+        if (trace) g_chain_trace[4 * t] = clock64();
+        const int src = t & 31;
+        cplx f[P];
+#pragma unroll
+        for (int i = 0; i < P; ++i) f[i] = shfl_c(r[i], src);
+        const cplx sf = lsig[t];
+        cplx fj;
+        double a2j;
+        const int j = decide_bits<P>(f, cd, thr2, fj, a2j);
+        const double inv2 = rcp_nr(a2j);
+        const cplx ci = cmk(-fj.x * inv2, fj.y * inv2);
+        if (lane == 0) {
+          lj[t] = j;
+          lci[t] = ci;
+#pragma unroll
+          for (int i = 0; i < P; ++i) lf[t * P + i] = f[i];
+          st_release(&flag[0], t + 1);
+        }
+        if (j >= 0) {
+          // r <- r + phi (c r_j), r_j (s_r - s_t) in column j
+          const cplx rj = sel<P>(r, j);
+          const cplx c2 = cmul(ci, rj);
+          const cplx nj = cmul(rj, csub(sg, sf));
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            const cplx v = cfma(f[i], c2, r[i]);
+            r[i] = (i == j) ? nj : v;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < P; ++i) cd[i] += (i == j);
+      }
+    }
+  } else if (warp < H) {
+    // ---------------- holder of block `warp`: steps < 32 warp ----------------
+    const int tlim = 32 * warp;
+    int avail = 0;
+    for (int t = 0; t < tlim; ++t) {
+      avail = wait_steps(&flag[0], t, avail);
+      const int j = lj[t];
+      if (j >= 0) {
+        const cplx rj = sel<P>(r, j);
+        const cplx c2 = cmul(lci[t], rj);
+        const cplx nj = cmul(rj, csub(sg, lsig[t]));
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const cplx v = cfma(lf[t * P + i], c2, r[i]);
+          r[i] = (i == j) ? nj : v;
+        }
+      }
+    }
+    // wait for the decider to take the previous block, then hand this one over
+    while (ld_acquire(&flag[1]) < warp - 1) __nanosleep(TR_SPIN_NS);
+#pragma unroll
+    for (int i = 0; i < P; ++i) xfer[lane * P + i] = r[i];
+    __syncwarp();
+    if (lane == 0) st_release(&flag[1], warp);
   }
   __syncthreads();
   // epilogue (warp 0): pivot log, basis length, ledger, deferred conditions in
@@ -1271,6 +1441,256 @@ __global__ void __launch_bounds__(512, 1) leaf_fused_kernel(LeafArgs a, SplitSta
                         nw);
 }
 
+// ------------------------------------ fused attempts, lane-resident front
+// One CTA per system runs every attempt of the leaf: the chain of
+// leaf_chain3_kernel (decider warp 0 alone on its scheduler, holders of the
+// later blocks), plus P basis-row warps that replay the published steps from
+// the log as fast as they can (acquire polling, never on the decider's
+// critical path), then the normalisation / self-check of finish_attempt; a
+// retry (ref tanint.py:395-434) loops inside the kernel, so a leaf is one
+// launch.  Warps != 0 mod 4 carry holders (slots 1..H-1) and basis rows
+// (slots H..H+P-1).
+template <int P, int DB, int NB>
+TR_D int poll_steps(cplx (&c)[DB][P], int (&deg)[P], RowState& st, int t, int& avail, int K, const int* lj,
+                    const cplx* lf, const cplx* lci, const cplx* lsig, const int* flag, int lane) {
+  for (; t < K; ++t) {
+    avail = wait_steps(flag, t, avail);
+    const int j = lj[t];
+    if (j >= 0) {
+      const int dj = sel_i<P>(deg, j);
+      if (dj >= 0) {
+        const int nd = max(st.dmax, dj + 1);
+        if (nd / 32 + 1 > NB) return t;
+#pragma unroll
+        for (int i = 0; i < P; ++i) deg[i] = (i == j) ? dj + 1 : max(deg[i], dj);
+        st.dmax = nd;
+        const cplx ci = lci[t];
+        cplx mu[P];
+#pragma unroll
+        for (int i = 0; i < P; ++i) mu[i] = cmul(lf[t * P + i], ci);
+        basis_step_j<P, DB, NB>(c, j, mu, cneg(lsig[t]), lane);
+      }
+    }
+    if (((t + 1) % RESCALE_PERIOD) == 0) {
+      bool b = false;
+#pragma unroll
+      for (int d = 0; d < NB; ++d)
+#pragma unroll
+        for (int i = 0; i < P; ++i) b |= cabs2(c[d][i]) > RESCALE_TRIGGER * RESCALE_TRIGGER;
+      st.big |= b;
+    }
+  }
+  return t;
+}
+
+struct Fused3Smem {
+  static size_t bytes(int K, int P, int M, int DB, bool stage) {
+    const size_t capr = 32 * (size_t)DB;
+    return sizeof(cplx) * ((size_t)K * P + 2 * (size_t)K + 32 * (size_t)P + M + capr + 2 * (size_t)P * P * M +
+                           (stage ? (size_t)P * P * capr : 0)) +
+           sizeof(int) * ((size_t)K + 2);
+  }
+};
+
+template <int P, int DB, int NTH>
+__global__ void __launch_bounds__(512, 1) leaf_fused3_kernel(LeafArgs a, SplitState s, int stage) {
+  const int sys = blockIdx.x;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int CAPR = 32 * DB;
+  const int K = a.K, rows = a.rows, M = a.M;
+  cplx* lf = reinterpret_cast<cplx*>(smem_raw);    // [K][P] decided rows
+  cplx* lci = lf + (size_t)K * P;                  // [K]
+  cplx* lsig = lci + K;                            // [K]
+  cplx* xfer = lsig + K;                           // [32][P]
+  cplx* wtab = xfer + 32 * P;                      // [M]
+  cplx* twl = wtab + M;                            // [CAPR]
+  cplx* gbuf = twl + CAPR;                         // [P*P][M]
+  cplx* vbuf = gbuf + (size_t)P * P * M;           // [P*P][M]
+  cplx* cbuf = vbuf + (size_t)P * P * M;           // [P*P][CAPR] (stage)
+  int* lj = reinterpret_cast<int*>(cbuf + (stage ? (size_t)P * P * CAPR : 0));  // [K]
+  int* flag = lj + K;                              // [0] published steps, [1] blocks handed over
+  __shared__ double red[8][8];
+  __shared__ double csafe[8];
+  __shared__ double wred[16];
+  __shared__ int sviol;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(FULL, tid >> 5, 0);
+  const int nw = blockDim.x >> 5;
+  const cplx* W = a.W + (long long)sys * a.w_sys;
+  const long long rowstride = (long long)rows * P;
+  int2* dlog = s.def_try + (long long)sys * s.kcap;
+  const int H = (K + 31) / 32;
+  const int slot = (warp & 3) ? warp - warp / 4 : 0;
+  const int blk = warp == 0 ? 0 : (slot >= 1 && slot < H) ? slot : -1;  // condition block held
+  const int brow = (slot >= H && slot < H + P) ? slot - H : -1;
+  for (int e = tid; e < M; e += blockDim.x) wtab[e] = __ldg(&a.twN[(long long)e * a.stride]);
+
+  for (int round = 0; round < a.nattempts; ++round) {
+    const int att = round;
+    const int mine = 32 * blk + lane;
+    cplx r[P];
+    cplx sg = cmk(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
+    if (blk >= 0 && mine < K) {
+      const long long node = cond_node(a, mine, att);
+      sg = __ldg(&a.twN[node]);
+      lsig[mine] = sg;
+      const cplx* wr = W + node * rowstride + (mine % rows) * P;
+#pragma unroll
+      for (int i = 0; i < P; ++i) r[i] = wr[i];
+    }
+    if (tid < 2) flag[tid] = 0;
+    if (tid == 0) sviol = 0;
+    cplx c[DB][P];  // basis row (basis warps only; set in their branch)
+    RowState st;
+    st.dmax = 0;
+    st.big = false;
+    __syncthreads();
+
+    if (warp == 0) {
+      // ---------------- decider (as leaf_chain3_kernel) ----------------
+      const double thr2 = a.thr * a.thr;
+      int cd[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
+      for (int b = 0; b < H; ++b) {
+        if (b > 0) {
+          while (ld_acquire(&flag[1]) < b) {
+          }
+#pragma unroll
+          for (int i = 0; i < P; ++i) r[i] = xfer[lane * P + i];
+          sg = lsig[min(32 * b + lane, K - 1)];
+        }
+        if (g_chain_trace_on && sys == 0 && round == 0 && lane == 0) g_chain_trace[3072 + b] = clock64();
+        const int tend = min(K, 32 * b + 32);
+        for (int t = 32 * b; t < tend; ++t) {
+          const int src = t & 31;
+          cplx f[P];
+#pragma unroll
+          for (int i = 0; i < P; ++i) f[i] = shfl_c(r[i], src);
+          const cplx sf = lsig[t];
+          cplx fj;
+          double a2j;
+          const int j = decide_bits<P>(f, cd, thr2, fj, a2j);
+          const double inv2 = rcp_nr(a2j);
+          const cplx ci = cmk(-fj.x * inv2, fj.y * inv2);
+          if (lane == 0) {
+            lj[t] = j;
+            lci[t] = ci;
+#pragma unroll
+            for (int i = 0; i < P; ++i) lf[t * P + i] = f[i];
+            st_release(&flag[0], t + 1);
+          }
+          if (j >= 0) {
+            const cplx rj = sel<P>(r, j);
+            const cplx c2 = cmul(ci, rj);
+            const cplx nj = cmul(rj, csub(sg, sf));
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+              const cplx v = cfma(f[i], c2, r[i]);
+              r[i] = (i == j) ? nj : v;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < P; ++i) cd[i] += (i == j);
+        }
+      }
+      if (g_chain_trace_on && sys == 0 && round == 0 && lane == 0) g_chain_trace[3072 + 9] = clock64();
+    } else if (blk >= 1) {
+      // ---------------- holder of block blk: steps < 32 blk ----------------
+      const int tlim = 32 * blk;
+      int avail = 0;
+      for (int t = 0; t < tlim; ++t) {
+        avail = wait_steps(&flag[0], t, avail);
+        const int j = lj[t];
+        if (j >= 0) {
+          const cplx rj = sel<P>(r, j);
+          const cplx c2 = cmul(lci[t], rj);
+          const cplx nj = cmul(rj, csub(sg, lsig[t]));
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            const cplx v = cfma(lf[t * P + i], c2, r[i]);
+            r[i] = (i == j) ? nj : v;
+          }
+        }
+      }
+      while (ld_acquire(&flag[1]) < blk - 1) __nanosleep(TR_SPIN_NS);
+#pragma unroll
+      for (int i = 0; i < P; ++i) xfer[lane * P + i] = r[i];
+      __syncwarp();
+      if (lane == 0) st_release(&flag[1], blk);
+    } else if (brow >= 0) {
+      // ---------------- basis row brow: replay published steps ----------------
+      int deg[P];
+#pragma unroll
+      for (int d = 0; d < DB; ++d)
+#pragma unroll
+        for (int i = 0; i < P; ++i) c[d][i] = cmk(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < P; ++i) deg[i] = i == brow ? 0 : -1;
+#pragma unroll
+      for (int i = 0; i < P; ++i)
+        if (i == brow && lane == 0) c[0][i] = cmk(1.0, 0.0);
+      int tb = 0, avail = 0;
+      while (tb < K) {
+        int need = st.dmax / 32 + 1;
+        avail = wait_steps(&flag[0], tb, avail);
+        const int j = lj[tb];
+        if (j >= 0) {
+          const int dj = sel_i<P>(deg, j);
+          if (dj >= 0) need = max(need, (dj + 1) / 32 + 1);
+        }
+        if (need > DB) {  // outgrew the register blocks: exact kernel
+          st.big = true;
+          break;
+        }
+#define TR_RUN3(NB) \
+  case NB: if constexpr (NB <= DB) tb = poll_steps<P, DB, NB>(c, deg, st, tb, avail, K, lj, lf, lci, lsig, flag, lane); break;
+        switch (need) {
+          TR_RUN3(1) TR_RUN3(2) TR_RUN3(3) TR_RUN3(4) TR_RUN3(5) TR_RUN3(6) TR_RUN3(7)
+          default: tb = K; break;
+        }
+#undef TR_RUN3
+      }
+    }
+    __syncthreads();
+    if (brow >= 0 && __any_sync(FULL, st.big) && lane == 0) sviol = 1;
+    // chain epilogue (warp 0): basis length, ledger, deferrals (ref tanint.py:200-206)
+    if (warp == 0) {
+      int len = 1, nd = 0;
+      int cdf[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) cdf[i] = a.cd[sys * 8 + i];
+      for (int base = 0; base < K; base += 32) {
+        const int t = base + lane;
+        const int j = t < K ? lj[t] : -2;
+        const unsigned def = __ballot_sync(FULL, j == -1);
+        len += __popc(__ballot_sync(FULL, j >= 0));
+        if (j == -1) dlog[nd + __popc(def & ((1u << lane) - 1u))] = make_int2((int)cond_node(a, t, att), t % rows);
+        nd += __popc(def);
+#pragma unroll
+        for (int i = 0; i < P; ++i) cdf[i] += __popc(__ballot_sync(FULL, j == i));
+      }
+      if (lane == 0) {
+        s.ndef_try[sys] = nd;
+        s.len_try[sys] = len;
+#pragma unroll
+        for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cdf[i];
+      }
+    }
+    if (g_chain_trace_on && sys == 0 && round == 0 && lane == 0 && (warp == 0 || brow >= 0))
+      g_chain_trace[3072 + (warp == 0 ? 10 : 11 + brow)] = clock64();
+    __syncthreads();
+    finish_attempt<P, DB>(a, s, round, sys, c, brow, stage, wtab, twl, gbuf, vbuf, cbuf, red, csafe, wred, &sviol,
+                          nw);
+    if (g_chain_trace_on && sys == 0 && round == 0 && tid == 0) g_chain_trace[3072 + 20] = clock64();
+    __syncthreads();
+    if (s.need[sys] != round + 1) break;
+    __syncthreads();
+  }
+}
+
 __global__ void fast_need_reset_kernel(int* need, int nsys) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nsys) need[i] = 0;
@@ -1332,7 +1752,76 @@ bool leaf_fast_supported(const LeafArgs& a) {
   return BasisSmem::bytes(a.K, a.P, a.M, db) <= 220 * 1024;
 }
 
+// fused attempts with the lane-resident chain (leaf_fused3_kernel): one
+// launch per leaf; returns -1 when the shape does not fit it
+int launch_fused3(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t st) {
+  static const char* fv = getenv("TR_F3");  // TR_F3=0: previous kernels
+  if (fv && fv[0] == '0') return -1;
+  if (nsys > 148) return -1;
+  const int H = (a.K + 31) / 32;
+  const int last = H + a.P - 1;  // highest slot
+  int nw = 1;
+  while (nw - 1 - (nw - 1) / 4 < last) ++nw;
+  if (nw > 16) return -1;
+  const int db = blocks_planned(a);
+  if (db > (a.P == 5 ? 4 : 3)) return -1;
+  size_t fs = Fused3Smem::bytes(a.K, a.P, a.M, db, true);
+  int stage = 1;
+  if (fs > 200 * 1024) {
+    fs = Fused3Smem::bytes(a.K, a.P, a.M, db, false);
+    stage = 0;
+  }
+  if (fs > 200 * 1024) return -1;
+  {
+    const double K = a.K, P = a.P;
+    tr_kernel_work(TRK_LEAF_PIVOT, 16.0 * nsys * K * P, 4.0 * nsys * P * K * (K - 1));
+    tr_kernel_work(TRK_LEAF_BUILD, 16.0 * nsys * (P * P * (K + 1) + K * P),
+                   4.0 * nsys * P * P * K * (K + 1) + 8.0 * nsys * (double)a.noff * P * P * a.M * a.M);
+  }
+  TrKTimer _kt(TRK_LEAF_PIVOT, st);
+#define TR_F3N(PP_, DB_, NTH_)                                                                             \
+  {                                                                                                        \
+    static bool set = false;                                                                               \
+    if (!set) {                                                                                            \
+      cudaFuncSetAttribute(leaf_fused3_kernel<PP_, DB_, NTH_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           200 * 1024);                                                                    \
+      cudaFuncAttributes fa;                                                                               \
+      cudaFuncGetAttributes(&fa, leaf_fused3_kernel<PP_, DB_, NTH_>);                                      \
+      if (getenv("TR_DEBUG"))                                                                              \
+        fprintf(stderr, "fused3<%d,%d,%d>: regs %d maxthreads %d smem %zu dyn %zu\n", PP_, DB_, NTH_,       \
+                fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, fs);                                \
+      set = true;                                                                                          \
+    }                                                                                                      \
+    leaf_fused3_kernel<PP_, DB_, NTH_><<<nsys, 32 * nw, fs, st>>>(a, s, stage);                           \
+  }
+#define TR_F3L(PP_, DB_)                  \
+  if (nw <= 14) TR_F3N(PP_, DB_, 448)     \
+  else TR_F3N(PP_, DB_, 512)
+  if (a.P == 5) {
+    switch (db) {
+      case 1: TR_F3L(5, 1) break;
+      case 2: TR_F3L(5, 2) break;
+      case 3: TR_F3L(5, 3) break;
+      default: TR_F3L(5, 4) break;
+    }
+  } else {
+    switch (db) {
+      case 1: TR_F3L(7, 1) break;
+      case 2: TR_F3L(7, 2) break;
+      default: TR_F3L(7, 3) break;
+    }
+  }
+#undef TR_F3L
+#undef TR_F3N
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
 int leaf_fast_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t st) {
+  {
+    const int rc = launch_fused3(a, s, nsys, st);
+    if (rc >= 0) return rc;
+  }
   {
     TrKTimer _kt(TRK_LEAF_PIVOT, st);
     fast_need_reset_kernel<<<(nsys + 255) / 256, 256, 0, st>>>(s.need, nsys);
@@ -1352,13 +1841,16 @@ int leaf_fast_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStrea
   const int nth2 = 32 * (1 + hk + (spread ? (hk - 1) / 3 : 0));
   static const char* cv = getenv("TR_CHAIN");  // TR_CHAIN=relay: previous chain kernel
   const bool relay = cv && cv[0] == 'r';
+  const bool lanes = cv && cv[0] == '3';  // TR_CHAIN=3: lane-resident front
+  const size_t csm3 = sizeof(cplx) * ((size_t)a.K * a.P + 2 * (size_t)a.K + 32 * (size_t)a.P) +
+                      sizeof(int) * (a.K + 2);
   // fused attempt kernel (chain + basis + check in one CTA) when the batch
   // fits the GPU at one CTA per SM and the basis fits the register blocks
   static const char* fv = getenv("TR_FUSED");  // TR_FUSED=0: two kernels
   const int fslots = hk + a.P;
   const int fwarps = fslots + (fslots - 1) / 3 + 1;
   const int fdb = blocks_planned(a);
-  const bool fused = !relay && !(fv && fv[0] == '0') && nsys <= 148 && fwarps <= 16 &&
+  const bool fused = !relay && !lanes && !(fv && fv[0] == '0') && nsys <= 148 && fwarps <= 16 &&
                      fdb <= (a.P == 5 ? 4 : 3);
   if (fused) {
     const int CAPR = 32 * fdb;
@@ -1406,6 +1898,9 @@ int leaf_fast_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStrea
       if (relay) {
         if (a.P == 5) leaf_chain_kernel<5><<<nsys, NT, csm, st>>>(a, s, round);
         else leaf_chain_kernel<7><<<nsys, NT, csm, st>>>(a, s, round);
+      } else if (lanes) {
+        if (a.P == 5) leaf_chain3_kernel<5><<<nsys, 32 * hk, csm3, st>>>(a, s, round);
+        else leaf_chain3_kernel<7><<<nsys, 32 * hk, csm3, st>>>(a, s, round);
       } else {
         if (a.P == 5) {
           if (spread) leaf_chain2_kernel<5, true><<<nsys, nth2, csm2, st>>>(a, s, round);

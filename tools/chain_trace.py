@@ -26,8 +26,12 @@ a = a[1:K - 1]; step = step[1:K - 2]
 dec = a[:, 1] - a[:, 0]; upd = a[:, 2] - a[:, 1]; pub = a[:, 3] - a[:, 2]
 print("K", K, "mean step cycles %.0f  decide+ci %.0f  log+arrive+sync-wait %.0f  pre+front %.0f" % (
     step.mean(), dec.mean(), upd.mean(), pub.mean()))
-print("per-step:", step[:40].tolist())
+print("per-step:", step.tolist())
 print("handover steps (32k-1 -> 32k):", [int(step[i]) for i in range(31, K - 1, 32)])
 b = np.frombuffer(buf, dtype=np.int64)[3072:3078]
 print("basis kernel phases (cycles from start): load %d build %d norm+write %d check %d" % (
     b[1] - b[0], b[2] - b[1], b[3] - b[2], b[4] - b[3]))
+b = np.frombuffer(buf, dtype=np.int64)[3072:3083]
+if b[1] > b[0] > 0:
+    print("fused3 phases (cycles from start): decider done %d, basis rows done %s, finish done %d" % (
+        b[1] - b[0], [int(x - b[0]) for x in b[2:9] if x > 0], b[10] - b[0]))
