@@ -29,6 +29,7 @@
 // does not fire and the basis kernel checks that no coefficient exceeded the
 // trigger at those points.  A leaf that violates this is redone by the exact
 // coupled kernel (leaf.cu).
+#include <cooperative_groups.h>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -1483,65 +1484,135 @@ TR_D int poll_steps(cplx (&c)[DB][P], int (&deg)[P], RowState& st, int t, int& a
   return t;
 }
 
+// Shared memory of leaf_fused3_kernel: the leaf's weights (natural node
+// order, loaded once for every attempt and the self-check), the step log,
+// the check buffers and the attempt bookkeeping.
 struct Fused3Smem {
-  static size_t bytes(int K, int P, int M, int DB, bool stage) {
+  static size_t bytes(int K, int P, int M, int DB) {
     const size_t capr = 32 * (size_t)DB;
-    return sizeof(cplx) * ((size_t)K * P + 2 * (size_t)K + 32 * (size_t)P + M + capr + 2 * (size_t)P * P * M +
-                           (stage ? (size_t)P * P * capr : 0)) +
-           sizeof(int) * ((size_t)K + 2);
+    return sizeof(cplx) * ((size_t)K * P /*wl*/ + (size_t)K * P /*lf*/ + 2 * (size_t)K /*lci, lsig*/ +
+                           32 * (size_t)P /*xfer*/ + M /*wtab*/ + 2 * capr /*twl x2*/ +
+                           2 * (size_t)P * P * M /*gbuf, vbuf*/ + (size_t)P * P * capr /*cbuf*/) +
+           sizeof(int2) * 2 * (size_t)K /*dtry, dbest*/ + sizeof(int) * ((size_t)K + 2);
   }
 };
 
-template <int P, int DB, int NTH>
-__global__ void __launch_bounds__(512, 1) leaf_fused3_kernel(LeafArgs a, SplitState s, int stage) {
-  const int sys = blockIdx.x;
+struct F3Book {  // attempt bookkeeping (ref tanint.py:395-434)
+  double res_try, factor_try, res_best, factor_best, scale;
+  int nd_try, len_try, viol_try, nd_best, len_best, next;
+  int cd_try[8], cd_best[8];
+};
+
+// The reference's retry rule applied to one more finished attempt `c`
+// (rounds are considered in order): returns bit0 = c becomes the best,
+// bit1 = done, bit2 = rescale speculation failed (exact kernel).
+TR_D int f3_pick(F3Book& bk, const F3Book& c, int round, int P, int nattempts, double tol) {
+  if (c.viol_try) return 4;
+  const bool better = round == 0 || c.res_try < bk.res_best;
+  if (better) {
+    bk.res_best = c.res_try;
+    bk.nd_best = c.nd_try;
+    bk.factor_best = c.factor_try;
+    bk.len_best = c.len_try;
+    for (int i = 0; i < P; ++i) bk.cd_best[i] = c.cd_try[i];
+  }
+  const bool done = bk.res_best <= tol || round + 1 >= nattempts;
+  return (better ? 1 : 0) | (done ? 2 : 0);
+}
+
+template <int P, int DB, int NTH, bool CL>
+__global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitState s) {
+  // CL: a cluster of two CTAs per system runs attempts 0 and 1 side by side
+  const int rank = CL ? (int)cooperative_groups::this_cluster().block_rank() : 0;
+  const int sys = CL ? blockIdx.x >> 1 : blockIdx.x;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int CAPR = 32 * DB;
-  const int K = a.K, rows = a.rows, M = a.M;
-  cplx* lf = reinterpret_cast<cplx*>(smem_raw);    // [K][P] decided rows
+  constexpr int PP = P * P;
+  const int K = a.K, rows = a.rows, M = a.M, cap = a.cap;
+  const int RP = rows * P;
+  cplx* wl = reinterpret_cast<cplx*>(smem_raw);    // [noff][M][rows][P] leaf weights
+  cplx* lf = wl + (size_t)K * P;                   // [K][P] decided rows
   cplx* lci = lf + (size_t)K * P;                  // [K]
   cplx* lsig = lci + K;                            // [K]
   cplx* xfer = lsig + K;                           // [32][P]
   cplx* wtab = xfer + 32 * P;                      // [M]
-  cplx* twl = wtab + M;                            // [CAPR]
-  cplx* gbuf = twl + CAPR;                         // [P*P][M]
-  cplx* vbuf = gbuf + (size_t)P * P * M;           // [P*P][M]
-  cplx* cbuf = vbuf + (size_t)P * P * M;           // [P*P][CAPR] (stage)
-  int* lj = reinterpret_cast<int*>(cbuf + (stage ? (size_t)P * P * CAPR : 0));  // [K]
+  cplx* twl = wtab + M;                            // [2][CAPR] coset twists
+  cplx* gbuf = twl + 2 * CAPR;                     // [P*P][M]
+  cplx* vbuf = gbuf + (size_t)PP * M;              // [P*P][M]
+  cplx* cbuf = vbuf + (size_t)PP * M;              // [P*P][CAPR] normalised basis
+  int2* dtry = reinterpret_cast<int2*>(cbuf + (size_t)PP * CAPR);  // [K]
+  int2* dbest = dtry + K;                          // [K]
+  int* lj = reinterpret_cast<int*>(dbest + K);     // [K]
   int* flag = lj + K;                              // [0] published steps, [1] blocks handed over
   __shared__ double red[8][8];
   __shared__ double csafe[8];
   __shared__ double wred[16];
-  __shared__ int sviol;
-  const int tid = threadIdx.x, lane = tid & 31;
+  __shared__ F3Book bk;
+  __shared__ long long tsm[24];  // clock stamps of system 0 (tr_debug_chain_trace)
+  __shared__ int cd0[8];         // column degrees entering the leaf
+  const int tid = threadIdx.x, lane = tid & 31, nt = blockDim.x;
   const int warp = __shfl_sync(FULL, tid >> 5, 0);
-  const int nw = blockDim.x >> 5;
+  const int nw = nt >> 5;
   const cplx* W = a.W + (long long)sys * a.w_sys;
-  const long long rowstride = (long long)rows * P;
-  int2* dlog = s.def_try + (long long)sys * s.kcap;
+  const long long rowstride = (long long)RP;
   const int H = (K + 31) / 32;
+  const int NH = H / 2;  // holder warps: blocks 2h-1 and 2h
   const int slot = (warp & 3) ? warp - warp / 4 : 0;
-  const int blk = warp == 0 ? 0 : (slot >= 1 && slot < H) ? slot : -1;  // condition block held
-  const int brow = (slot >= H && slot < H + P) ? slot - H : -1;
-  for (int e = tid; e < M; e += blockDim.x) wtab[e] = __ldg(&a.twN[(long long)e * a.stride]);
+  const int hold = (slot >= 1 && slot <= NH) ? slot : 0;
+  const int brow = (slot > NH && slot <= NH + P) ? slot - NH - 1 : -1;
+  const int hb1 = 2 * hold - 1, hb2 = 2 * hold;  // blocks held (hb2 < H: two)
 
-  for (int round = 0; round < a.nattempts; ++round) {
+  // ---- once per leaf: weights, DFT table, coset twists, weight scale ----
+  double sc = 0.0;
+  for (int e = tid; e < K * P; e += nt) {
+    const int pos = e / RP, rem = e - pos * RP;
+    const cplx w = W[node_of(a, pos) * rowstride + rem];
+    const int cs = a.noff == 1 ? 0 : (pos & 1), tt = a.noff == 1 ? pos : (pos >> 1);
+    wl[(cs * M + tt) * RP + rem] = w;
+    sc = fmax(sc, cabs2(w));
+  }
+  for (int e = tid; e < M; e += nt) wtab[e] = __ldg(&a.twN[(long long)e * a.stride]);
+  if (tid < P) cd0[tid] = a.cd[sys * 8 + tid];
+  for (int e = tid; e < a.noff * CAPR; e += nt) {
+    const int cs = e / CAPR, l = e - cs * CAPR;
+    const long long oc = cs ? a.o1 : a.o0;
+    twl[e] = __ldg(&a.twN[(oc * l) % a.N]);
+  }
+  sc = wmax(sc);
+  if (lane == 0) wred[warp] = sc;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int w = 0; w < nw; ++w) m = fmax(m, wred[w]);
+    bk.scale = sqrt(m);
+  }
+
+  int round = rank;
+  bool viol = false;
+  for (;; ++round) {
     const int att = round;
-    const int mine = 32 * blk + lane;
-    cplx r[P];
-    cplx sg = cmk(0.0, 0.0);
+    cplx r[P], r2[P];
+    cplx sg = cmk(0.0, 0.0), sg2 = cmk(0.0, 0.0);
+    auto load_row = [&](int m, cplx (&rr)[P], cplx& sgv) {
 #pragma unroll
-    for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
-    if (blk >= 0 && mine < K) {
-      const long long node = cond_node(a, mine, att);
-      sg = __ldg(&a.twN[node]);
-      lsig[mine] = sg;
-      const cplx* wr = W + node * rowstride + (mine % rows) * P;
+      for (int i = 0; i < P; ++i) rr[i] = cmk(0.0, 0.0);
+      if (m < K) {
+        const int pidx = perm_of(m / rows, a.ord_stride[att], a.ord_reverse[att], a.count);
+        const int cs = a.noff == 1 ? 0 : (pidx & 1), tt = a.noff == 1 ? pidx : (pidx >> 1);
+        sgv = __ldg(&a.twN[node_of(a, pidx)]);
+        lsig[m] = sgv;
+        const cplx* wr = wl + (cs * M + tt) * RP + (m % rows) * P;
 #pragma unroll
-      for (int i = 0; i < P; ++i) r[i] = wr[i];
+        for (int i = 0; i < P; ++i) rr[i] = wr[i];
+      }
+    };
+    if (warp == 0) load_row(lane, r, sg);
+    if (hold) {
+      load_row(32 * hb1 + lane, r, sg);
+      if (hb2 < H) load_row(32 * hb2 + lane, r2, sg2);
     }
     if (tid < 2) flag[tid] = 0;
-    if (tid == 0) sviol = 0;
+    if (tid == 0) bk.viol_try = 0;
     cplx c[DB][P];  // basis row (basis warps only; set in their branch)
     RowState st;
     st.dmax = 0;
@@ -1553,7 +1624,7 @@ __global__ void __launch_bounds__(512, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
       const double thr2 = a.thr * a.thr;
       int cd[P];
 #pragma unroll
-      for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
+      for (int i = 0; i < P; ++i) cd[i] = cd0[i];
       for (int b = 0; b < H; ++b) {
         if (b > 0) {
           while (ld_acquire(&flag[1]) < b) {
@@ -1562,7 +1633,7 @@ __global__ void __launch_bounds__(512, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
           for (int i = 0; i < P; ++i) r[i] = xfer[lane * P + i];
           sg = lsig[min(32 * b + lane, K - 1)];
         }
-        if (g_chain_trace_on && sys == 0 && round == 0 && lane == 0) g_chain_trace[3072 + b] = clock64();
+        if (lane == 0 && b < 12) tsm[b] = clock64();
         const int tend = min(K, 32 * b + 32);
         for (int t = 32 * b; t < tend; ++t) {
           const int src = t & 31;
@@ -1596,30 +1667,45 @@ __global__ void __launch_bounds__(512, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
           for (int i = 0; i < P; ++i) cd[i] += (i == j);
         }
       }
-      if (g_chain_trace_on && sys == 0 && round == 0 && lane == 0) g_chain_trace[3072 + 9] = clock64();
-    } else if (blk >= 1) {
-      // ---------------- holder of block blk: steps < 32 blk ----------------
-      const int tlim = 32 * blk;
-      int avail = 0;
-      for (int t = 0; t < tlim; ++t) {
+      if (lane == 0) tsm[12] = clock64();
+    } else if (hold) {
+      // ---------------- holder of blocks hb1, hb2: steps < 32 hb ----------------
+      auto step_row = [&](int t, int j, cplx (&rr)[P], cplx sgv) {
+        const cplx rj = sel<P>(rr, j);
+        const cplx c2 = cmul(lci[t], rj);
+        const cplx nj = cmul(rj, csub(sgv, lsig[t]));
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const cplx v = cfma(lf[t * P + i], c2, rr[i]);
+          rr[i] = (i == j) ? nj : v;
+        }
+      };
+      auto hand_over = [&](int b, const cplx (&rr)[P]) {
+        while (ld_acquire(&flag[1]) < b - 1) __nanosleep(TR_SPIN_NS);
+#pragma unroll
+        for (int i = 0; i < P; ++i) xfer[lane * P + i] = rr[i];
+        __syncwarp();
+        if (lane == 0) st_release(&flag[1], b);
+      };
+      const bool two = hb2 < H;
+      int avail = 0, t = 0;
+      for (; t < 32 * hb1; ++t) {
         avail = wait_steps(&flag[0], t, avail);
         const int j = lj[t];
         if (j >= 0) {
-          const cplx rj = sel<P>(r, j);
-          const cplx c2 = cmul(lci[t], rj);
-          const cplx nj = cmul(rj, csub(sg, lsig[t]));
-#pragma unroll
-          for (int i = 0; i < P; ++i) {
-            const cplx v = cfma(lf[t * P + i], c2, r[i]);
-            r[i] = (i == j) ? nj : v;
-          }
+          step_row(t, j, r, sg);
+          if (two) step_row(t, j, r2, sg2);
         }
       }
-      while (ld_acquire(&flag[1]) < blk - 1) __nanosleep(TR_SPIN_NS);
-#pragma unroll
-      for (int i = 0; i < P; ++i) xfer[lane * P + i] = r[i];
-      __syncwarp();
-      if (lane == 0) st_release(&flag[1], blk);
+      hand_over(hb1, r);
+      if (two) {
+        for (; t < 32 * hb2; ++t) {
+          avail = wait_steps(&flag[0], t, avail);
+          const int j = lj[t];
+          if (j >= 0) step_row(t, j, r2, sg2);
+        }
+        hand_over(hb2, r2);
+      }
     } else if (brow >= 0) {
       // ---------------- basis row brow: replay published steps ----------------
       int deg[P];
@@ -1653,41 +1739,232 @@ __global__ void __launch_bounds__(512, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
         }
 #undef TR_RUN3
       }
+      // column maxima of this row (ref tanint.py:179-183)
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        double m = 0.0;
+#pragma unroll
+        for (int d = 0; d < DB; ++d) m = fmax(m, cabs2(c[d][i]));
+        m = wmax(m);
+        if (lane == 0) red[brow][i] = m;
+      }
+      if (__any_sync(FULL, st.big) && lane == 0) bk.viol_try = 1;
     }
     __syncthreads();
-    if (brow >= 0 && __any_sync(FULL, st.big) && lane == 0) sviol = 1;
-    // chain epilogue (warp 0): basis length, ledger, deferrals (ref tanint.py:200-206)
+    if (tid == 0) tsm[13] = clock64();
+    // ---- chain epilogue (warp 0): length, ledger, deferrals in step order (ref tanint.py:200-206)
     if (warp == 0) {
       int len = 1, nd = 0;
       int cdf[P];
 #pragma unroll
-      for (int i = 0; i < P; ++i) cdf[i] = a.cd[sys * 8 + i];
+      for (int i = 0; i < P; ++i) cdf[i] = cd0[i];
       for (int base = 0; base < K; base += 32) {
         const int t = base + lane;
         const int j = t < K ? lj[t] : -2;
         const unsigned def = __ballot_sync(FULL, j == -1);
         len += __popc(__ballot_sync(FULL, j >= 0));
-        if (j == -1) dlog[nd + __popc(def & ((1u << lane) - 1u))] = make_int2((int)cond_node(a, t, att), t % rows);
+        if (j == -1) dtry[nd + __popc(def & ((1u << lane) - 1u))] = make_int2((int)cond_node(a, t, att), t % rows);
         nd += __popc(def);
 #pragma unroll
         for (int i = 0; i < P; ++i) cdf[i] += __popc(__ballot_sync(FULL, j == i));
       }
       if (lane == 0) {
-        s.ndef_try[sys] = nd;
-        s.len_try[sys] = len;
+        bk.nd_try = nd;
+        bk.len_try = len;
 #pragma unroll
-        for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cdf[i];
+        for (int i = 0; i < P; ++i) bk.cd_try[i] = cdf[i];
+      }
+    } else if (tid < 32 + P && tid >= 32) {
+      const int i = tid - 32;
+      double m = 0.0;
+      for (int k = 0; k < P; ++k) m = fmax(m, red[k][i]);
+      m = sqrt(m);
+      csafe[i] = m > 0.0 ? m : 1.0;
+    }
+    __syncthreads();
+    // ---- normalise and write the attempt's basis (round 0: out, else scratch) ----
+    cplx* dst = (round == 0 ? a.out : a.scratch) + (long long)sys * a.out_sys;
+    if (brow >= 0) {
+      const int k = brow;
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const double inv = 1.0 / csafe[i];
+#pragma unroll
+        for (int d = 0; d < DB; ++d) {
+          const int l = 32 * d + lane;
+          const cplx v = cscale(c[d][i], inv);
+          if (l < cap) dst[(long long)(k * P + i) * cap + l] = v;
+          cbuf[(k * P + i) * CAPR + l] = v;
+        }
       }
     }
-    if (g_chain_trace_on && sys == 0 && round == 0 && lane == 0 && (warp == 0 || brow >= 0))
-      g_chain_trace[3072 + (warp == 0 ? 10 : 11 + brow)] = clock64();
+    if (cap > CAPR) {
+      const int tail = cap - CAPR;
+      for (int e = tid; e < PP * tail; e += nt) dst[(long long)(e / tail) * cap + CAPR + e % tail] = cmk(0.0, 0.0);
+    }
     __syncthreads();
-    finish_attempt<P, DB>(a, s, round, sys, c, brow, stage, wtab, twl, gbuf, vbuf, cbuf, red, csafe, wred, &sviol,
-                          nw);
-    if (g_chain_trace_on && sys == 0 && round == 0 && tid == 0) g_chain_trace[3072 + 20] = clock64();
+    if (tid == 0) tsm[14] = clock64();
+    // ---- self-residual (ref tanint.py:262-270): fold + M-point DFT per coset ----
+    const int len = min(min(bk.len_try, cap), CAPR);
+    double resm = 0.0;
+    for (int cs = 0; cs < a.noff; ++cs) {
+      const cplx* tw = twl + cs * CAPR;
+      for (int e = tid; e < PP * M; e += nt) {
+        const int pq = e / M, q = e % M;
+        const cplx* src = cbuf + (size_t)pq * CAPR;
+        cplx a0 = cmk(0.0, 0.0), a1 = cmk(0.0, 0.0);
+        int l = q;
+        for (; l + M < len; l += 2 * M) {
+          a0 = cfma(src[l], tw[l], a0);
+          a1 = cfma(src[l + M], tw[l + M], a1);
+        }
+        if (l < len) a0 = cfma(src[l], tw[l], a0);
+        gbuf[e] = cadd(a0, a1);
+      }
+      __syncthreads();
+      if (tid == 0) tsm[16 + 3 * cs] = clock64();
+      // M-point DFT of every folded entry: the node power w = omega^(q t)
+      // runs as a recurrence (re-anchored from the table every 16 terms), so
+      // the loop reads only the broadcast fold values from shared memory
+      for (int e = tid; e < P * M; e += nt) {
+        const int k = e / M, t = e % M;
+        const cplx* g = gbuf + (size_t)k * P * M;
+        const cplx wt = wtab[t];
+        cplx acc[P];
+#pragma unroll
+        for (int i = 0; i < P; ++i) acc[i] = cmk(0.0, 0.0);
+        cplx w = cmk(1.0, 0.0);
+        int kk = 0;
+        for (int q = 0; q < M; ++q) {
+          if ((q & 15) == 0) w = wtab[kk];
+#pragma unroll
+          for (int i = 0; i < P; ++i) acc[i] = cfma(g[i * M + q], w, acc[i]);
+          w = cmul(w, wt);
+          kk += t;
+          if (kk >= M) kk -= M;
+        }
+#pragma unroll
+        for (int i = 0; i < P; ++i) vbuf[(k * P + i) * M + t] = acc[i];
+      }
+      __syncthreads();
+      if (tid == 0) tsm[17 + 3 * cs] = clock64();
+      for (int e = tid; e < M * RP; e += nt) {
+        const int tt = e / RP, rem = e % RP;
+        const int rr = rem / P, jj = rem % P;
+        const cplx* wrow = wl + (cs * M + tt) * RP + rr * P;
+        cplx acc = cmk(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < P; ++i) acc = cfma(wrow[i], vbuf[(i * P + jj) * M + tt], acc);
+        resm = fmax(resm, cabs2(acc));
+      }
+      __syncthreads();
+      if (tid == 0) tsm[18 + 3 * cs] = clock64();
+    }
+    resm = wmax(resm);
+    if (lane == 0) wred[warp] = resm;
     __syncthreads();
-    if (s.need[sys] != round + 1) break;
+    if (tid == 0) {
+      tsm[15] = clock64();
+      if (g_chain_trace_on && sys == 0 && round < 4)
+        for (int e = 0; e < 24; ++e) g_chain_trace[3072 + 32 * round + e] = tsm[e];
+    }
+    // ---- best attempt, retry or commit ----
+    if (tid == 0) {
+      double rm = 0.0;
+      for (int w = 0; w < nw; ++w) rm = fmax(rm, wred[w]);
+      bk.res_try = (bk.scale == 0.0) ? 0.0 : sqrt(rm) / bk.scale;
+      double factor = 1.0;
+      for (int i = 0; i < P; ++i) factor = fmax(factor, csafe[i]);
+      bk.factor_try = factor;
+    }
+    if constexpr (CL) {
+      if (round < 2) {
+        // attempts 0 and 1 finished side by side: rank 0 applies the retry
+        // rule to both in order (the partner's book and deferrals via DSMEM)
+        cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+        cl.sync();
+        F3Book* pb = cl.map_shared_rank(&bk, 1);
+        int2* pd = cl.map_shared_rank(dtry, 1);
+        if (rank == 0) {
+          if (tid == 0) {
+            int nx = f3_pick(bk, bk, 0, P, a.nattempts, a.check_tol);
+            if (!(nx & 6)) {
+              const int n1 = f3_pick(bk, *pb, 1, P, a.nattempts, a.check_tol);
+              nx = (nx & 1) | (n1 << 3);  // bits 3..5: attempt 1's verdict
+            }
+            bk.next = nx;
+          }
+          __syncthreads();
+          const int nx = bk.next;
+          const int n1 = nx >> 3;
+          if ((nx & 1) && !(n1 & 1)) {
+            for (int e = tid; e < bk.nd_try; e += nt) dbest[e] = dtry[e];
+          }
+          if (n1 & 1) {
+            const int nd = pb->nd_try;
+            for (int e = tid; e < nd; e += nt) dbest[e] = pd[e];
+            cplx* o = a.out + (long long)sys * a.out_sys;
+            const cplx* sd = a.scratch + (long long)sys * a.out_sys;
+            for (long long e = tid; e < (long long)PP * cap; e += nt) o[e] = sd[e];
+          }
+        }
+        cl.sync();  // the partner's shared memory is no longer read
+        if (rank == 1) return;
+        const int nx = bk.next;
+        const int n1 = nx >> 3;
+        if ((nx & 4) || (n1 & 4)) {
+          viol = true;
+          break;
+        }
+        if ((nx & 2) || (n1 & 2)) break;
+        round = 1;  // continue with attempt 2
+        __syncthreads();
+        continue;
+      }
+    }
+    if (tid == 0) bk.next = f3_pick(bk, bk, round, P, a.nattempts, a.check_tol);
     __syncthreads();
+    const int nx = bk.next;
+    if (nx & 4) {
+      viol = true;
+      break;
+    }
+    if (nx & 1) {
+      const int nd = bk.nd_try;
+      for (int e = tid; e < nd; e += nt) dbest[e] = dtry[e];
+      if (round > 0) {
+        cplx* o = a.out + (long long)sys * a.out_sys;
+        for (long long e = tid; e < (long long)PP * cap; e += nt) o[e] = dst[e];
+      }
+    }
+    if (nx & 2) break;
+    __syncthreads();
+  }
+  __syncthreads();
+  if (g_chain_trace_on && sys == 0 && tid == 0) g_chain_trace[3072 + 128] = clock64();
+  // ---- commit (ref tanint.py:430-434) or hand the leaf to the exact kernel ----
+  if (viol) {
+    if (tid == 0) {
+      s.viol[sys] = 1;
+      s.need[sys] = SPLIT_EXACT;
+    }
+    return;
+  }
+  const int base = a.dcount[sys];
+  const int nb = bk.nd_best;
+  const int room = a.dmax - base;
+  const int nput = nb < room ? nb : room;
+  for (int e = tid; e < nput; e += nt) a.defer[(long long)sys * a.dmax + base + e] = dbest[e];
+  if (tid < P) a.cd[sys * 8 + tid] = bk.cd_best[tid];
+  if (tid == 0) {
+    s.viol[sys] = 0;
+    a.dcount[sys] = base + nb;
+    if (nb > room) a.status[sys] = 5;
+    a.max_scale[sys] = fmax(a.max_scale[sys], bk.factor_best);
+    if (round > 0) a.retried[sys] += 1;
+    if (a.res_out) a.res_out[sys] = bk.res_best;
+    if (a.len_out) a.len_out[sys] = bk.len_best;
+    s.need[sys] = SPLIT_DONE;
   }
 }
 
@@ -1752,6 +2029,36 @@ bool leaf_fast_supported(const LeafArgs& a) {
   return BasisSmem::bytes(a.K, a.P, a.M, db) <= 220 * 1024;
 }
 
+template <int P, int DB, int NTH, bool CL>
+int launch_f3(const LeafArgs& a, const SplitState& s, int nsys, int nw, size_t fs, cudaStream_t st) {
+  static int max_threads = -1;
+  if (max_threads < 0) {
+    cudaFuncSetAttribute(leaf_fused3_kernel<P, DB, NTH, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    cudaFuncAttributes fa;
+    TR_CUDA_CHECK(cudaFuncGetAttributes(&fa, leaf_fused3_kernel<P, DB, NTH, CL>));
+    max_threads = fa.maxThreadsPerBlock;
+    if (getenv("TR_DEBUG"))
+      fprintf(stderr, "fused3<%d,%d,%d,%d>: regs %d max threads %d\n", P, DB, NTH, (int)CL, fa.numRegs,
+              fa.maxThreadsPerBlock);
+  }
+  if (32 * nw > max_threads) return -1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(CL ? 2 * nsys : nsys));
+  cfg.blockDim = dim3(32 * nw);
+  cfg.dynamicSmemBytes = fs;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL ? 2 : 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = CL ? 1 : 0;
+  TR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, leaf_fused3_kernel<P, DB, NTH, CL>, a, s));
+  return 0;
+}
+
 // fused attempts with the lane-resident chain (leaf_fused3_kernel): one
 // launch per leaf; returns -1 when the shape does not fit it
 int launch_fused3(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t st) {
@@ -1759,18 +2066,13 @@ int launch_fused3(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t
   if (fv && fv[0] == '0') return -1;
   if (nsys > 148) return -1;
   const int H = (a.K + 31) / 32;
-  const int last = H + a.P - 1;  // highest slot
+  const int last = H / 2 + a.P;  // highest slot: H/2 holders, then the basis rows
   int nw = 1;
   while (nw - 1 - (nw - 1) / 4 < last) ++nw;
   if (nw > 16) return -1;
   const int db = blocks_planned(a);
   if (db > (a.P == 5 ? 4 : 3)) return -1;
-  size_t fs = Fused3Smem::bytes(a.K, a.P, a.M, db, true);
-  int stage = 1;
-  if (fs > 200 * 1024) {
-    fs = Fused3Smem::bytes(a.K, a.P, a.M, db, false);
-    stage = 0;
-  }
+  const size_t fs = Fused3Smem::bytes(a.K, a.P, a.M, db);
   if (fs > 200 * 1024) return -1;
   {
     const double K = a.K, P = a.P;
@@ -1778,24 +2080,19 @@ int launch_fused3(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t
     tr_kernel_work(TRK_LEAF_BUILD, 16.0 * nsys * (P * P * (K + 1) + K * P),
                    4.0 * nsys * P * P * K * (K + 1) + 8.0 * nsys * (double)a.noff * P * P * a.M * a.M);
   }
+  // attempts 0 and 1 side by side (2-CTA clusters) while the batch leaves
+  // SMs idle: the retry tail of a leaf then costs no extra chain time
+  static const char* cv2 = getenv("TR_F3_PAIR");  // TR_F3_PAIR=0: sequential attempts
+  const bool cl = a.nattempts > 1 && 2 * nsys <= 148 && !(cv2 && cv2[0] == '0');
+  int rc = 0;
   TrKTimer _kt(TRK_LEAF_PIVOT, st);
 #define TR_F3N(PP_, DB_, NTH_)                                                                             \
   {                                                                                                        \
-    static bool set = false;                                                                               \
-    if (!set) {                                                                                            \
-      cudaFuncSetAttribute(leaf_fused3_kernel<PP_, DB_, NTH_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           200 * 1024);                                                                    \
-      cudaFuncAttributes fa;                                                                               \
-      cudaFuncGetAttributes(&fa, leaf_fused3_kernel<PP_, DB_, NTH_>);                                      \
-      if (getenv("TR_DEBUG"))                                                                              \
-        fprintf(stderr, "fused3<%d,%d,%d>: regs %d maxthreads %d smem %zu dyn %zu\n", PP_, DB_, NTH_,       \
-                fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, fs);                                \
-      set = true;                                                                                          \
-    }                                                                                                      \
-    leaf_fused3_kernel<PP_, DB_, NTH_><<<nsys, 32 * nw, fs, st>>>(a, s, stage);                           \
+    if (cl) rc = launch_f3<PP_, DB_, NTH_, true>(a, s, nsys, nw, fs, st);                                  \
+    else rc = launch_f3<PP_, DB_, NTH_, false>(a, s, nsys, nw, fs, st);                                    \
   }
 #define TR_F3L(PP_, DB_)                  \
-  if (nw <= 14) TR_F3N(PP_, DB_, 448)     \
+  if (nw <= 12) TR_F3N(PP_, DB_, 384)     \
   else TR_F3N(PP_, DB_, 512)
   if (a.P == 5) {
     switch (db) {
@@ -1813,6 +2110,7 @@ int launch_fused3(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t
   }
 #undef TR_F3L
 #undef TR_F3N
+  if (rc) return rc;  // -1: does not fit, the caller falls back
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }

@@ -997,36 +997,102 @@ struct GraphEntry {
 std::mutex g_graph_mu;
 std::map<std::string, GraphEntry> g_graphs;
 
-int run_solve(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx* x_out, int refine,
-              cudaStream_t st, void* ws) {
+// A batch may be split into groups that run on their own streams (captured
+// into the same graph): the leaf sweeps of one group (latency-bound, one SM
+// per system) then overlap the batched FFT / combine launches of the others.
+struct Group {
+  long long first = 0, count = 0;
+  size_t off = 0;  // workspace offset
+  Inputs in;
+  WS w;
+  cplx* x = nullptr;
+};
+
+int batch_groups(long long batch) {
+  static const char* e = getenv("TR_GROUPS");
+  int g = 1;
+  if (e) g = atoi(e);
+  else if (batch >= 32 && batch <= 148) g = 2;
+  if (g < 1) g = 1;
+  if (g > 4) g = 4;
+  if (g > batch) g = (int)batch;
+  return g;
+}
+
+// group sizes and workspace offsets (the same split for sizing and solving)
+size_t plan_groups(const Plan& p, long long batch, std::vector<Group>* out) {
+  const int G = batch_groups(batch);
+  size_t off = 0;
+  long long first = 0;
+  for (int g = 0; g < G; ++g) {
+    Group gr;
+    gr.first = first;
+    gr.count = batch / G + (g < batch % G ? 1 : 0);
+    gr.off = off;
+    WS w;
+    off += (layout(p, gr.count, nullptr, &w) + 255) & ~(size_t)255;
+    first += gr.count;
+    if (out) out->push_back(gr);
+  }
+  return off;
+}
+
+int solve_groups(const Plan& p, std::vector<Group>& gs, int refine, cudaStream_t st) {
+  static thread_local cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
+  static thread_local cudaEvent_t fork = nullptr, join[4] = {nullptr, nullptr, nullptr, nullptr};
+  const int G = (int)gs.size();
+  if (G == 1 || g_timing.load()) {  // kernel timing: one stream, groups in order
+    for (auto& g : gs) TR_TRY(solve_chunk(p, g.in, g.count, g.w, g.x, refine, st, nullptr));
+    return 0;
+  }
+  if (!fork) {
+    TR_CUDA_CHECK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    for (int i = 0; i < 4; ++i) {
+      TR_CUDA_CHECK(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
+      TR_CUDA_CHECK(cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming));
+    }
+  }
+  TR_CUDA_CHECK(cudaEventRecord(fork, st));
+  for (int g = 1; g < G; ++g) {
+    TR_CUDA_CHECK(cudaStreamWaitEvent(side[g], fork, 0));
+    TR_TRY(solve_chunk(p, gs[g].in, gs[g].count, gs[g].w, gs[g].x, refine, side[g], nullptr));
+    TR_CUDA_CHECK(cudaEventRecord(join[g], side[g]));
+  }
+  TR_TRY(solve_chunk(p, gs[0].in, gs[0].count, gs[0].w, gs[0].x, refine, st, nullptr));
+  for (int g = 1; g < G; ++g) TR_CUDA_CHECK(cudaStreamWaitEvent(st, join[g], 0));
+  return 0;
+}
+
+int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine, cudaStream_t st, void* ws) {
   static const char* env = getenv("TR_GRAPHS");
   static const bool trace = getenv("TR_LEAF_TRACE") != nullptr;
   const bool graphs = !(env && env[0] == '0') && !trace && !g_timing.load();
-  if (!graphs) return solve_chunk(p, in, nsys, w, x_out, refine, st, nullptr);
+  if (!graphs) return solve_groups(p, gs, refine, st);
+  const Inputs& in = gs[0].in;
   int dev = 0;
   cudaGetDevice(&dev);
   char key[512];
-  snprintf(key, sizeof key, "%d|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%d|%p|%p|%d", dev,
+  snprintf(key, sizeof key, "%d|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%d|%p|%p|%d|%d", dev,
            (const void*)&p, nsys, (const void*)in.T, in.T_bs, (const void*)in.L, in.L_bs,
            (const void*)in.G, in.G_bs, (const void*)in.beta_sq, in.beta_bs, (const void*)in.rhs,
-           in.rhs_bs, in.rhs_is_normal, (void*)x_out, ws, refine);
+           in.rhs_bs, in.rhs_is_normal, (void*)gs[0].x, ws, refine, (int)gs.size());
   std::lock_guard<std::mutex> lk(g_graph_mu);
   GraphEntry& e = g_graphs[key];
   e.calls += 1;
-  if (!e.exec && e.calls < 2) return solve_chunk(p, in, nsys, w, x_out, refine, st, nullptr);
-  static thread_local cudaStream_t gs = nullptr;
+  if (!e.exec && e.calls < 2) return solve_groups(p, gs, refine, st);
+  static thread_local cudaStream_t gst = nullptr;
   static thread_local cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  if (!gs) {
-    TR_CUDA_CHECK(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+  if (!gst) {
+    TR_CUDA_CHECK(cudaStreamCreateWithFlags(&gst, cudaStreamNonBlocking));
     TR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
     TR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
   }
   if (!e.exec) {
     cudaGraph_t g = nullptr;
     const long long n0 = g_launches.load();
-    TR_CUDA_CHECK(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
-    int rc = solve_chunk(p, in, nsys, w, x_out, refine, gs, nullptr);
-    cudaError_t ce = cudaStreamEndCapture(gs, &g);
+    TR_CUDA_CHECK(cudaStreamBeginCapture(gst, cudaStreamCaptureModeThreadLocal));
+    int rc = solve_groups(p, gs, refine, gst);
+    cudaError_t ce = cudaStreamEndCapture(gst, &g);
     if (rc) {
       if (g) cudaGraphDestroy(g);
       return rc;
@@ -1046,9 +1112,9 @@ int run_solve(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
     }
   }
   TR_CUDA_CHECK(cudaEventRecord(ev_in, st));
-  TR_CUDA_CHECK(cudaStreamWaitEvent(gs, ev_in, 0));
-  TR_CUDA_CHECK(cudaGraphLaunch(e.exec, gs));
-  TR_CUDA_CHECK(cudaEventRecord(ev_out, gs));
+  TR_CUDA_CHECK(cudaStreamWaitEvent(gst, ev_in, 0));
+  TR_CUDA_CHECK(cudaGraphLaunch(e.exec, gst));
+  TR_CUDA_CHECK(cudaEventRecord(ev_out, gst));
   TR_CUDA_CHECK(cudaStreamWaitEvent(st, ev_out, 0));
   g_launches.fetch_add(e.nodes);
   return 0;
@@ -1060,8 +1126,8 @@ int run_solve(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
 extern "C" size_t tr_workspace_bytes(const tr_desc* d, int64_t batch) {
   Plan* p;
   if (get_plan(d, &p)) return 0;
-  WS w;
-  return layout(*p, batch, nullptr, &w);
+  if (batch <= 0) return 0;
+  return plan_groups(*p, batch, nullptr);
 }
 
 extern "C" int tr_plan_info(const tr_desc* d, int64_t* order, int64_t* leaves, int32_t* depth,
@@ -1084,8 +1150,8 @@ extern "C" int tr_solve_batch(const tr_desc* d, int64_t batch, const double* T_g
   TR_TRY(get_plan(d, &p));
   if (batch <= 0) return 0;
   TR_TRY(ensure_fft(p));
-  WS w;
-  size_t need = layout(*p, batch, nullptr, &w);
+  std::vector<Group> gs;
+  const size_t need = plan_groups(*p, batch, &gs);
   if (!workspace || ws_bytes < need) {
     tr_set_error("workspace too small: need %zu bytes, got %zu", need, ws_bytes);
     return 2;
@@ -1095,26 +1161,29 @@ extern "C" int tr_solve_batch(const tr_desc* d, int64_t batch, const double* T_g
   if (p->variant == TR_GRAMIAN && !G_col) { tr_set_error("G column required"); return 2; }
   if (p->variant == TR_L2 && !beta_sq) { tr_set_error("beta_sq required"); return 2; }
   if (!rhs || !x_out) { tr_set_error("rhs and x_out required"); return 2; }
-  layout(*p, batch, (char*)workspace, &w);
-  static const double zero = 0.0;
-  (void)zero;
-  Inputs in;
-  in.T = reinterpret_cast<const cplx*>(T_gen);
-  in.L = reinterpret_cast<const cplx*>(L_gen);
-  in.G = reinterpret_cast<const cplx*>(G_col);
-  in.rhs = reinterpret_cast<const cplx*>(rhs);
-  in.T_bs = T_bs;
-  in.L_bs = L_bs;
-  in.G_bs = G_bs;
-  in.rhs_bs = rhs_bs;
-  in.beta_sq = beta_sq;
-  in.beta_bs = beta_bs;
-  in.rhs_is_normal = rhs_is_normal;
-  // beta_sq is only read for l2; point others at the workspace norm slot
-  if (!in.beta_sq) { in.beta_sq = w.nrm; in.beta_bs = 0; }
+  for (auto& g : gs) {
+    layout(*p, g.count, (char*)workspace + g.off, &g.w);
+    Inputs& in = g.in;
+    const long long f = g.first;
+    in.T = T_gen ? reinterpret_cast<const cplx*>(T_gen) + f * T_bs : nullptr;
+    in.L = L_gen ? reinterpret_cast<const cplx*>(L_gen) + f * L_bs : nullptr;
+    in.G = G_col ? reinterpret_cast<const cplx*>(G_col) + f * G_bs : nullptr;
+    in.rhs = reinterpret_cast<const cplx*>(rhs) + f * rhs_bs;
+    in.T_bs = T_bs;
+    in.L_bs = L_bs;
+    in.G_bs = G_bs;
+    in.rhs_bs = rhs_bs;
+    in.beta_sq = beta_sq ? beta_sq + f * beta_bs : nullptr;
+    in.beta_bs = beta_bs;
+    in.rhs_is_normal = rhs_is_normal;
+    // beta_sq is only read for l2; point others at the workspace norm slot
+    if (!in.beta_sq) { in.beta_sq = g.w.nrm; in.beta_bs = 0; }
+    g.x = reinterpret_cast<cplx*>(x_out) + f * p->n;
+  }
   cudaStream_t st = (cudaStream_t)stream;
-  TR_TRY(run_solve(*p, in, batch, w, reinterpret_cast<cplx*>(x_out), d->refine, st, workspace));
-  if (diag_host) TR_TRY(read_diag(*p, batch, w, st, diag_host));
+  TR_TRY(run_solve(*p, gs, batch, d->refine, st, workspace));
+  if (diag_host)
+    for (auto& g : gs) TR_TRY(read_diag(*p, g.count, g.w, st, diag_host + g.first));
   if (diag_host) {
     for (long long s = 0; s < batch; ++s) {
       if (diag_host[s].status == 3) return 3;

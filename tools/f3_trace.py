@@ -1,4 +1,5 @@
-"""Phase clock trace of leaf_fused3_kernel (system 0, round 0, last leaf)."""
+"""Phase clock trace of leaf_fused3_kernel (system 0, last leaf): per round
+[start, decider end, basis end, normalise, residual] and the commit."""
 import ctypes as C, os, sys
 import numpy as np, torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -19,8 +20,13 @@ f(1, None, 0)
 db.run(); torch.cuda.synchronize()
 buf = (C.c_longlong * 4096)()
 f(0, C.addressof(buf), 4096)
-b = np.frombuffer(buf, dtype=np.int64)[3072:3072 + 24].copy()
+b = np.frombuffer(buf, dtype=np.int64)[3072:3072 + 129].copy()
 t0 = b[0]
-print("block starts:", [int(x - t0) for x in b[:9] if x > 0])
-print("decider end %d; loop end decider %d; basis ends %s; finish end %d" % (
-    b[9] - t0, b[10] - t0, [int(x - t0) for x in b[11:18] if x > 0], b[20] - t0))
+for r in range(4):
+    x = b[32 * r:32 * r + 24]
+    if x[0] > 0 and abs(x[0] - t0) < 1e8:
+        blocks = [int(v - x[0]) for v in x[:12] if 0 < v - x[0] < 1e8]
+        print("round %d: start %d, block starts %s, decider end %d, chain+basis %d, normalised %d, residual %d"
+              % (r, x[0] - t0, blocks, x[12] - x[0], x[13] - x[0], x[14] - x[0], x[15] - x[0]))
+        print("   residual detail (fold, dft, rows per coset):", [int(v - x[0]) for v in x[16:22]])
+print("commit at %d" % (b[128] - t0))
