@@ -105,6 +105,44 @@ int tr_solve_batch_host(const tr_desc* d, int64_t batch,
                         const double* rhs, int64_t rhs_bs, int32_t rhs_is_normal,
                         double* x_out, tr_diag* diag_host);
 
+/* Conjugate gradients from a zero start on the normal equations, batched
+ * (replaces toepreg.solver.cg_solve, pkg/src/toepreg/solver.py:184-215).
+ * Same inputs as tr_solve_batch; max_iterations <= 0 means the reference
+ * default max(10 n, 100); systems stop individually at
+ * ||r|| <= tolerance ||rhs||; time_budget > 0 is checked after completed
+ * iterations.  x_out [batch][n] device, iterations [batch] host.  The
+ * workspace is tr_cg_workspace_bytes(d, batch). */
+size_t tr_cg_workspace_bytes(const tr_desc* d, int64_t batch);
+int tr_cg_batch(const tr_desc* d, int64_t batch,
+                const double* T_gen, int64_t T_bs,
+                const double* L_gen, int64_t L_bs,
+                const double* G_col, int64_t G_bs,
+                const double* beta_sq, int64_t beta_bs,
+                const double* rhs, int64_t rhs_bs, int32_t rhs_is_normal,
+                int64_t max_iterations, double tolerance, double time_budget,
+                double* x_out, int64_t* iterations,
+                void* workspace, size_t ws_bytes, void* stream);
+
+/* y = A x with A the normal matrix (replaces NormalOperator.apply,
+ * pkg/src/toepreg/solver.py:104-167): T^H T + |beta|^2 I (l2),
+ * T^H T + L^H L (general), G + L^H L (gramian).  x, y [batch][n] device;
+ * workspace as tr_cg_workspace_bytes. */
+int tr_normal_apply(const tr_desc* d, int64_t batch,
+                    const double* T_gen, int64_t T_bs,
+                    const double* L_gen, int64_t L_bs,
+                    const double* G_col, int64_t G_bs,
+                    const double* beta_sq, int64_t beta_bs,
+                    const double* x, double* y,
+                    void* workspace, size_t ws_bytes, void* stream);
+
+/* Nonuniform Fourier sums for the Gramian setup (replaces the dense
+ * exp(outer(...)) forms of pkg/src/toepreg/nufft.py:60-72 and :106-114):
+ *   adjoint != 0: out[d] = sum_{k<K} in[k] exp(sign 2 pi i freqs[k] d), d < n
+ *   adjoint == 0: out[k] = sum_{j<n} in[j] exp(sign 2 pi i freqs[k] j), k < K
+ * freqs [K] float64, in / out complex128 (interleaved); device pointers. */
+int tr_nudft(const double* freqs, int64_t K, int64_t n, const double* in, int32_t adjoint,
+             int32_t sign, double* out, void* stream);
+
 /* Stage entry points mirroring reference helpers, for stage-level parity:
  *  tr_grid_eval   ~ fftpoly.grid_eval(coeffs, N, offset, stride) (:64-89)
  *  tr_fft         ~ batched unnormalised DFT, sign +1/-1

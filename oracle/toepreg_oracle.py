@@ -652,3 +652,46 @@ def cg_exact(problem, tol=1e-15, max_iter=None):
         d = r + (rho2 / rho) * d
         rho = rho2
     return x
+
+
+def cg_solve(problem, max_iterations=None, tolerance=1e-12):
+    """Plain conjugate gradients from a zero start, restating the reference's
+    cg_solve (ref:solver.py:184-215) on normal_apply; the time budget is not
+    restated.  Returns (x, iterations)."""
+    rhs = normal_rhs(problem)
+    n = rhs.size
+    x = np.zeros(n, dtype=np.complex128)
+    rhs_norm = float(np.linalg.norm(rhs))
+    if rhs_norm == 0.0:
+        return x, 0
+    limit = max_iterations if max_iterations is not None else max(10 * n, 100)
+    r = rhs.copy()
+    d = r.copy()
+    rho = float(np.vdot(r, r).real)
+    iterations = 0
+    for _ in range(limit):
+        ad = normal_apply(problem, d)
+        alpha = rho / float(np.vdot(d, ad).real)
+        x += alpha * d
+        r -= alpha * ad
+        rho_next = float(np.vdot(r, r).real)
+        iterations += 1
+        if math.sqrt(rho_next) <= tolerance * rhs_norm:
+            break
+        d = r + (rho_next / rho) * d
+        rho = rho_next
+    return x, iterations
+
+
+def nufft_gramian_col(freqs, weights, n):
+    """First column of A^H W A (ref:nufft.py:60-72), dense as the reference."""
+    lags = np.arange(n)
+    return np.einsum("k,kd->d", np.asarray(weights, dtype=np.float64) + 0j,
+                     np.exp(2j * np.pi * np.outer(np.asarray(freqs, dtype=np.float64), lags)))
+
+
+def nufft_samples_and_rhs(freqs, weights, x):
+    """Samples A x and rhs A^H (w * samples), dense (ref:nufft.py:106-114)."""
+    a = np.exp(-2j * np.pi * np.outer(freqs, np.arange(x.size)))
+    samples = a @ x
+    return samples, a.conj().T @ (weights * samples)

@@ -11,6 +11,7 @@ from .toeplitz import (HermitianToeplitzSpec, ProblemSpec, ToeplitzSpec, adjoint
                        identity_spec)
 from .solver import (DeviceBatch, SingularSystemError, SolveReport, SolverConfig,
                      TanIntDiagnostics, plan_info, solve_tikhonov, solve_tikhonov_batch)
+from .iterative import CGConfig, NormalOperator, apply_normal_operator, cg_solve, cg_solve_batch
 
 __version__ = "0.1.0"
 
@@ -18,4 +19,5 @@ __all__ = [
     "ToeplitzSpec", "HermitianToeplitzSpec", "ProblemSpec", "identity_spec", "adjoint_spec",
     "SolverConfig", "SolveReport", "TanIntDiagnostics", "SingularSystemError",
     "solve_tikhonov", "solve_tikhonov_batch", "DeviceBatch", "plan_info", "__version__",
+    "NormalOperator", "apply_normal_operator", "CGConfig", "cg_solve", "cg_solve_batch",
 ]

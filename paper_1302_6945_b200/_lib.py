@@ -61,6 +61,13 @@ SIGNATURES = {
                                  C.c_size_t, _P]),
     "tr_solve_batch_host": (C.c_int, [C.POINTER(TrDesc), _I64, _P, _I64, _P, _I64, _P, _I64,
                                       _P, _I64, _P, _I64, _I32, _P, C.POINTER(TrDiag)]),
+    "tr_cg_workspace_bytes": (C.c_size_t, [C.POINTER(TrDesc), _I64]),
+    "tr_cg_batch": (C.c_int, [C.POINTER(TrDesc), _I64, _P, _I64, _P, _I64, _P, _I64,
+                              _P, _I64, _P, _I64, _I32, _I64, C.c_double, C.c_double,
+                              _P, C.POINTER(_I64), _P, C.c_size_t, _P]),
+    "tr_normal_apply": (C.c_int, [C.POINTER(TrDesc), _I64, _P, _I64, _P, _I64, _P, _I64,
+                                  _P, _I64, _P, _P, _P, C.c_size_t, _P]),
+    "tr_nudft": (C.c_int, [_P, _I64, _I64, _P, _I32, _I32, _P, _P]),
     "tr_fft": (C.c_int, [_P, _P, _I64, _I64, _I32, _P]),
     "tr_grid_eval": (C.c_int, [_P, _I64, _I64, _I64, _I64, _I64, _P, _P]),
     "tr_matpoly_mul": (C.c_int, [_P, _I64, _P, _I64, _I32, _P, _P]),

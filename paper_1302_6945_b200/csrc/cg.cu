@@ -1,0 +1,124 @@
+// Conjugate gradients on the normal equations (ref: pkg/src/toepreg/solver.py
+// :184-215 cg_solve), batched over systems.  The operator application is the
+// FFT NormalOperator of solver.cu (normal_apply); the vector part of one
+// iteration -- alpha = rho / Re<d, Ad>, x += alpha d, r -= alpha Ad,
+// rho' = |r|^2, the stopping test, d = r + (rho'/rho) d -- is one kernel with
+// one CTA per system (two block reductions), so an iteration costs the
+// operator's transforms plus one launch and nothing syncs with the host.
+#include "kernels.cuh"
+
+namespace {
+
+constexpr int CGT = 1024;
+
+__device__ __forceinline__ double blk_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < CGT / 32; ++w) s += sh[w];  // fixed order: deterministic
+  return s;
+}
+
+__global__ void __launch_bounds__(CGT) cg_init_kernel(cplx* X, cplx* R, cplx* D, const cplx* Y, long long n,
+                                                      double* st, int* it) {
+  __shared__ double sh[CGT / 32];
+  const long long sys = blockIdx.x;
+  const cplx* y = Y + sys * n;
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += CGT) {
+    const cplx v = y[i];
+    X[sys * n + i] = cmk(0.0, 0.0);
+    R[sys * n + i] = v;
+    D[sys * n + i] = v;
+    s += cabs2(v);
+  }
+  s = blk_sum(s, sh);
+  if (threadIdx.x == 0) {
+    st[sys * 4 + 0] = s;            // rho
+    st[sys * 4 + 1] = sqrt(s);      // |rhs|
+    st[sys * 4 + 2] = s > 0.0;      // active
+    it[sys] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(CGT) cg_update_kernel(cplx* X, cplx* R, cplx* D, const cplx* AD,
+                                                        const double* beta_sq, long long beta_bs, int ridge,
+                                                        long long n, double tol, double* st, int* it) {
+  __shared__ double sh[CGT / 32];
+  const long long sys = blockIdx.x;
+  if (st[sys * 4 + 2] == 0.0) return;
+  cplx* x = X + sys * n;
+  cplx* r = R + sys * n;
+  cplx* d = D + sys * n;
+  const cplx* ad = AD + sys * n;
+  const double b2 = ridge ? beta_sq[sys * beta_bs] : 0.0;
+  // Re <d, A d> (A d = normal operator + |beta|^2 d for the ridge variant)
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += CGT) {
+    const cplx dv = d[i], av = ad[i];
+    s += dv.x * (av.x + b2 * dv.x) + dv.y * (av.y + b2 * dv.y);
+  }
+  const double dad = blk_sum(s, sh);
+  const double rho = st[sys * 4 + 0];
+  const double alpha = rho / dad;
+  s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += CGT) {
+    const cplx dv = d[i], av = ad[i];
+    const cplx adv = cmk(av.x + b2 * dv.x, av.y + b2 * dv.y);
+    x[i] = cmk(x[i].x + alpha * dv.x, x[i].y + alpha * dv.y);
+    const cplx rv = cmk(r[i].x - alpha * adv.x, r[i].y - alpha * adv.y);
+    r[i] = rv;
+    s += cabs2(rv);
+  }
+  const double rho_next = blk_sum(s, sh);
+  const bool stop = sqrt(rho_next) <= tol * st[sys * 4 + 1];
+  if (!stop) {
+    const double beta = rho_next / rho;
+    for (long long i = threadIdx.x; i < n; i += CGT) {
+      const cplx rv = r[i], dv = d[i];
+      d[i] = cmk(rv.x + beta * dv.x, rv.y + beta * dv.y);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    it[sys] += 1;
+    st[sys * 4 + 0] = rho_next;
+    if (stop) st[sys * 4 + 2] = 0.0;
+  }
+}
+
+__global__ void cg_active_kernel(const double* st, long long nsys, int* any) {
+  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int a = (s < nsys && st[s * 4 + 2] != 0.0) ? 1 : 0;
+  a = __syncthreads_or(a);
+  if (threadIdx.x == 0 && a) atomicOr(any, 1);
+}
+
+}  // namespace
+
+int launch_cg_init(cplx* X, cplx* R, cplx* D, const cplx* Y, long long n, double* st, int* it, long long nsys,
+                   cudaStream_t s) {
+  { TrKTimer _kt(TRK_NORMAL, s); cg_init_kernel<<<(unsigned)nsys, CGT, 0, s>>>(X, R, D, Y, n, st, it); }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int launch_cg_update(cplx* X, cplx* R, cplx* D, const cplx* AD, const double* beta_sq, long long beta_bs,
+                     int ridge, long long n, double tol, double* st, int* it, long long nsys, cudaStream_t s) {
+  {
+    TrKTimer _kt(TRK_NORMAL, s);
+    cg_update_kernel<<<(unsigned)nsys, CGT, 0, s>>>(X, R, D, AD, beta_sq, beta_bs, ridge, n, tol, st, it);
+  }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int launch_cg_active(const double* st, long long nsys, int* any, cudaStream_t s) {
+  TR_CUDA_CHECK(cudaMemsetAsync(any, 0, sizeof(int), s));
+  { TrKTimer _kt(TRK_NORMAL, s); cg_active_kernel<<<(unsigned)((nsys + 255) / 256), 256, 0, s>>>(st, nsys, any); }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}

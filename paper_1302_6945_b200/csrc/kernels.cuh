@@ -106,3 +106,18 @@ int launch_extract(const ExtractArgs& a, long long nsys, cudaStream_t st);
 int launch_norms(const cplx* v, long long n, long long nsys, double* partial, int nchunk,
                  double* out, cudaStream_t st);
 int launch_add_inplace(cplx* x, const cplx* d, long long n, long long nsys, cudaStream_t st);
+
+// ---- conjugate gradients (cg.cu) ----
+// st[sys][4] = {rho, |rhs|, active, -}; it[sys] = iterations done
+int launch_cg_init(cplx* X, cplx* R, cplx* D, const cplx* Y, long long n, double* st, int* it, long long nsys,
+                   cudaStream_t s);
+int launch_cg_update(cplx* X, cplx* R, cplx* D, const cplx* AD, const double* beta_sq, long long beta_bs,
+                     int ridge, long long n, double tol, double* st, int* it, long long nsys, cudaStream_t s);
+int launch_cg_active(const double* st, long long nsys, int* any, cudaStream_t s);
+
+// ---- nonuniform Fourier sums (nufft.cu) ----
+// adjoint: y[d] = sum_k c_k exp(sign 2 pi i f_k d), d < n; forward: y[k] = sum_j x_j exp(sign 2 pi i f_k j)
+int launch_nudft_adjoint(const double* f, const cplx* c, long long K, long long n, int sign, cplx* y,
+                         cudaStream_t st);
+int launch_nudft_forward(const double* f, const cplx* x, long long K, long long n, int sign, cplx* y,
+                         cudaStream_t st);

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <map>
 #include <mutex>
 #include <numeric>
@@ -1239,6 +1240,163 @@ extern "C" int tr_solve_batch_host(const tr_desc* d, int64_t batch, const double
   cudaStreamDestroy(st);
   cudaFree(dev);
   return rc;
+}
+
+// ------------------------------------------------------ conjugate gradients
+// Batched plain CG from a zero start on the normal equations (ref
+// solver.py:184-215): operator = the FFT NormalOperator (normal_apply), the
+// vector part of an iteration = one kernel (cg.cu).  Systems stop
+// individually at sqrt(rho) <= tol |rhs|; the host checks for any active
+// system every `chunk` iterations (every iteration when a time budget is
+// given, which is checked after completed iterations as in the reference).
+extern "C" size_t tr_cg_workspace_bytes(const tr_desc* d, int64_t batch) {
+  Plan* p;
+  if (get_plan(d, &p)) return 0;
+  if (batch <= 0) return 0;
+  WS w;
+  return layout(*p, batch, nullptr, &w);
+}
+
+extern "C" int tr_cg_batch(const tr_desc* d, int64_t batch, const double* T_gen, int64_t T_bs,
+                           const double* L_gen, int64_t L_bs, const double* G_col, int64_t G_bs,
+                           const double* beta_sq, int64_t beta_bs, const double* rhs, int64_t rhs_bs,
+                           int32_t rhs_is_normal, int64_t max_iterations, double tolerance,
+                           double time_budget, double* x_out, int64_t* iterations, void* workspace,
+                           size_t ws_bytes, void* stream) {
+  Plan* p;
+  TR_TRY(get_plan(d, &p));
+  if (batch <= 0) return 0;
+  TR_TRY(ensure_fft(p));
+  WS w;
+  const size_t need = layout(*p, batch, nullptr, &w);
+  if (!workspace || ws_bytes < need) {
+    tr_set_error("workspace too small: need %zu bytes, got %zu", need, ws_bytes);
+    return 2;
+  }
+  if (p->variant != TR_GRAMIAN && !T_gen) { tr_set_error("T generator required"); return 2; }
+  if (p->variant != TR_L2 && !L_gen) { tr_set_error("L generator required"); return 2; }
+  if (p->variant == TR_GRAMIAN && !G_col) { tr_set_error("G column required"); return 2; }
+  if (p->variant == TR_L2 && !beta_sq) { tr_set_error("beta_sq required"); return 2; }
+  if (!rhs || !x_out) { tr_set_error("rhs and x_out required"); return 2; }
+  if (!(tolerance >= 0.0)) { tr_set_error("tolerance must be >= 0"); return 2; }
+  layout(*p, batch, (char*)workspace, &w);
+  Inputs in;
+  in.T = reinterpret_cast<const cplx*>(T_gen);
+  in.L = reinterpret_cast<const cplx*>(L_gen);
+  in.G = reinterpret_cast<const cplx*>(G_col);
+  in.rhs = reinterpret_cast<const cplx*>(rhs);
+  in.T_bs = T_bs;
+  in.L_bs = L_bs;
+  in.G_bs = G_bs;
+  in.rhs_bs = rhs_bs;
+  in.beta_sq = beta_sq ? beta_sq : w.nrm;
+  in.beta_bs = beta_sq ? beta_bs : 0;
+  in.rhs_is_normal = rhs_is_normal;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long n = p->n;
+  long long sbs = 0;
+  TR_TRY(embed_spectra(*p, in, batch, w, st, &sbs));
+  TR_TRY(normal_rhs(*p, in, batch, w, sbs, st));
+  double* cst = w.partial;  // [sys][4] (NORM_CHUNKS >= 4)
+  int* its = w.blen;
+  int* any = w.dcount;
+  TR_TRY(launch_cg_init(w.X, w.Rv, w.X2, w.Y, n, cst, its, batch, st));
+  const long long limit = max_iterations > 0 ? max_iterations : std::max<long long>(10 * n, 100);
+  const int chunk = time_budget > 0.0 ? 1 : 16;
+  const int ridge = p->variant == TR_L2;
+  const auto t0 = std::chrono::steady_clock::now();
+  long long done = 0;
+  int host_any = 1;
+  while (done < limit) {
+    const long long k = std::min<long long>(chunk, limit - done);
+    for (long long i = 0; i < k; ++i) {
+      TR_TRY(normal_apply(*p, batch, w, sbs, w.X2, st));
+      TR_TRY(launch_cg_update(w.X, w.Rv, w.X2, w.AX, in.beta_sq, in.beta_bs, ridge, n, tolerance, cst, its,
+                              batch, st));
+    }
+    done += k;
+    TR_TRY(launch_cg_active(cst, batch, any, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(&host_any, any, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TR_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (!host_any) break;
+    if (time_budget > 0.0) {
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (el >= time_budget) break;
+    }
+  }
+  TR_CUDA_CHECK(cudaMemcpyAsync(x_out, w.X, sizeof(cplx) * batch * n, cudaMemcpyDeviceToDevice, st));
+  if (iterations) {
+    std::vector<int> h(batch);
+    TR_CUDA_CHECK(cudaMemcpyAsync(h.data(), its, sizeof(int) * batch, cudaMemcpyDeviceToHost, st));
+    TR_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (long long s = 0; s < batch; ++s) iterations[s] = h[s];
+  }
+  return 0;
+}
+
+// Normal operator on a batch (ref solver.py:104-167 NormalOperator.apply):
+// y = (T^H T + L^H L) x (+ |beta|^2 x for l2, G x + L^H L x for gramian).
+extern "C" int tr_normal_apply(const tr_desc* d, int64_t batch, const double* T_gen, int64_t T_bs,
+                               const double* L_gen, int64_t L_bs, const double* G_col, int64_t G_bs,
+                               const double* beta_sq, int64_t beta_bs, const double* x, double* y,
+                               void* workspace, size_t ws_bytes, void* stream) {
+  Plan* p;
+  TR_TRY(get_plan(d, &p));
+  if (batch <= 0) return 0;
+  TR_TRY(ensure_fft(p));
+  WS w;
+  const size_t need = layout(*p, batch, nullptr, &w);
+  if (!workspace || ws_bytes < need) {
+    tr_set_error("workspace too small: need %zu bytes, got %zu", need, ws_bytes);
+    return 2;
+  }
+  if (!x || !y) { tr_set_error("x and y required"); return 2; }
+  if (p->variant == TR_L2 && !beta_sq) { tr_set_error("beta_sq required"); return 2; }
+  layout(*p, batch, (char*)workspace, &w);
+  Inputs in;
+  in.T = reinterpret_cast<const cplx*>(T_gen);
+  in.L = reinterpret_cast<const cplx*>(L_gen);
+  in.G = reinterpret_cast<const cplx*>(G_col);
+  in.rhs = nullptr;
+  in.T_bs = T_bs;
+  in.L_bs = L_bs;
+  in.G_bs = G_bs;
+  in.rhs_bs = 0;
+  in.beta_sq = beta_sq ? beta_sq : w.nrm;
+  in.beta_bs = beta_sq ? beta_bs : 0;
+  in.rhs_is_normal = 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  long long sbs = 0;
+  TR_TRY(embed_spectra(*p, in, batch, w, st, &sbs));
+  const cplx* xv = reinterpret_cast<const cplx*>(x);
+  TR_TRY(normal_apply(*p, batch, w, sbs, xv, st));
+  // y = AX (+ |beta|^2 x): residual kernel computes r = y0 - (AX + ridge x); use y0 = 0 and negate
+  TR_CUDA_CHECK(cudaMemsetAsync(w.Y, 0, sizeof(cplx) * batch * p->n, st));
+  TR_TRY(launch_residual(w.Rv, w.AX, xv, w.Y, p->n, in.beta_sq, in.beta_bs, p->variant == TR_L2, batch, st));
+  TR_TRY(launch_accum(reinterpret_cast<cplx*>(y), p->n, w.Rv, p->n, p->n, -1.0, 1, batch, st));
+  return 0;
+}
+
+// ------------------------------------------------ nonuniform Fourier sums
+// Setup of the Gramian variant from scattered frequencies (ref
+// nufft.py:60-72, :106-114): with T[k][j] = exp(-2 pi i f_k j),
+//   Gramian first column  col[d] = sum_k w_k exp(+2 pi i f_k d)  (adjoint, sign +1, c = w)
+//   normal rhs            T^H b  = sum_k b_k exp(+2 pi i f_k j)  (adjoint, sign +1, c = b)
+//   samples               T x    = sum_j x_j exp(-2 pi i f_k j)  (forward, sign -1)
+extern "C" int tr_nudft(const double* freqs, int64_t K, int64_t n, const double* in, int32_t adjoint,
+                        int32_t sign, double* out, void* stream) {
+  if (K < 0 || n < 0 || (sign != 1 && sign != -1)) {
+    tr_set_error("tr_nudft: bad arguments (K=%lld n=%lld sign=%d)", (long long)K, (long long)n, sign);
+    return 2;
+  }
+  if (K == 0 || n == 0) return 0;
+  if (!freqs || !in || !out) { tr_set_error("tr_nudft: null pointer"); return 2; }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (adjoint)
+    return launch_nudft_adjoint(freqs, reinterpret_cast<const cplx*>(in), K, n, sign,
+                                reinterpret_cast<cplx*>(out), st);
+  return launch_nudft_forward(freqs, reinterpret_cast<const cplx*>(in), K, n, sign,
+                              reinterpret_cast<cplx*>(out), st);
 }
 
 // ---------------------------------------------------------------- stages

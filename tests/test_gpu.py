@@ -14,6 +14,7 @@ Tolerances (relative 2-norm unless stated):
 """
 
 import ctypes as C
+import glob
 import os
 
 import numpy as np
@@ -280,3 +281,114 @@ def test_stage_leaf_against_oracle(gpu, label):
     L = coeffs.shape[2]
     assert np.abs(g[:, :, :L] - coeffs).max() <= 1e-9 * np.abs(coeffs).max()
     assert rr.value < 1e-11
+
+
+CG_CASES = sorted(glob.glob(os.path.join(GOLDEN, "stages", "cg_*_n96.npz")))
+
+
+def _cg_problem(tb, path):
+    d = dict(np.load(path))
+    raw = {k: (v.item() if v.ndim == 0 else v) for k, v in d.items()}
+    raw["variant"] = str(d["variant"])
+    return wl.to_problem(raw, tb), d
+
+
+@pytest.mark.parametrize("path", CG_CASES, ids=lambda p: os.path.basename(p)[:-4])
+def test_normal_operator_matches_reference(gpu, path):
+    tb = gpu
+    prob, d = _cg_problem(tb, path)
+    op = tb.NormalOperator(prob)
+    assert rel(op.apply(d["x"]), d["ax"]) < 1e-12
+    assert op.transforms == int(d["transforms"])
+    assert rel(tb.apply_normal_operator(prob, d["x"]), d["ax"]) < 1e-12
+
+
+@pytest.mark.parametrize("path", CG_CASES, ids=lambda p: os.path.basename(p)[:-4])
+def test_cg_matches_reference(gpu, path):
+    """GPU CG against the reference's cg_solve: the same stopping rule, so the
+    iteration count agrees up to rounding (+-2) and x to the CG tolerance."""
+    tb = gpu
+    prob, d = _cg_problem(tb, path)
+    x, it = tb.cg_solve(prob)
+    assert abs(it - int(d["it_cg"])) <= 2, (it, int(d["it_cg"]))
+    assert rel(x, d["x_cg"]) < 1e-9
+    x5, it5 = tb.cg_solve(prob, tb.CGConfig(max_iterations=5))
+    assert it5 == 5
+    assert rel(x5, d["x_cg5"]) < 1e-10
+    op = tb.NormalOperator(prob)
+    _, it_op = tb.cg_solve(prob, tb.CGConfig(max_iterations=3), operator=op)
+    assert it_op == 3 and op.transforms == 3 * int(d["transforms"])
+
+
+def test_cg_edge_cases(gpu):
+    tb = gpu
+    rng = np.random.default_rng(5)
+    raw = wl.random_problem("l2", 64, rng)
+    raw["b"] = np.zeros_like(raw["b"])
+    x, it = tb.cg_solve(wl.to_problem(raw, tb))
+    assert it == 0 and not np.any(x)
+    raw = wl.random_problem("l2", 64, rng)
+    x, it = tb.cg_solve(wl.to_problem(raw, tb), tb.CGConfig(time_budget=1e-9))
+    assert it == 1  # the budget is checked after a completed iteration
+    x, it = tb.cg_solve(wl.to_problem(raw, tb), tb.CGConfig(max_iterations=0))
+    assert it == 0
+
+
+def test_cg_batch_per_system_stopping(gpu):
+    tb = gpu
+    raw = wl.c5_random(n=512, count=4, seed=3)
+    probs = [wl.to_problem(raw, tb, i) for i in range(4)]
+    out = tb.cg_solve_batch(probs)
+    for p, (x, it) in zip(probs, out):
+        xo, ito = O.cg_solve(p)
+        assert abs(it - ito) <= 2
+        assert rel(x, xo) < 1e-9
+        assert rel(x, tb.solve_tikhonov(p).x_hat) < 1e-9
+
+
+def test_cg_full_size_c5_agrees_with_direct_solve(gpu):
+    tb = gpu
+    raw = wl.c5_random(n=16384, count=1, seed=0)
+    p = wl.to_problem(raw, tb, 0)
+    x, it = tb.cg_solve(p)
+    assert 0 < it < 10 * 16384
+    assert rel(x, tb.solve_tikhonov(p).x_hat) < 1e-9
+
+
+def test_nufft_setup_matches_reference(gpu):
+    from paper_1302_6945_b200 import nufft as nf
+    g = np.load(os.path.join(GOLDEN, "stages", "nufft.npz"))
+    col = nf.weighted_fourier_gramian(g["freqs"], g["weights"], 256).gen
+    assert rel(col, g["gram"]) < 1e-12
+    big = nf.weighted_fourier_gramian(g["freqs"][:64], g["weights"][:64], 20000).gen
+    assert rel(big, g["gram_big"]) < 1e-10  # phases up to 2 pi 0.5 2e4: reference rounding ~1e-12
+    assert rel(nf.nufft_samples(g["freqs"], g["x"]), g["samples"]) < 1e-12
+    assert rel(nf.nufft_normal_rhs(g["freqs"], g["weights"] * g["samples"], 256), g["rhs"]) < 1e-12
+    # against the oracle at the c4 shape ratio (K = n / 2)
+    rng = np.random.default_rng(11)
+    f = rng.uniform(0.0, 1.0, 512)
+    b = rng.standard_normal(512) + 1j * rng.standard_normal(512)
+    assert rel(nf.nufft_normal_rhs(f, b, 1024), np.exp(2j * np.pi * np.outer(np.arange(1024), f)) @ b) < 1e-12
+    assert rel(nf.weighted_fourier_gramian(f, np.abs(b), 1024).gen, O.nufft_gramian_col(f, np.abs(b), 1024)) < 1e-12
+
+
+def test_run_nufft_matches_reference(gpu):
+    from paper_1302_6945_b200 import nufft as nf
+    g = np.load(os.path.join(GOLDEN, "stages", "nufft.npz"))
+    out = nf.run_nufft(nf.NufftConfig(n=256, samples=320))
+    assert out["weights_sum"] == float(g["run_wsum"])
+    assert out["difficult_points"] == int(g["run_dp"])
+    x = np.array(out["x_direct_re"]) + 1j * np.array(out["x_direct_im"])
+    # the regularised problem is ill-conditioned (reg_scale 1e-4): judge both
+    # solves against the exact solution of the same problem (dense oracle)
+    rng = np.random.default_rng(np.random.SeedSequence((0, 93)))
+    f = rng.triangular(-0.5, 0.0, 0.5, size=320)
+    w = nf.voronoi_weights(f)
+    xt = nf.make_signal(256, 3, 0.02, rng)
+    _, rhs = O.nufft_samples_and_rhs(f, w, xt)
+    prob = gpu.ProblemSpec.gramian(gpu.HermitianToeplitzSpec(256, O.nufft_gramian_col(f, w, 256)),
+                                   nf.second_difference_regularizer(256, 1e-4), rhs)
+    exact = O.dense_solution(prob)
+    assert rel(x, exact) <= rel(g["run_x"], exact) * 1.01 + 1e-12
+    assert out["rel_err_direct"] <= float(g["run_err"]) * 1.01
+    assert out["cg_iterations"] >= 1 and out["rel_residual_direct"] < 1e-6

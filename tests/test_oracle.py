@@ -2,6 +2,7 @@
 by tests/golden/make_golden.py from /root/reference), the reference tests'
 known answers, and the extension-size hand traces."""
 
+import glob
 import os
 
 import numpy as np
@@ -121,3 +122,45 @@ def test_oracle_matches_dense_and_cg_exact():
     assert rel(x, d["x_exact"]) < 1e-12
     xc = O.cg_exact(p, tol=1e-14)
     assert rel(xc, x) < 1e-11
+
+
+CG_CASES = sorted(glob.glob(os.path.join(GOLDEN, "stages", "cg_*_n96.npz")))
+
+
+def _cg_problem(path, mod):
+    from paper_1302_6945_b200 import workloads as wl
+    d = dict(np.load(path))
+    raw = {k: (v.item() if v.ndim == 0 else v) for k, v in d.items()}
+    raw["variant"] = str(d["variant"])
+    return wl.to_problem(raw, mod), d
+
+
+@pytest.mark.parametrize("path", CG_CASES, ids=lambda p: os.path.basename(p)[:-4])
+def test_oracle_normal_operator_and_cg_match_reference(path):
+    """Oracle NormalOperator.apply and cg_solve against the reference's own
+    outputs (tests/golden/make_golden_cg.py): same iteration counts."""
+    import paper_1302_6945_b200 as tb
+    prob, d = _cg_problem(path, tb)
+    assert rel(O.normal_apply(prob, d["x"]), d["ax"]) < 1e-13
+    x, it = O.cg_solve(prob)
+    assert it == int(d["it_cg"])
+    assert rel(x, d["x_cg"]) < 1e-12
+    x5, it5 = O.cg_solve(prob, max_iterations=5)
+    assert it5 == int(d["it_cg5"]) == 5
+    assert rel(x5, d["x_cg5"]) < 1e-12
+
+
+def test_oracle_nufft_setup_matches_reference():
+    """Gramian column, samples and rhs of the NUFFT setup against the
+    reference (tests/golden/make_golden_nufft.py); host helpers identical."""
+    from paper_1302_6945_b200 import nufft as nf
+    g = np.load(os.path.join(GOLDEN, "stages", "nufft.npz"))
+    assert rel(O.nufft_gramian_col(g["freqs"], g["weights"], 256), g["gram"]) < 1e-14
+    s, r = O.nufft_samples_and_rhs(g["freqs"], g["weights"], g["x"])
+    assert rel(s, g["samples"]) < 1e-14 and rel(r, g["rhs"]) < 1e-14
+    assert np.array_equal(nf.voronoi_weights(g["freqs"]), g["weights"])
+    rng = np.random.default_rng(np.random.SeedSequence((7, 93)))
+    rng.triangular(-0.5, 0.0, 0.5, size=300)
+    assert np.array_equal(nf.make_signal(256, 3, 0.02, rng), g["x"])
+    reg = nf.second_difference_regularizer(5, 2.0)
+    assert reg.gen[4] == 4.0 and reg.gen[3] == -2.0 and reg.gen[5] == -2.0
