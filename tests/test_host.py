@@ -60,3 +60,22 @@ def test_reference_problem_objects_are_accepted_by_shape_logic():
     raw = wl.random_problem("general", 8, np.random.default_rng(1))
     rp = wl.to_problem(raw, ref)
     assert tb.solver._shape(rp) == ("general", 8, 8, 8)
+
+
+def test_json_formats_roundtrip_like_the_reference():
+    """Interchange formats of ref toeplitz.py:236-263 (README:68-72)."""
+    import json
+    import sys
+    import numpy as np
+    import paper_1302_6945_b200 as tb
+    g = np.array([1 + 2j, 3.5, -1j, 0.25, 7.0])
+    spec = tb.ToeplitzSpec(3, 3, g)
+    obj = json.loads(json.dumps(tb.spec_to_json(spec)))
+    assert obj["rows"] == 3 and obj["cols"] == 3 and obj["gen_re"][0] == 1.0
+    back = tb.spec_from_json(json.dumps(obj))
+    assert np.array_equal(back.gen, spec.gen)
+    assert np.array_equal(tb.spec_from_json({"rows": 1, "cols": 2, "gen_re": [1.0, 2.0]}).gen,
+                          np.array([1.0, 2.0], dtype=np.complex128))
+    v = np.array([1.0 - 1j, 2.0, 1e-300j])
+    assert np.array_equal(tb.vector_from_json(json.dumps(tb.vector_to_json(v))), v)
+    assert np.array_equal(tb.vector_from_json({"re": [1.0, 2.0]}), np.array([1.0, 2.0], dtype=complex))
