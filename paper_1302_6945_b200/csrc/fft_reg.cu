@@ -117,7 +117,7 @@ TR_D void run_stage(cplx* sm, const FastArgs& a, long long lin, long long lout, 
 // CTA = TL lines x T threads (TL chosen at launch so small batches still
 // spread over the SMs)
 template <int LOG2, int Q>
-__global__ void __launch_bounds__(NTH) fft_reg_kernel(FastArgs a, int TL) {
+__global__ void __launch_bounds__(NTH, 3) fft_reg_kernel(FastArgs a, int TL) {
   using G = Plan<LOG2, Q>;
   extern __shared__ __align__(16) unsigned char fsm[];
   const int sl = threadIdx.x / G::T, tb = threadIdx.x % G::T;

@@ -1,6 +1,7 @@
 timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-python tools/ab_check.py c2 64 /tmp/a2.npz; TR_GROUPS=1 python tools/ab_check.py c2 64 /tmp/b2.npz; python tools/ab_check.py --cmp /tmp/a2.npz /tmp/b2.npz
-for v in 1 2 3 4; do
-  TR_GROUPS=$v python bench.py --steps 10 --no-cpu-baseline | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print('G=$v', d['config']['config'], 'solves/s %.1f'%d['value'], 'e2e %.1f'%d['e2e']['value'])"
+for v in "TR_TRIM=new" "TR_TRIM=old"; do
+ for c in "" "--config c5 --batch 256"; do
+  env $v python bench.py --steps 5 --no-cpu-baseline $c | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$v', d['config']['config'], 'solves/s %.1f'%d['value'], {k:round(v['ms_per_step'],2) for k,v in d['kernels'].items()})"
+ done
 done
