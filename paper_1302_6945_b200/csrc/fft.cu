@@ -510,36 +510,59 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
   tr_kernel_work(TRK_FFT, 16.0 * lines * (double)(in_len + n),
                  5.0 * lines * (double)n * std::log2((double)n));
   if (p.col) {
+    // Lines go through both passes in chunks whose intermediate fits in L2
+    // (the same scratch region for every chunk): pass B reads pass A's output
+    // from L2, and the dirty scratch lines are overwritten by the next chunk
+    // instead of being written back, so HBM sees one read and one write per
+    // transform.  TR_FFT_L2MB sets the chunk size (0: one chunk).
+    static const long long chunk_bytes = [] {
+      const char* e = getenv("TR_FFT_L2MB");
+      return (long long)(e ? atof(e) : 16.0) * (1LL << 20);
+    }();
+    long long cl = lines;
+    if (chunk_bytes > 0) {
+      cl = chunk_bytes / (n * (long long)sizeof(cplx));
+      if (cl < 1) cl = 1;
+      if (cl > lines) cl = lines;
+    }
     const long long N1 = 1LL << p.a1, N2 = (long long)p.q2 << p.a2;
-    ColArgs c;
-    c.in = in;
-    c.in_ls = in_ls;
-    c.in_len = in_len;
-    c.in_es = (int)N2;
-    c.out = scratch;
-    c.out_ls = n;
-    c.out_es = 1;
-    c.subs = (int)N2;
-    c.lines = lines;
-    c.twR = p.tw1;
-    c.twN = p.twN;
-    c.tw2 = p.twc;
-    c.sign = sign;
-    int rc = col_launch(true, p.a1, 1, c, st);
-    if (rc == 0) {
+    for (long long s0 = 0; s0 < lines; s0 += cl) {
+      const long long nl = std::min(cl, lines - s0);
+      ColArgs c;
+      c.in = in + s0 * in_ls;
+      c.in_ls = in_ls;
+      c.in_len = in_len;
+      c.in_es = (int)N2;
+      c.out = scratch;
+      c.out_ls = n;
+      c.out_es = 1;
+      c.subs = (int)N2;
+      c.lines = nl;
+      c.twR = p.tw1;
+      c.twN = p.twN;
+      c.tw2 = p.twc;
+      c.sign = sign;
+      int rc = col_launch(true, p.a1, 1, c, st);
+      if (rc) {
+        if (s0 == 0) break;  // no column kernel: the pass plan below
+        tr_set_error("fft column plan has no kernel for n=%lld", n);
+        return 2;
+      }
       c.in = scratch;
       c.in_ls = n;
       c.in_len = n;
       c.in_es = (int)N1;
-      c.out = out;
+      c.out = out + s0 * out_ls;
       c.out_ls = out_ls;
       c.out_es = (int)N1;
       c.subs = (int)N1;
       c.twR = p.tw2;
       rc = col_launch(false, p.a2, p.q2, c, st);
       if (rc) { tr_set_error("fft column plan has no kernel for n=%lld", n); return 2; }
-      TR_CUDA_CHECK(cudaGetLastError());
-      return 0;
+      if (s0 + nl >= lines) {
+        TR_CUDA_CHECK(cudaGetLastError());
+        return 0;
+      }
     }
   }
   if (p.npass == 1) {

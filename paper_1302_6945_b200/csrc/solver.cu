@@ -715,6 +715,23 @@ int normal_apply(const Plan& p, long long nsys, const WS& w, long long sbs, cons
   return 0;
 }
 
+// Systems per chunk for a tree op whose per-system intermediate is `elems`
+// complex values: the whole batch when the intermediates of all systems are
+// small or the batch is small (launch-latency bound), else chunks of about
+// TR_TREE_L2MB so they stay in L2 between the op's kernels (default 0 = off:
+// measured slower, the narrower launches cost more than the L2 reuse gains).
+long long l2_chunk(long long nsys, long long elems) {
+  static const long long budget = [] {
+    const char* e = getenv("TR_TREE_L2MB");
+    return (long long)((e ? atof(e) : 0.0) * (1 << 20));
+  }();
+  const long long per = elems * (long long)sizeof(cplx);
+  if (budget <= 0 || nsys * per <= 2 * budget) return nsys;
+  long long cs = budget / per;
+  if (cs < 8) cs = 8;  // keep each launch wide enough for the GPU
+  return cs < nsys ? cs : nsys;
+}
+
 // Stages 1-4 for normal right-hand sides Y -> solution X
 int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, const cplx* Y,
                cplx* X, cudaStream_t st) {
@@ -846,33 +863,44 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
     } else if (op.kind == OP_UPDATE) {
       long long cnt = N / op.stride;
       long long scap = p.slot_cap[op.slot_a];
-      TR_TRY(launch_twist_fold(w.S1, w.slot[op.slot_a], PP * scap, scap, PP, op.cap_a, op.o0, op.o1,
-                               op.noff, cnt, N, twN, nsys, st));
-      TR_TRY(fft_exec(F(p, cnt), w.S1, cnt, cnt, w.S1, cnt, w.S2, nsys * op.noff * PP, +1, st));
-      TR_TRY(launch_apply_update(w.W, w_sys, w.S1, rows, P, op.o0, op.o1, op.noff, op.stride, cnt,
-                                 nsys, st));
+      // systems in chunks whose folded values stay in L2 between the three kernels
+      const long long cs = l2_chunk(nsys, (long long)op.noff * PP * cnt * 2);
+      for (long long s0 = 0; s0 < nsys; s0 += cs) {
+        const long long ns = std::min(cs, nsys - s0);
+        TR_TRY(launch_twist_fold(w.S1, w.slot[op.slot_a] + s0 * PP * scap, PP * scap, scap, PP, op.cap_a,
+                                 op.o0, op.o1, op.noff, cnt, N, twN, ns, st));
+        TR_TRY(fft_exec(F(p, cnt), w.S1, cnt, cnt, w.S1, cnt, w.S2, ns * op.noff * PP, +1, st));
+        TR_TRY(launch_apply_update(w.W + s0 * w_sys, w_sys, w.S1, rows, P, op.o0, op.o1, op.noff, op.stride,
+                                   cnt, ns, st));
+      }
     } else {
       long long R = op.R;
       long long ca = p.slot_cap[op.slot_a], cb = p.slot_cap[op.slot_b];
       const FftPlan& fp = F(p, R);
-      TR_TRY(fft_exec(fp, w.slot[op.slot_a], ca, op.cap_a, w.S1, R, w.S3, nsys * PP, -1, st));
-      TR_TRY(fft_exec(fp, w.slot[op.slot_b], cb, op.cap_b, w.S2, R, w.S3, nsys * PP, -1, st));
-      TR_TRY(launch_pointwise_matmul(w.S1, w.S2, P, R, nsys, st));
-      TR_TRY(fft_exec(fp, w.S1, R, R, w.S1, R, w.S3, nsys * PP, +1, st));
-      TrimArgs ta;
-      ta.F = w.S1;
-      ta.R = R;
-      ta.L = op.cap_a + op.cap_b - 1;
-      ta.P = P;
-      ta.prof = w.prof;
-      ta.red = w.red;
-      ta.out = w.slot[op.slot_out];
-      ta.cap = p.slot_cap[op.slot_out];
-      ta.out_sys = (long long)PP * ta.cap;
-      ta.cap_node = op.cap_out;
-      ta.max_scale = w.max_scale;
-      ta.trim_over = w.trim_over;
-      TR_TRY(launch_trim_normalize(ta, nsys, st));
+      // systems in chunks whose two spectra stay in L2 from the forward
+      // transforms through the product, the inverse transform and the trim
+      const long long cs = l2_chunk(nsys, 2LL * PP * R);
+      for (long long s0 = 0; s0 < nsys; s0 += cs) {
+        const long long ns = std::min(cs, nsys - s0);
+        TR_TRY(fft_exec(fp, w.slot[op.slot_a] + s0 * PP * ca, ca, op.cap_a, w.S1, R, w.S3, ns * PP, -1, st));
+        TR_TRY(fft_exec(fp, w.slot[op.slot_b] + s0 * PP * cb, cb, op.cap_b, w.S2, R, w.S3, ns * PP, -1, st));
+        TR_TRY(launch_pointwise_matmul(w.S1, w.S2, P, R, ns, st));
+        TR_TRY(fft_exec(fp, w.S1, R, R, w.S1, R, w.S3, ns * PP, +1, st));
+        TrimArgs ta;
+        ta.F = w.S1;
+        ta.R = R;
+        ta.L = op.cap_a + op.cap_b - 1;
+        ta.P = P;
+        ta.prof = w.prof;
+        ta.red = w.red;
+        ta.cap = p.slot_cap[op.slot_out];
+        ta.out_sys = (long long)PP * ta.cap;
+        ta.out = w.slot[op.slot_out] + s0 * ta.out_sys;
+        ta.cap_node = op.cap_out;
+        ta.max_scale = w.max_scale + s0;
+        ta.trim_over = w.trim_over + s0;
+        TR_TRY(launch_trim_normalize(ta, ns, st));
+      }
     }
   }
 
