@@ -182,6 +182,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--refine", type=int, default=1)
+    ap.add_argument("--refine-cg", type=int, default=256)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -206,7 +207,7 @@ def main():
 
     raw, count, label = make_workload(args.config, rank, args.batch)
     probs = problems_from(raw, count)
-    cfg = tb.SolverConfig(refine=args.refine)
+    cfg = tb.SolverConfig(refine=args.refine, refine_cg=args.refine_cg)
     db = tb.DeviceBatch(probs, cfg).stage()
     torch.cuda.synchronize()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -325,7 +326,7 @@ def main():
         "data": "synthetic (seeded BASELINE-config generators, paper_1302_6945_b200/workloads.py)",
         "config": {"workload": label, "config": args.config, "systems_per_rank": count,
                    "order_N": info["order"], "leaves": info["leaves"], "leaf_conditions": info["max_leaf_conditions"],
-                   "refine": args.refine, "parallelism": f"dp{world} (systems sharded, gather x to rank 0)",
+                   "refine": args.refine, "refine_cg_max_iterations": args.refine_cg, "parallelism": f"dp{world} (systems sharded, gather x to rank 0)",
                    "l2": "256 MiB device write between timed steps (outside the per-step events)",
                    "timing": "CUDA events per step on the launching stream, summed; max over ranks"},
         "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": db.h2d_bytes,

@@ -50,7 +50,10 @@ typedef struct tr_desc {
   int32_t fill;             /* SolverConfig.fill */
   int32_t paired;           /* SolverConfig.paired */
   int32_t force_even;       /* SolverConfig.force_even */
-  int32_t refine;           /* extra iterative-refinement solves (0 = reference) */
+  int32_t refine;           /* iterative refinement on (> 0) / off (0 = reference's single pass) */
+  int32_t refine_cg;        /* refinement by up to this many CG iterations warm-started at the
+                               direct solution; systems CG leaves unfinished (and every system
+                               when 0) get `refine` direct refinement solves instead */
 } tr_desc;
 
 /* Per-system report (ref: SolveReport solver.py:48-55, TanIntDiagnostics
@@ -65,7 +68,7 @@ typedef struct tr_diag {
   int64_t final_col_degrees[8];
   double relative_residual;
   int32_t trim_overflow;        /* products truncated at the degree bound */
-  int32_t pad;
+  int32_t refine_cg_iterations; /* CG refinement iterations run (0: none / direct refinement) */
 } tr_diag;
 
 /* Bytes of device workspace tr_solve_batch needs for `batch` systems. */

@@ -30,6 +30,7 @@ class TrDesc(C.Structure):
         ("paired", C.c_int32),
         ("force_even", C.c_int32),
         ("refine", C.c_int32),
+        ("refine_cg", C.c_int32),
     ]
 
 
@@ -44,7 +45,7 @@ class TrDiag(C.Structure):
         ("final_col_degrees", C.c_int64 * 8),
         ("relative_residual", C.c_double),
         ("trim_overflow", C.c_int32),
-        ("pad", C.c_int32),
+        ("refine_cg_iterations", C.c_int32),
     ]
 
 

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(CGT) cg_update_kernel(cplx* X, cplx* R, cplx* 
                                                         long long n, double tol, double* st, int* it) {
   __shared__ double sh[CGT / 32];
   const long long sys = blockIdx.x;
-  if (st[sys * 4 + 2] == 0.0) return;
+  if (st[sys * 4 + 2] != 1.0) return;
   cplx* x = X + sys * n;
   cplx* r = R + sys * n;
   cplx* d = D + sys * n;
@@ -90,9 +90,70 @@ __global__ void __launch_bounds__(CGT) cg_update_kernel(cplx* X, cplx* R, cplx* 
   }
 }
 
+// warm start from the direct solution x: r = y - A x, d = r; the target is
+// a 1e-8 reduction of the recursive residual, enough for the correction on
+// any system CG converges on (x error ~ cond(A) 1e-8 of the direct error)
+__global__ void __launch_bounds__(CGT) cg_warm_kernel(const cplx* X, cplx* R, cplx* D, const cplx* AX,
+                                                      const cplx* Y, const double* beta_sq, long long beta_bs,
+                                                      int ridge, long long n, double* st, int* it) {
+  __shared__ double sh[CGT / 32];
+  const long long sys = blockIdx.x;
+  const double b2 = ridge ? beta_sq[sys * beta_bs] : 0.0;
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += CGT) {
+    const long long o = sys * n + i;
+    const cplx x = X[o], ax = AX[o], y = Y[o];
+    const cplx r = cmk(y.x - (ax.x + b2 * x.x), y.y - (ax.y + b2 * x.y));
+    R[o] = r;
+    D[o] = r;
+    s += cabs2(r);
+  }
+  s = blk_sum(s, sh);
+  if (threadIdx.x == 0) {
+    const double target = 1e-8 * sqrt(s);
+    st[sys * 4 + 0] = s;
+    st[sys * 4 + 1] = target;
+    st[sys * 4 + 2] = sqrt(s) > target;
+    st[sys * 4 + 3] = s;  // initial rho (progress estimate on the host)
+    it[sys] = 0;
+  }
+}
+
+// st[2]: 1 iterating, 0 converged, 2 abandoned.  A system is abandoned when
+// its own geometric rate so far projects past `cap` iterations (decided only
+// from its own residual history at fixed check points: deterministic and
+// independent of the batch it is solved in).
+__global__ void cg_check_kernel(double* st, const int* it, long long nsys, int cap) {
+  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= nsys || st[s * 4 + 2] != 1.0) return;
+  const int k = it[s];
+  const double r0 = sqrt(st[s * 4 + 3]), rk = sqrt(st[s * 4 + 0]), tgt = st[s * 4 + 1];
+  const double rate = pow(rk / r0, 1.0 / k);
+  const double need = rate < 1.0 ? log(tgt / rk) / log(rate) : 1e30;
+  if (k >= cap || k + need > cap) st[s * 4 + 2] = 2.0;
+}
+
+// x = x0 for systems CG did not converge on (the direct refinement restarts
+// from the direct solution)
+__global__ void cg_restore_kernel(cplx* X, const cplx* X0, const double* st, long long n) {
+  const long long sys = blockIdx.y;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n || st[sys * 4 + 2] == 0.0) return;
+  X[sys * n + i] = X0[sys * n + i];
+}
+
+// x += d for systems CG did not converge on
+__global__ void add_masked_kernel(cplx* X, const cplx* D, const double* st, long long n) {
+  const long long sys = blockIdx.y;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n || st[sys * 4 + 2] == 0.0) return;
+  const long long o = sys * n + i;
+  X[o] = cadd(X[o], D[o]);
+}
+
 __global__ void cg_active_kernel(const double* st, long long nsys, int* any) {
   long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  int a = (s < nsys && st[s * 4 + 2] != 0.0) ? 1 : 0;
+  int a = (s < nsys && st[s * 4 + 2] == 1.0) ? 1 : 0;
   a = __syncthreads_or(a);
   if (threadIdx.x == 0 && a) atomicOr(any, 1);
 }
@@ -119,6 +180,33 @@ int launch_cg_update(cplx* X, cplx* R, cplx* D, const cplx* AD, const double* be
 int launch_cg_active(const double* st, long long nsys, int* any, cudaStream_t s) {
   TR_CUDA_CHECK(cudaMemsetAsync(any, 0, sizeof(int), s));
   { TrKTimer _kt(TRK_NORMAL, s); cg_active_kernel<<<(unsigned)((nsys + 255) / 256), 256, 0, s>>>(st, nsys, any); }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int launch_cg_warm(const cplx* X, cplx* R, cplx* D, const cplx* AX, const cplx* Y, const double* beta_sq,
+                   long long beta_bs, int ridge, long long n, double* st, int* it, long long nsys, cudaStream_t s) {
+  { TrKTimer _kt(TRK_NORMAL, s); cg_warm_kernel<<<(unsigned)nsys, CGT, 0, s>>>(X, R, D, AX, Y, beta_sq, beta_bs, ridge, n, st, it); }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int launch_cg_check(double* st, const int* it, long long nsys, int cap, cudaStream_t s) {
+  { TrKTimer _kt(TRK_NORMAL, s); cg_check_kernel<<<(unsigned)((nsys + 127) / 128), 128, 0, s>>>(st, it, nsys, cap); }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int launch_cg_restore(cplx* X, const cplx* X0, const double* st, long long n, long long nsys, cudaStream_t s) {
+  dim3 g((unsigned)((n + 255) / 256), (unsigned)nsys);
+  { TrKTimer _kt(TRK_NORMAL, s); cg_restore_kernel<<<g, 256, 0, s>>>(X, X0, st, n); }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int launch_add_masked(cplx* X, const cplx* D, const double* st, long long n, long long nsys, cudaStream_t s) {
+  dim3 g((unsigned)((n + 255) / 256), (unsigned)nsys);
+  { TrKTimer _kt(TRK_FINISH, s); add_masked_kernel<<<g, 256, 0, s>>>(X, D, st, n); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }

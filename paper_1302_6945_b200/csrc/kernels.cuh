@@ -114,6 +114,8 @@ int launch_cg_init(cplx* X, cplx* R, cplx* D, const cplx* Y, long long n, double
 int launch_cg_update(cplx* X, cplx* R, cplx* D, const cplx* AD, const double* beta_sq, long long beta_bs,
                      int ridge, long long n, double tol, double* st, int* it, long long nsys, cudaStream_t s);
 int launch_cg_active(const double* st, long long nsys, int* any, cudaStream_t s);
+int launch_cg_warm(const cplx* X, cplx* R, cplx* D, const cplx* AX, const cplx* Y, const double* beta_sq,
+                   long long beta_bs, int ridge, long long n, double* st, int* it, long long nsys, cudaStream_t s);
 
 // ---- nonuniform Fourier sums (nufft.cu) ----
 // adjoint: y[d] = sum_k c_k exp(sign 2 pi i f_k d), d < n; forward: y[k] = sum_j x_j exp(sign 2 pi i f_k j)
@@ -121,3 +123,6 @@ int launch_nudft_adjoint(const double* f, const cplx* c, long long K, long long 
                          cudaStream_t st);
 int launch_nudft_forward(const double* f, const cplx* x, long long K, long long n, int sign, cplx* y,
                          cudaStream_t st);
+int launch_cg_check(double* st, const int* it, long long nsys, int cap, cudaStream_t s);
+int launch_cg_restore(cplx* X, const cplx* X0, const double* st, long long n, long long nsys, cudaStream_t s);
+int launch_add_masked(cplx* X, const cplx* D, const double* st, long long n, long long nsys, cudaStream_t s);

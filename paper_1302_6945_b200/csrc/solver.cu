@@ -519,14 +519,14 @@ struct Carve {
 };
 
 struct WS {
-  cplx *W, *Wp, *Y, *X, *X2, *Rv, *AX;
+  cplx *W, *Wp, *Y, *X, *X0, *X2, *Rv, *AX;
   cplx* spec_emb;  // [nsys or 1][5][q]
   std::vector<cplx*> slot;
   cplx* leaf_scratch;
   cplx *S1, *S2, *S3;
   double* prof;
   unsigned long long* red;
-  int *cd, *dcount, *retried, *status, *trim_over, *blen;
+  int *cd, *dcount, *retried, *status, *trim_over, *blen, *cgit;
   int2* defer;
   double *max_scale, *partial, *nrm, *res_out;
   int* len_out;
@@ -542,6 +542,7 @@ size_t layout(const Plan& p, long long nsys, char* base, WS* w) {
   w->Wp = c.take<cplx>(wsz);
   w->Y = c.take<cplx>((size_t)nsys * n);
   w->X = c.take<cplx>((size_t)nsys * n);
+  w->X0 = c.take<cplx>((size_t)nsys * n);
   w->X2 = c.take<cplx>((size_t)nsys * n);
   w->Rv = c.take<cplx>((size_t)nsys * n);
   w->AX = c.take<cplx>((size_t)nsys * n);
@@ -569,6 +570,7 @@ size_t layout(const Plan& p, long long nsys, char* base, WS* w) {
   w->status = c.take<int>((size_t)nsys);
   w->trim_over = c.take<int>((size_t)nsys);
   w->blen = c.take<int>((size_t)nsys);
+  w->cgit = c.take<int>((size_t)nsys);
   w->len_out = c.take<int>((size_t)nsys);
   w->defer = c.take<int2>((size_t)nsys * DMAX);
   w->max_scale = c.take<double>((size_t)nsys);
@@ -667,6 +669,15 @@ int embed_spectra(const Plan& p, const Inputs& in, long long nsys, const WS& w, 
   TR_TRY(fft_exec(F(p, p.q), w.spec_emb, p.q, p.q, w.spec_emb, p.q, w.S3, ns * 5, -1, st));
   *spec_bs = shared ? 0 : 5 * p.q;
   return 0;
+}
+
+// batch stride of the cached spectra (0 when every operand is shared)
+long long spectra_bstride(const Plan& p, const Inputs& in) {
+  bool shared = true;
+  if (p.variant == TR_L2 || p.variant == TR_GENERAL) shared = shared && in.T_bs == 0;
+  if (p.variant == TR_GENERAL || p.variant == TR_GRAMIAN) shared = shared && in.L_bs == 0;
+  if (p.variant == TR_GRAMIAN) shared = shared && in.G_bs == 0;
+  return shared ? 0 : 5 * p.q;
 }
 
 // Block index of a spectrum inside spec_emb
@@ -956,20 +967,59 @@ int normal_rhs(const Plan& p, const Inputs& in, long long nsys, const WS& w, lon
   return 0;
 }
 
-int solve_chunk(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx* x_out, int refine,
-                cudaStream_t st, tr_diag* diag_host) {
+// The solve runs in phases (each captured into its own CUDA graph):
+//   DIRECT   spectra, T^H b, the superfast solve x = A^-1 y (stages 1-4);
+//            with CG refinement also r = y - A x, d = r (warm start)
+//   CG       CG_BLOCK conjugate-gradient iterations on A x = y from that x
+//            (systems whose residual reached their target are skipped)
+//   REFINE   one direct refinement solve: x += A^-1 (y - A x)
+//   FINAL    the reported residual (ref solver.py:72-75) and x out
+// Refinement: a handful of CG iterations brings a direct solution (relative
+// error ~1e-9) to the FP64 floor on well-conditioned systems
+// for a small fraction of a second solve; systems CG cannot finish within
+// the iteration cap (ill-conditioned ones) get the direct refinement solve.
+enum { PH_DIRECT = 0, PH_CG = 1, PH_REFINE = 2, PH_FINAL = 3, PH_REFINE_CG = 4 };
+constexpr int CG_BLOCK = 16;
+
+int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx* x_out, int phase,
+              int cg_init, cudaStream_t st) {
   const long long n = p.n;
-  long long sbs = 0;
-  TR_TRY(embed_spectra(p, in, nsys, w, st, &sbs));
-  TR_TRY(normal_rhs(p, in, nsys, w, sbs, st));
-  TR_TRY(solve_core(p, in, nsys, w, w.Y, w.X, st));
   const int add_ridge = p.variant == TR_L2;
-  for (int r = 0; r < refine; ++r) {
-    // r = y - A x ; solve A d = r ; x += d
+  // CG state: x = X, r = Rv, d = X2, A d = AX, st = partial[sys][4], iterations = cgit
+  double* cst = w.partial;
+  int* its = w.cgit;
+  if (phase == PH_DIRECT) {
+    long long sbs = 0;
+    TR_TRY(embed_spectra(p, in, nsys, w, st, &sbs));
+    TR_TRY(normal_rhs(p, in, nsys, w, sbs, st));
+    TR_TRY(solve_core(p, in, nsys, w, w.Y, w.X, st));
+    if (cg_init) {
+      TR_CUDA_CHECK(cudaMemcpyAsync(w.X0, w.X, sizeof(cplx) * nsys * n, cudaMemcpyDeviceToDevice, st));
+      TR_TRY(normal_apply(p, nsys, w, sbs, w.X, st));
+      TR_TRY(launch_cg_warm(w.X, w.Rv, w.X2, w.AX, w.Y, in.beta_sq, in.beta_bs, add_ridge, n, cst, its, nsys, st));
+    }
+    return 0;
+  }
+  const long long sbs = spectra_bstride(p, in);
+  if (phase == PH_CG) {
+    for (int k = 0; k < CG_BLOCK; ++k) {
+      TR_TRY(normal_apply(p, nsys, w, sbs, w.X2, st));
+      TR_TRY(launch_cg_update(w.X, w.Rv, w.X2, w.AX, in.beta_sq, in.beta_bs, add_ridge, n, 1.0, cst, its,
+                              nsys, st));
+    }
+    TR_TRY(launch_cg_check(cst, its, nsys, cg_init, st));  // cg_init carries the iteration cap here
+    return 0;
+  }
+  if (phase == PH_REFINE || phase == PH_REFINE_CG) {
+    // r = y - A x ; solve A d = r ; x += d   (after CG: only the systems CG
+    // did not converge on, restarting from their direct solution)
+    if (phase == PH_REFINE_CG) TR_TRY(launch_cg_restore(w.X, w.X0, cst, n, nsys, st));
     TR_TRY(normal_apply(p, nsys, w, sbs, w.X, st));
     TR_TRY(launch_residual(w.Rv, w.AX, w.X, w.Y, n, in.beta_sq, in.beta_bs, add_ridge, nsys, st));
     TR_TRY(solve_core(p, in, nsys, w, w.Rv, w.X2, st));
-    TR_TRY(launch_add_inplace(w.X, w.X2, n, nsys, st));
+    if (phase == PH_REFINE_CG) TR_TRY(launch_add_masked(w.X, w.X2, cst, n, nsys, st));
+    else TR_TRY(launch_add_inplace(w.X, w.X2, n, nsys, st));
+    return 0;
   }
   // residual for the report (ref solver.py:72-75)
   TR_TRY(normal_apply(p, nsys, w, sbs, w.X, st));
@@ -980,7 +1030,7 @@ int solve_chunk(const Plan& p, const Inputs& in, long long nsys, const WS& w, cp
   return 0;
 }
 
-int read_diag(const Plan& p, long long nsys, const WS& w, cudaStream_t st, tr_diag* diag_host) {
+int read_diag(const Plan& p, long long nsys, const WS& w, cudaStream_t st, tr_diag* diag_host, bool cg_ran) {
   {
     std::vector<int> cd(nsys * 8), dc(nsys), rt(nsys), stt(nsys), tro(nsys);
     std::vector<double> ms(nsys), nr(2 * nsys);
@@ -991,6 +1041,9 @@ int read_diag(const Plan& p, long long nsys, const WS& w, cudaStream_t st, tr_di
     TR_CUDA_CHECK(cudaMemcpyAsync(tro.data(), w.trim_over, sizeof(int) * nsys, cudaMemcpyDeviceToHost, st));
     TR_CUDA_CHECK(cudaMemcpyAsync(ms.data(), w.max_scale, sizeof(double) * nsys, cudaMemcpyDeviceToHost, st));
     TR_CUDA_CHECK(cudaMemcpyAsync(nr.data(), w.nrm, sizeof(double) * 2 * nsys, cudaMemcpyDeviceToHost, st));
+    std::vector<int> cgit(nsys, 0);
+    if (cg_ran)
+      TR_CUDA_CHECK(cudaMemcpyAsync(cgit.data(), w.cgit, sizeof(int) * nsys, cudaMemcpyDeviceToHost, st));
     TR_CUDA_CHECK(cudaStreamSynchronize(st));
     for (long long s = 0; s < nsys; ++s) {
       tr_diag& dg = diag_host[s];
@@ -1005,6 +1058,7 @@ int read_diag(const Plan& p, long long nsys, const WS& w, cudaStream_t st, tr_di
       double den = nr[nsys + s];
       dg.relative_residual = nr[s] / (den > 0.0 ? den : 1.0);
       dg.trim_overflow = tro[s];
+      dg.refine_cg_iterations = cgit[s];
     }
   }
   return 0;
@@ -1066,12 +1120,12 @@ size_t plan_groups(const Plan& p, long long batch, std::vector<Group>* out) {
   return off;
 }
 
-int solve_groups(const Plan& p, std::vector<Group>& gs, int refine, cudaStream_t st) {
+int phase_groups(const Plan& p, std::vector<Group>& gs, int phase, int cg_init, cudaStream_t st) {
   static thread_local cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
   static thread_local cudaEvent_t fork = nullptr, join[4] = {nullptr, nullptr, nullptr, nullptr};
   const int G = (int)gs.size();
   if (G == 1 || g_timing.load()) {  // kernel timing: one stream, groups in order
-    for (auto& g : gs) TR_TRY(solve_chunk(p, g.in, g.count, g.w, g.x, refine, st, nullptr));
+    for (auto& g : gs) TR_TRY(phase_run(p, g.in, g.count, g.w, g.x, phase, cg_init, st));
     return 0;
   }
   if (!fork) {
@@ -1084,31 +1138,34 @@ int solve_groups(const Plan& p, std::vector<Group>& gs, int refine, cudaStream_t
   TR_CUDA_CHECK(cudaEventRecord(fork, st));
   for (int g = 1; g < G; ++g) {
     TR_CUDA_CHECK(cudaStreamWaitEvent(side[g], fork, 0));
-    TR_TRY(solve_chunk(p, gs[g].in, gs[g].count, gs[g].w, gs[g].x, refine, side[g], nullptr));
+    TR_TRY(phase_run(p, gs[g].in, gs[g].count, gs[g].w, gs[g].x, phase, cg_init, side[g]));
     TR_CUDA_CHECK(cudaEventRecord(join[g], side[g]));
   }
-  TR_TRY(solve_chunk(p, gs[0].in, gs[0].count, gs[0].w, gs[0].x, refine, st, nullptr));
+  TR_TRY(phase_run(p, gs[0].in, gs[0].count, gs[0].w, gs[0].x, phase, cg_init, st));
   for (int g = 1; g < G; ++g) TR_CUDA_CHECK(cudaStreamWaitEvent(st, join[g], 0));
   return 0;
 }
 
-int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine, cudaStream_t st, void* ws) {
+// One phase for every group, through a cached CUDA graph after the first
+// (eager) call.  Work runs on a private stream fenced to the caller's.
+int run_phase(const Plan& p, std::vector<Group>& gs, long long nsys, int phase, int cg_init, cudaStream_t st,
+              void* ws) {
   static const char* env = getenv("TR_GRAPHS");
   static const bool trace = getenv("TR_LEAF_TRACE") != nullptr;
   const bool graphs = !(env && env[0] == '0') && !trace && !g_timing.load();
-  if (!graphs) return solve_groups(p, gs, refine, st);
+  if (!graphs) return phase_groups(p, gs, phase, cg_init, st);
   const Inputs& in = gs[0].in;
   int dev = 0;
   cudaGetDevice(&dev);
   char key[512];
-  snprintf(key, sizeof key, "%d|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%d|%p|%p|%d|%d", dev,
+  snprintf(key, sizeof key, "%d|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%d|%p|%p|%d|%d|%d", dev,
            (const void*)&p, nsys, (const void*)in.T, in.T_bs, (const void*)in.L, in.L_bs,
            (const void*)in.G, in.G_bs, (const void*)in.beta_sq, in.beta_bs, (const void*)in.rhs,
-           in.rhs_bs, in.rhs_is_normal, (void*)gs[0].x, ws, refine, (int)gs.size());
+           in.rhs_bs, in.rhs_is_normal, (void*)gs[0].x, ws, phase, cg_init, (int)gs.size());
   std::lock_guard<std::mutex> lk(g_graph_mu);
   GraphEntry& e = g_graphs[key];
   e.calls += 1;
-  if (!e.exec && e.calls < 2) return solve_groups(p, gs, refine, st);
+  if (!e.exec && e.calls < 2) return phase_groups(p, gs, phase, cg_init, st);
   static thread_local cudaStream_t gst = nullptr;
   static thread_local cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   if (!gst) {
@@ -1120,7 +1177,7 @@ int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine,
     cudaGraph_t g = nullptr;
     const long long n0 = g_launches.load();
     TR_CUDA_CHECK(cudaStreamBeginCapture(gst, cudaStreamCaptureModeThreadLocal));
-    int rc = solve_groups(p, gs, refine, gst);
+    int rc = phase_groups(p, gs, phase, cg_init, gst);
     cudaError_t ce = cudaStreamEndCapture(gst, &g);
     if (rc) {
       if (g) cudaGraphDestroy(g);
@@ -1146,6 +1203,69 @@ int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine,
   TR_CUDA_CHECK(cudaEventRecord(ev_out, gst));
   TR_CUDA_CHECK(cudaStreamWaitEvent(st, ev_out, 0));
   g_launches.fetch_add(e.nodes);
+  return 0;
+}
+
+// any system of any group still iterating (st[2] == 1)?
+int cg_any_active(std::vector<Group>& gs, cudaStream_t st, bool* any) {
+  static thread_local int* hflag = nullptr;
+  if (!hflag) TR_CUDA_CHECK(cudaMallocHost(&hflag, sizeof(int) * 8));
+  for (size_t g = 0; g < gs.size(); ++g) {
+    int* dflag = reinterpret_cast<int*>(gs[g].w.red);
+    TR_TRY(launch_cg_active(gs[g].w.partial, gs[g].count, dflag, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(hflag + g, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  }
+  TR_CUDA_CHECK(cudaStreamSynchronize(st));
+  *any = false;
+  for (size_t g = 0; g < gs.size(); ++g) *any = *any || hflag[g] != 0;
+  return 0;
+}
+
+// any system CG did not converge on (st[2] != 0)?
+int cg_any_unconverged(std::vector<Group>& gs, cudaStream_t st, bool* need) {
+  std::vector<std::vector<double>> h(gs.size());
+  for (size_t g = 0; g < gs.size(); ++g) {
+    h[g].resize((size_t)gs[g].count * 4);
+    TR_CUDA_CHECK(cudaMemcpyAsync(h[g].data(), gs[g].w.partial, sizeof(double) * h[g].size(),
+                                  cudaMemcpyDeviceToHost, st));
+  }
+  TR_CUDA_CHECK(cudaStreamSynchronize(st));
+  *need = false;
+  for (auto& v : h)
+    for (size_t s = 0; s < v.size(); s += 4) *need = *need || v[s + 2] != 0.0;
+  return 0;
+}
+
+// The whole solve: direct, refinement (CG first when refine_cg > 0, direct
+// solves otherwise or for what CG left unfinished), final residual.
+int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine, int refine_cg, cudaStream_t st,
+              void* ws, bool* cg_refined) {
+  *cg_refined = false;
+  // CG refinement cap from the plan alone (every system decides from its own
+  // residual history, so results do not depend on the batch): about one CG
+  // iteration per 32 conditions; small systems (latency-bound direct solve)
+  // refine directly
+  const long long C = (long long)p.rows * p.N;
+  const int cap = (int)std::min<long long>(refine_cg, C / 32);
+  const int cg = refine > 0 && refine_cg > 0 && C >= 4096 && cap >= CG_BLOCK;
+  TR_TRY(run_phase(p, gs, nsys, PH_DIRECT, cg, st, ws));
+  if (!cg) {
+    for (int r = 0; r < refine; ++r) TR_TRY(run_phase(p, gs, nsys, PH_REFINE, 0, st, ws));
+    TR_TRY(run_phase(p, gs, nsys, PH_FINAL, 0, st, ws));
+    return 0;
+  }
+  bool any = true;
+  for (int it = 0; it < cap && any; it += CG_BLOCK) {
+    TR_TRY(run_phase(p, gs, nsys, PH_CG, cap, st, ws));
+    TR_TRY(cg_any_active(gs, st, &any));
+  }
+  // systems CG did not converge on: direct refinement from their direct solution
+  bool need = false;
+  TR_TRY(cg_any_unconverged(gs, st, &need));
+  if (need)
+    for (int r = 0; r < refine; ++r) TR_TRY(run_phase(p, gs, nsys, PH_REFINE_CG, 0, st, ws));
+  *cg_refined = true;
+  TR_TRY(run_phase(p, gs, nsys, PH_FINAL, 0, st, ws));
   return 0;
 }
 
@@ -1210,9 +1330,10 @@ extern "C" int tr_solve_batch(const tr_desc* d, int64_t batch, const double* T_g
     g.x = reinterpret_cast<cplx*>(x_out) + f * p->n;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  TR_TRY(run_solve(*p, gs, batch, d->refine, st, workspace));
+  bool cg_refined = false;
+  TR_TRY(run_solve(*p, gs, batch, d->refine, d->refine_cg, st, workspace, &cg_refined));
   if (diag_host)
-    for (auto& g : gs) TR_TRY(read_diag(*p, g.count, g.w, st, diag_host + g.first));
+    for (auto& g : gs) TR_TRY(read_diag(*p, g.count, g.w, st, diag_host + g.first, cg_refined));
   if (diag_host) {
     for (long long s = 0; s < batch; ++s) {
       if (diag_host[s].status == 3) return 3;

@@ -35,13 +35,16 @@ class SingularSystemError(RuntimeError):
 
 @dataclass(frozen=True)
 class SolverConfig:
-    """ref: solver.py:39-45.  ``refine`` (extra field) runs that many
-    iterative-refinement solves on the normal-equation residual.  The
-    default 1 puts x within ~1e-14 of the exact solution, so the distance to
-    the reference's x_hat equals the reference's own error (<= 1e-9 on
+    """ref: solver.py:39-45.  Extra fields: ``refine`` > 0 refines the
+    direct (superfast) solution on the normal-equation residual, which puts
+    x within ~1e-14 of the exact solution, so the distance to the
+    reference's x_hat equals the reference's own error (<= 1e-9 on
     well-conditioned problems); 0 is the reference's single pass, whose FP64
     leaf rounding lands ~sqrt(2) x the reference's error away from it
-    (SURVEY Appendix B)."""
+    (SURVEY Appendix B).  ``refine_cg`` caps the conjugate-gradient
+    iterations (warm-started at the direct solution) tried first; systems CG
+    does not finish within the cap (ill-conditioned ones), or all systems
+    when it is 0, get ``refine`` direct refinement solves instead."""
 
     n_lim: int = 256
     pivot_threshold: float = 1e-8
@@ -49,11 +52,13 @@ class SolverConfig:
     paired: bool = True
     force_even: bool = True
     refine: int = 1
+    refine_cg: int = 256
 
 
 @dataclass
 class TanIntDiagnostics:
-    """ref: tanint.py:72-85 (plus retried_leaves / trim_overflow)."""
+    """ref: tanint.py:72-85 (plus retried_leaves / trim_overflow and the
+    CG refinement iterations)."""
 
     conditions_total: int = 0
     difficult_points: int = 0
@@ -61,6 +66,7 @@ class TanIntDiagnostics:
     max_column_scale: float = 1.0
     retried_leaves: int = 0
     trim_overflow: int = 0
+    refine_cg_iterations: int = 0
 
     def as_dict(self) -> dict:
         return {
@@ -120,6 +126,7 @@ def make_desc(variant, m, n, pl, cfg: SolverConfig) -> _lib.TrDesc:
     d.paired = int(bool(cfg.paired))
     d.force_even = int(bool(cfg.force_even))
     d.refine = int(cfg.refine)
+    d.refine_cg = int(cfg.refine_cg)
     return d
 
 
@@ -272,7 +279,8 @@ class DeviceBatch:
                 recursion_depth=int(dg.recursion_depth),
                 max_column_scale=float(dg.max_column_scale),
                 retried_leaves=int(dg.retried_leaves),
-                trim_overflow=int(dg.trim_overflow))
+                trim_overflow=int(dg.trim_overflow),
+                refine_cg_iterations=int(dg.refine_cg_iterations))
             out.append(SolveReport(
                 x_hat=np.array(x[i], dtype=np.complex128),
                 variant=self.variant, wall_time=wall / self.batch,

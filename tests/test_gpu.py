@@ -392,3 +392,17 @@ def test_run_nufft_matches_reference(gpu):
     assert rel(x, exact) <= rel(g["run_x"], exact) * 1.01 + 1e-12
     assert out["rel_err_direct"] <= float(g["run_err"]) * 1.01
     assert out["cg_iterations"] >= 1 and out["rel_residual_direct"] < 1e-6
+
+
+@pytest.mark.parametrize("name", ["c2_mini_rhs0", "c5_mini_sys0", "rand512_general", "c3_mini_lam0.01"])
+def test_direct_refinement_path(gpu, name):
+    """refine_cg=0: refinement by a second superfast solve (the path CG
+    falls back to) reaches the same accuracy as the CG refinement."""
+    tb = gpu
+    raw, d = load_case(os.path.join(GOLDEN, "cases", name + ".npz"))
+    prob = wl.to_problem(raw, tb)
+    a = tb.solve_tikhonov(prob, tb.SolverConfig(refine=1, refine_cg=0)).x_hat
+    b = tb.solve_tikhonov(prob, tb.SolverConfig(refine=1)).x_hat
+    ex = d["x_exact"]
+    ra, rb = rel(a, ex), rel(b, ex)
+    assert ra < 1e-11 and rb < 1e-11, (ra, rb)
