@@ -3,6 +3,7 @@
 #include <cmath>
 // Batched complex128 multi-pass Stockham FFT (see fft.cuh).
 #include "fft.cuh"
+#include "kernels.cuh"
 #include "fft_fast.cuh"
 
 #include <math.h>
@@ -448,10 +449,14 @@ int fft_plan(long long n, FftPlan* out) {
 }
 
 static int launch_pass(const FftPlan& p, int i, const cplx* in, long long in_ls, long long in_len,
-                       cplx* out, long long out_ls, long long lines, int sign, cudaStream_t st) {
+                       cplx* out, long long out_ls, long long lines, int sign, cudaStream_t st,
+                       const cplx* mul = nullptr, long long mul_ls = 0, double mul_scale = 1.0) {
   const FftPass& ps = p.pass[i];
   if (ps.fast) {
     FastArgs f;
+    f.mul = mul;
+    f.mul_ls = mul_ls;
+    f.mul_scale = mul_scale;
     f.in = in;
     f.in_ls = in_ls;
     f.in_len = (int)in_len;
@@ -469,6 +474,7 @@ static int launch_pass(const FftPlan& p, int i, const cplx* in, long long in_ls,
     const bool small = p.npass == 1 && ps.R <= 1024;
     static const bool old_kernels = getenv("TR_FFT_OLD") != nullptr;
     if (p.npass == 1 && !old_kernels && reg_launch(ps.log2, ps.q, f, st) == 0) return 0;
+    f.mul = nullptr;  // (fft_exec multiplied first when the register kernel cannot fuse it)
     if (fast_launch(ps.log2, ps.q, small, f, st) == 0) return 0;
   }
   PassArgs a;
@@ -503,10 +509,27 @@ static int launch_pass(const FftPlan& p, int i, const cplx* in, long long in_ls,
 }
 
 int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len, cplx* out,
-             long long out_ls, cplx* scratch, long long lines, int sign, cudaStream_t st) {
+             long long out_ls, cplx* scratch, long long lines, int sign, cudaStream_t st,
+             const cplx* mul, long long mul_ls, double mul_scale) {
   if (lines <= 0) return 0;
   if (in_len > p.n) in_len = p.n;
   const long long n = p.n;
+  static const bool old_kernels = getenv("TR_FFT_OLD") != nullptr;
+  if (mul) {
+    // the column kernels and the single-pass register kernel fuse the factor
+    // into their loads; other plans multiply first
+    const FftPass& p0 = p.pass[0];
+    const int q0 = p0.q;
+    const bool reg = p.npass == 1 && p0.fast && !old_kernels && p0.R >= 2 && p0.R <= 4096 && p0.log2 <= 12 &&
+                     (q0 == 1 || q0 == 3 || q0 == 5 || q0 == 7 || q0 == 9 || q0 == 15);
+    if (!p.col && !reg) {
+      if (in_len != n) { tr_set_error("fft_exec: fused factor needs full-length lines"); return 2; }
+      { const int rc0 = launch_spec_mul(out, out_ls, in, in_ls, mul, mul_ls, n, mul_scale, lines, st); if (rc0) return rc0; }
+      in = out;
+      in_ls = out_ls;
+      mul = nullptr;
+    }
+  }
   tr_kernel_work(TRK_FFT, 16.0 * lines * (double)(in_len + n),
                  5.0 * lines * (double)n * std::log2((double)n));
   if (p.col) {
@@ -542,12 +565,16 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
       c.twN = p.twN;
       c.tw2 = p.twc;
       c.sign = sign;
+      c.mul = mul ? mul + s0 * mul_ls : nullptr;
+      c.mul_ls = mul_ls;
+      c.mul_scale = mul_scale;
       int rc = col_launch(true, p.a1, 1, c, st);
       if (rc) {
         if (s0 == 0) break;  // no column kernel: the pass plan below
         tr_set_error("fft column plan has no kernel for n=%lld", n);
         return 2;
       }
+      c.mul = nullptr;
       c.in = scratch;
       c.in_ls = n;
       c.in_len = n;
@@ -566,7 +593,7 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
     }
   }
   if (p.npass == 1) {
-    launch_pass(p, 0, in, in_ls, in_len, out, out_ls, lines, sign, st);
+    launch_pass(p, 0, in, in_ls, in_len, out, out_ls, lines, sign, st, mul, mul_ls, mul_scale);
   } else if (p.npass == 2) {
     launch_pass(p, 0, in, in_ls, in_len, scratch, n, lines, sign, st);
     launch_pass(p, 1, scratch, n, n, out, out_ls, lines, sign, st);

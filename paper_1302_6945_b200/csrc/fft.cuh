@@ -45,13 +45,15 @@ bool fft_supported(long long n);
 // Smallest supported length >= n with cheap factors (cost-ranked).
 long long fft_good_len(long long n);
 
-// Batched transform of `lines` lines.  Line i of the input starts at
+// Batched transform of `lines` lines (optionally of in[e] * mul_scale *
+// mul[line * mul_ls + e], the product fused into the load).  Line i of the input starts at
 // in + i*in_ls and holds in_len <= n valid values (zero-padded to n); the
 // output line i starts at out + i*out_ls.  `scratch` must hold lines*n
 // values.  in == out is allowed.
 int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len,
              cplx* out, long long out_ls, cplx* scratch, long long lines, int sign,
-             cudaStream_t st);
+             cudaStream_t st,
+             const cplx* mul = nullptr, long long mul_ls = 0, double mul_scale = 1.0);
 
 // Twiddle table exp(2 pi i k / n), k < n (cached, device memory).
 const cplx* twiddle_table(long long n);

@@ -63,7 +63,7 @@ TR_D void tw_apply(cplx (&v)[RS], const cplx* twR, int k, int step, int sign) {
 // element e of sub-transform s of line: in[line*in_ls + s + e*in_es]
 template <int LOG2, int Q, bool PASSA, int S>
 TR_D void col_stage(cplx* sm, const ColArgs& a, long long lbase_in, long long lbase_out, int s, bool live,
-                    int tb) {
+                    int tb, const cplx* mrow) {
   using G = CPlan<LOG2, Q>;
   constexpr int R = G::R, r = G::radix(S), NS = G::ns(S), B = R / r, T = G::T;
   constexpr int IT = (B + T - 1) / T;
@@ -80,6 +80,9 @@ TR_D void col_stage(cplx* sm, const ColArgs& a, long long lbase_in, long long lb
         if constexpr (FIRST) {
           const long long gi = s + (long long)e * a.in_es;
           cplx x = gi < a.in_len ? a.in[lbase_in + gi] : cmk(0.0, 0.0);
+          if constexpr (PASSA) {
+            if (mrow) x = cmul(x, cscale(mrow[gi], a.mul_scale));
+          }
           if constexpr (!PASSA) {
             // W_N^(n2 k1) = W_N^(n2 k1h TL) W_N^(n2 k1l), k1 = s = s0 + sl: the first
             // factor is warp-uniform (broadcast), the second a coalesced [N2][TL] row
@@ -119,7 +122,7 @@ TR_D void col_stage(cplx* sm, const ColArgs& a, long long lbase_in, long long lb
   }
   if constexpr (!LAST) {
     __syncthreads();
-    col_stage<LOG2, Q, PASSA, S + 1>(sm, a, lbase_in, lbase_out, s, live, tb);
+    col_stage<LOG2, Q, PASSA, S + 1>(sm, a, lbase_in, lbase_out, s, live, tb, mrow);
   }
 }
 
@@ -134,7 +137,8 @@ __global__ void __launch_bounds__(NTH) fft_col_kernel(ColArgs a) {
   const int s0 = (int)(sub0 - line * a.subs);
   const bool live = line < a.lines;
   const long long lin = line * a.in_ls, lout = line * a.out_ls;
-  col_stage<LOG2, Q, PASSA, 0>(tile + (size_t)sl * G::LS, a, lin, lout, s0 + sl, live, tb);
+  const cplx* mrow = (PASSA && a.mul) ? a.mul + line * a.mul_ls : nullptr;
+  col_stage<LOG2, Q, PASSA, 0>(tile + (size_t)sl * G::LS, a, lin, lout, s0 + sl, live, tb, mrow);
   if constexpr (PASSA) {
     // outputs of each sub-transform are contiguous: Y[s R + k]
     __syncthreads();

@@ -16,6 +16,10 @@ struct FastArgs {
   const cplx* twN;
   const cplx* twR;
   int sign;
+  // optional pointwise factor applied on load: x[e] * mul_scale * mul[line * mul_ls + e]
+  const cplx* mul = nullptr;
+  long long mul_ls = 0;
+  double mul_scale = 1.0;
 };
 
 bool fast_supported(int log2, int q);
@@ -39,6 +43,10 @@ struct ColArgs {
   const cplx* twN;    // exp(2 pi i k / n)
   const cplx* tw2;    // pass B: exp(2 pi i n2 l / n), [N2][TL]
   int sign;
+  // pass A only: pointwise factor on load, x[gi] * mul_scale * mul[line * mul_ls + gi]
+  const cplx* mul = nullptr;
+  long long mul_ls = 0;
+  double mul_scale = 1.0;
 };
 // sub-transforms per CTA of the column kernels for transform length R
 inline int col_tile(int R) {

@@ -66,7 +66,7 @@ TR_D void tw_apply(cplx (&v)[RS], const cplx* twR, int k, int step, int sign) {
 
 template <int LOG2, int Q, int S>
 TR_D void run_stage(cplx* sm, const FastArgs& a, long long lin, long long lout, bool live, int tb,
-                    int sign) {
+                    int sign, const cplx* mrow) {
   using G = Plan<LOG2, Q>;
   constexpr int R = G::R, r = G::radix(S), NS = G::ns(S), B = R / r, T = G::T;
   constexpr int IT = (B + T - 1) / T;
@@ -82,6 +82,7 @@ TR_D void run_stage(cplx* sm, const FastArgs& a, long long lin, long long lout, 
         const int e = b + u * B;
         if constexpr (FIRST) {
           v[it][u] = e < a.in_len ? a.in[lin + e] : cmk(0.0, 0.0);
+          if (mrow) v[it][u] = cmul(v[it][u], cscale(mrow[e], a.mul_scale));
         } else {
           v[it][u] = sm[e + (e >> PSH)];
         }
@@ -110,7 +111,7 @@ TR_D void run_stage(cplx* sm, const FastArgs& a, long long lin, long long lout, 
   }
   if constexpr (!LAST) {
     __syncthreads();
-    run_stage<LOG2, Q, S + 1>(sm, a, lin, lout, live, tb, sign);
+    run_stage<LOG2, Q, S + 1>(sm, a, lin, lout, live, tb, sign, mrow);
   }
 }
 
@@ -124,7 +125,8 @@ __global__ void __launch_bounds__(NTH, 3) fft_reg_kernel(FastArgs a, int TL) {
   const long long line = (long long)blockIdx.x * TL + sl;
   const bool live = line < a.nsub;
   cplx* sm = reinterpret_cast<cplx*>(fsm) + (size_t)sl * G::LS;
-  run_stage<LOG2, Q, 0>(sm, a, line * a.in_ls, line * a.out_ls, live, tb, a.sign);
+  const cplx* mrow = a.mul ? a.mul + line * a.mul_ls : nullptr;
+  run_stage<LOG2, Q, 0>(sm, a, line * a.in_ls, line * a.out_ls, live, tb, a.sign, mrow);
 }
 
 template <int LOG2, int Q>

@@ -696,12 +696,11 @@ int gram_term(const Plan& p, long long nsys, const WS& w, long long sbs, int fwd
   const long long q = p.q;
   const cplx* Ef = w.spec_emb + (long long)eidx(p, fwd) * q;
   const cplx* Ea = w.spec_emb + (long long)eidx(p, adj) * q;
-  TR_TRY(launch_spec_mul(w.S2, q, w.S1, q, Ef, sbs, q, 1.0, nsys, st));
-  TR_TRY(fft_exec(F(p, q), w.S2, q, q, w.S2, q, w.S3, nsys, +1, st));
-  TR_TRY(launch_mask_scale(w.S2, q, q, rows_blk, 1.0 / (double)q, nsys, st));
-  TR_TRY(fft_exec(F(p, q), w.S2, q, q, w.S2, q, w.S3, nsys, -1, st));
-  TR_TRY(launch_spec_mul(w.S2, q, w.S2, q, Ea, sbs, q, 1.0 / (double)q, nsys, st));
-  TR_TRY(fft_exec(F(p, q), w.S2, q, q, w.S2, q, w.S3, nsys, +1, st));
+  // ifft(Ef . FX) (factor fused into the load), keep the first rows_blk
+  // values (zero padding of the next load), fft, ifft(Ea . (1/q^2)), first n
+  TR_TRY(fft_exec(F(p, q), w.S1, q, q, w.S2, q, w.S3, nsys, +1, st, Ef, sbs, 1.0));
+  TR_TRY(fft_exec(F(p, q), w.S2, q, rows_blk, w.S2, q, w.S3, nsys, -1, st));
+  TR_TRY(fft_exec(F(p, q), w.S2, q, q, w.S2, q, w.S3, nsys, +1, st, Ea, sbs, 1.0 / ((double)q * (double)q)));
   TR_TRY(launch_accum(w.AX, p.n, w.S2, q, p.n, 1.0, overwrite, nsys, st));
   return 0;
 }
@@ -718,8 +717,7 @@ int normal_apply(const Plan& p, long long nsys, const WS& w, long long sbs, cons
     TR_TRY(gram_term(p, nsys, w, sbs, 2, 3, p.pl, 0, st));
   } else {
     const cplx* Eg = w.spec_emb + (long long)eidx(p, 4) * q;
-    TR_TRY(launch_spec_mul(w.S2, q, w.S1, q, Eg, sbs, q, 1.0 / (double)q, nsys, st));
-    TR_TRY(fft_exec(F(p, q), w.S2, q, q, w.S2, q, w.S3, nsys, +1, st));
+    TR_TRY(fft_exec(F(p, q), w.S1, q, q, w.S2, q, w.S3, nsys, +1, st, Eg, sbs, 1.0 / (double)q));
     TR_TRY(launch_accum(w.AX, n, w.S2, q, n, 1.0, 1, nsys, st));
     TR_TRY(gram_term(p, nsys, w, sbs, 2, 3, p.pl, 0, st));
   }
