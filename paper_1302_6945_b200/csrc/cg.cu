@@ -45,15 +45,15 @@ __global__ void __launch_bounds__(CGT) cg_init_kernel(cplx* X, cplx* R, cplx* D,
 }
 
 __global__ void __launch_bounds__(CGT) cg_update_kernel(cplx* X, cplx* R, cplx* D, const cplx* AD,
-                                                        const double* beta_sq, long long beta_bs, int ridge,
-                                                        long long n, double tol, double* st, int* it) {
+                                                        long long ad_ls, const double* beta_sq, long long beta_bs,
+                                                        int ridge, long long n, double tol, double* st, int* it) {
   __shared__ double sh[CGT / 32];
   const long long sys = blockIdx.x;
   if (st[sys * 4 + 2] != 1.0) return;
   cplx* x = X + sys * n;
   cplx* r = R + sys * n;
   cplx* d = D + sys * n;
-  const cplx* ad = AD + sys * n;
+  const cplx* ad = AD + sys * ad_ls;
   const double b2 = ridge ? beta_sq[sys * beta_bs] : 0.0;
   // Re <d, A d> (A d = normal operator + |beta|^2 d for the ridge variant)
   double s = 0.0;
@@ -168,10 +168,12 @@ int launch_cg_init(cplx* X, cplx* R, cplx* D, const cplx* Y, long long n, double
 }
 
 int launch_cg_update(cplx* X, cplx* R, cplx* D, const cplx* AD, const double* beta_sq, long long beta_bs,
-                     int ridge, long long n, double tol, double* st, int* it, long long nsys, cudaStream_t s) {
+                     int ridge, long long n, double tol, double* st, int* it, long long nsys, cudaStream_t s,
+                     long long ad_ls) {
   {
     TrKTimer _kt(TRK_NORMAL, s);
-    cg_update_kernel<<<(unsigned)nsys, CGT, 0, s>>>(X, R, D, AD, beta_sq, beta_bs, ridge, n, tol, st, it);
+    cg_update_kernel<<<(unsigned)nsys, CGT, 0, s>>>(X, R, D, AD, ad_ls > 0 ? ad_ls : n, beta_sq, beta_bs, ridge, n,
+                                                    tol, st, it);
   }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;

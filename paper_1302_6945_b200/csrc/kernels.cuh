@@ -112,7 +112,8 @@ int launch_add_inplace(cplx* x, const cplx* d, long long n, long long nsys, cuda
 int launch_cg_init(cplx* X, cplx* R, cplx* D, const cplx* Y, long long n, double* st, int* it, long long nsys,
                    cudaStream_t s);
 int launch_cg_update(cplx* X, cplx* R, cplx* D, const cplx* AD, const double* beta_sq, long long beta_bs,
-                     int ridge, long long n, double tol, double* st, int* it, long long nsys, cudaStream_t s);
+                     int ridge, long long n, double tol, double* st, int* it, long long nsys, cudaStream_t s,
+                     long long ad_ls = 0);
 int launch_cg_active(const double* st, long long nsys, int* any, cudaStream_t s);
 int launch_cg_warm(const cplx* X, cplx* R, cplx* D, const cplx* AX, const cplx* Y, const double* beta_sq,
                    long long beta_bs, int ridge, long long n, double* st, int* it, long long nsys, cudaStream_t s);

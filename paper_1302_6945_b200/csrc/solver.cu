@@ -690,7 +690,8 @@ int eidx(const Plan& p, int which) {
   return which == 2 ? 0 : which == 3 ? 1 : 2;
 }
 
-// acc (=|+=) B2^H-side gram term: adj(B) (B x) from FX = fft(x)
+// acc (=|+=) B2^H-side gram term: adj(B) (B x) from FX = fft(x); overwrite
+// < 0 leaves the term in S2 (first n of every length-q line) instead
 int gram_term(const Plan& p, long long nsys, const WS& w, long long sbs, int fwd, int adj,
               long long rows_blk, int overwrite, cudaStream_t st) {
   const long long q = p.q;
@@ -701,7 +702,7 @@ int gram_term(const Plan& p, long long nsys, const WS& w, long long sbs, int fwd
   TR_TRY(fft_exec(F(p, q), w.S1, q, q, w.S2, q, w.S3, nsys, +1, st, Ef, sbs, 1.0));
   TR_TRY(fft_exec(F(p, q), w.S2, q, rows_blk, w.S2, q, w.S3, nsys, -1, st));
   TR_TRY(fft_exec(F(p, q), w.S2, q, q, w.S2, q, w.S3, nsys, +1, st, Ea, sbs, 1.0 / ((double)q * (double)q)));
-  TR_TRY(launch_accum(w.AX, p.n, w.S2, q, p.n, 1.0, overwrite, nsys, st));
+  if (overwrite >= 0) TR_TRY(launch_accum(w.AX, p.n, w.S2, q, p.n, 1.0, overwrite, nsys, st));
   return 0;
 }
 
@@ -1001,9 +1002,16 @@ int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
   const long long sbs = spectra_bstride(p, in);
   if (phase == PH_CG) {
     for (int k = 0; k < CG_BLOCK; ++k) {
-      TR_TRY(normal_apply(p, nsys, w, sbs, w.X2, st));
-      TR_TRY(launch_cg_update(w.X, w.Rv, w.X2, w.AX, in.beta_sq, in.beta_bs, add_ridge, n, 1.0, cst, its,
-                              nsys, st));
+      if (p.variant == TR_L2) {  // one Gram term: the update reads it from the transform buffer
+        TR_TRY(fft_exec(F(p, p.q), w.X2, n, n, w.S1, p.q, w.S3, nsys, -1, st));
+        TR_TRY(gram_term(p, nsys, w, sbs, 0, 1, p.m, -1, st));
+        TR_TRY(launch_cg_update(w.X, w.Rv, w.X2, w.S2, in.beta_sq, in.beta_bs, add_ridge, n, 1.0, cst, its,
+                                nsys, st, p.q));
+      } else {
+        TR_TRY(normal_apply(p, nsys, w, sbs, w.X2, st));
+        TR_TRY(launch_cg_update(w.X, w.Rv, w.X2, w.AX, in.beta_sq, in.beta_bs, add_ridge, n, 1.0, cst, its,
+                                nsys, st));
+      }
     }
     TR_TRY(launch_cg_check(cst, its, nsys, cg_init, st));  // cg_init carries the iteration cap here
     return 0;
