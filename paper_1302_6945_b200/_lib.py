@@ -80,6 +80,7 @@ SIGNATURES = {
     "tr_kernel_stats": (C.c_int, [_I32, C.POINTER(C.c_double), C.POINTER(_I64)]),
     "tr_kernel_work_stats": (C.c_int, [_I32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "tr_fp64_peak": (C.c_int, [C.POINTER(C.c_double)]),
+    "tr_fft_breakdown": (C.c_int, [C.POINTER(_I64), C.POINTER(C.c_double), C.c_int]),
     "tr_last_error": (C.c_char_p, []),
 }
 

@@ -4,6 +4,8 @@
 // Batched complex128 multi-pass Stockham FFT (see fft.cuh).
 #include "fft.cuh"
 #include "kernels.cuh"
+
+extern thread_local long long g_fft_tag;
 #include "fft_fast.cuh"
 
 #include <math.h>
@@ -510,10 +512,11 @@ static int launch_pass(const FftPlan& p, int i, const cplx* in, long long in_ls,
 
 int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len, cplx* out,
              long long out_ls, cplx* scratch, long long lines, int sign, cudaStream_t st,
-             const cplx* mul, long long mul_ls, double mul_scale) {
+             const cplx* mul, long long mul_ls, double mul_scale, long long chunk_bytes_override) {
   if (lines <= 0) return 0;
   if (in_len > p.n) in_len = p.n;
   const long long n = p.n;
+  g_fft_tag = (n << 20) + (lines & ((1 << 20) - 1));
   static const bool old_kernels = getenv("TR_FFT_OLD") != nullptr;
   if (mul) {
     // the column kernels and the single-pass register kernel fuse the factor
@@ -543,8 +546,9 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
       return (long long)(e ? atof(e) : 16.0) * (1LL << 20);
     }();
     long long cl = lines;
-    if (chunk_bytes > 0) {
-      cl = chunk_bytes / (n * (long long)sizeof(cplx));
+    const long long cb = chunk_bytes_override >= 0 ? chunk_bytes_override : chunk_bytes;
+    if (cb > 0) {
+      cl = cb / (n * (long long)sizeof(cplx));
       if (cl < 1) cl = 1;
       if (cl > lines) cl = lines;
     }

@@ -53,7 +53,8 @@ long long fft_good_len(long long n);
 int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len,
              cplx* out, long long out_ls, cplx* scratch, long long lines, int sign,
              cudaStream_t st,
-             const cplx* mul = nullptr, long long mul_ls = 0, double mul_scale = 1.0);
+             const cplx* mul = nullptr, long long mul_ls = 0, double mul_scale = 1.0,
+             long long chunk_bytes_override = -1);
 
 // Twiddle table exp(2 pi i k / n), k < n (cached, device memory).
 const cplx* twiddle_table(long long n);

@@ -127,7 +127,7 @@ TR_D void col_stage(cplx* sm, const ColArgs& a, long long lbase_in, long long lb
 }
 
 template <int LOG2, int Q, bool PASSA>
-__global__ void __launch_bounds__(NTH) fft_col_kernel(ColArgs a) {
+__global__ void __launch_bounds__(NTH, 3) fft_col_kernel(ColArgs a) {
   using G = CPlan<LOG2, Q>;
   extern __shared__ __align__(16) unsigned char fsm[];
   cplx* tile = reinterpret_cast<cplx*>(fsm);

@@ -48,6 +48,7 @@ std::atomic<bool> g_timing{false};
 struct KEvent {
   int cls;
   cudaEvent_t a, b;
+  long long tag;  // FFT launches: n * 2^20 + lines (diagnostic breakdown)
 };
 std::mutex g_kmu;
 std::vector<KEvent> g_kpending;
@@ -57,6 +58,10 @@ long long g_kcount[TRK_NCLASS] = {0};
 double g_kbytes[TRK_NCLASS] = {0};
 double g_kflops[TRK_NCLASS] = {0};
 thread_local int g_kcur = -1;
+std::map<long long, std::pair<double, long long>> g_fft_by_tag;
+}  // namespace
+thread_local long long g_fft_tag = 0;  // set by fft_exec (fft.cu)
+namespace {
 
 cudaEvent_t kev_get() {
   if (!g_kpool.empty()) {
@@ -74,7 +79,7 @@ void tr_kernel_begin(int cls, cudaStream_t st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (!g_timing.load(std::memory_order_relaxed)) return;
   std::lock_guard<std::mutex> lk(g_kmu);
-  KEvent k{cls, kev_get(), kev_get()};
+  KEvent k{cls, kev_get(), kev_get(), cls == TRK_FFT ? g_fft_tag : 0};
   cudaEventRecord(k.a, st);
   g_kpending.push_back(k);
   g_kcur = (int)g_kpending.size() - 1;
@@ -103,6 +108,11 @@ static void kernel_stats_drain() {
     cudaEventElapsedTime(&ms, k.a, k.b);
     g_kms[k.cls] += ms;
     g_kcount[k.cls] += 1;
+    if (k.tag) {
+      auto& e = g_fft_by_tag[k.tag];
+      e.first += ms;
+      e.second += 1;
+    }
     g_kpool.push_back(k.a);
     g_kpool.push_back(k.b);
   }
@@ -120,8 +130,27 @@ extern "C" int tr_kernel_timing(int32_t enable) {
     g_kbytes[c] = 0.0;
     g_kflops[c] = 0.0;
   }
+  g_fft_by_tag.clear();
   g_timing.store(enable != 0);
   return 0;
+}
+
+// FFT time by (length, lines) while timing was enabled, largest first:
+// fills up to `cap` rows of {n, lines, launches} and ms; returns the rows
+extern "C" int tr_fft_breakdown(int64_t* rows, double* ms, int cap) {
+  kernel_stats_drain();
+  std::lock_guard<std::mutex> lk(g_kmu);
+  std::vector<std::pair<double, long long>> v;
+  for (auto& kv : g_fft_by_tag) v.push_back({kv.second.first, kv.first});
+  std::sort(v.rbegin(), v.rend());
+  int k = 0;
+  for (; k < cap && k < (int)v.size(); ++k) {
+    rows[3 * k] = v[k].second >> 20;
+    rows[3 * k + 1] = v[k].second & ((1 << 20) - 1);
+    rows[3 * k + 2] = g_fft_by_tag[v[k].second].second;
+    ms[k] = v[k].first;
+  }
+  return k;
 }
 
 extern "C" int tr_kernel_stats(int32_t cls, double* total_ms, int64_t* launches) {
@@ -690,6 +719,16 @@ int eidx(const Plan& p, int which) {
   return which == 2 ? 0 : which == 3 ? 1 : 2;
 }
 
+// L2 chunk budget of the normal operator's transforms (TR_NOP_L2MB, MB; the
+// operator runs hundreds of times per CG refinement)
+long long nop_chunk() {
+  static const long long b = [] {
+    const char* e = getenv("TR_NOP_L2MB");
+    return e ? (long long)(atof(e) * (1 << 20)) : -1LL;
+  }();
+  return b;
+}
+
 // acc (=|+=) B2^H-side gram term: adj(B) (B x) from FX = fft(x); overwrite
 // < 0 leaves the term in S2 (first n of every length-q line) instead
 int gram_term(const Plan& p, long long nsys, const WS& w, long long sbs, int fwd, int adj,
@@ -699,9 +738,10 @@ int gram_term(const Plan& p, long long nsys, const WS& w, long long sbs, int fwd
   const cplx* Ea = w.spec_emb + (long long)eidx(p, adj) * q;
   // ifft(Ef . FX) (factor fused into the load), keep the first rows_blk
   // values (zero padding of the next load), fft, ifft(Ea . (1/q^2)), first n
-  TR_TRY(fft_exec(F(p, q), w.S1, q, q, w.S2, q, w.S3, nsys, +1, st, Ef, sbs, 1.0));
-  TR_TRY(fft_exec(F(p, q), w.S2, q, rows_blk, w.S2, q, w.S3, nsys, -1, st));
-  TR_TRY(fft_exec(F(p, q), w.S2, q, q, w.S2, q, w.S3, nsys, +1, st, Ea, sbs, 1.0 / ((double)q * (double)q)));
+  const long long cb = nop_chunk();
+  TR_TRY(fft_exec(F(p, q), w.S1, q, q, w.S2, q, w.S3, nsys, +1, st, Ef, sbs, 1.0, cb));
+  TR_TRY(fft_exec(F(p, q), w.S2, q, rows_blk, w.S2, q, w.S3, nsys, -1, st, nullptr, 0, 1.0, cb));
+  TR_TRY(fft_exec(F(p, q), w.S2, q, q, w.S2, q, w.S3, nsys, +1, st, Ea, sbs, 1.0 / ((double)q * (double)q), cb));
   if (overwrite >= 0) TR_TRY(launch_accum(w.AX, p.n, w.S2, q, p.n, 1.0, overwrite, nsys, st));
   return 0;
 }
@@ -1003,7 +1043,7 @@ int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
   if (phase == PH_CG) {
     for (int k = 0; k < CG_BLOCK; ++k) {
       if (p.variant == TR_L2) {  // one Gram term: the update reads it from the transform buffer
-        TR_TRY(fft_exec(F(p, p.q), w.X2, n, n, w.S1, p.q, w.S3, nsys, -1, st));
+        TR_TRY(fft_exec(F(p, p.q), w.X2, n, n, w.S1, p.q, w.S3, nsys, -1, st, nullptr, 0, 1.0, nop_chunk()));
         TR_TRY(gram_term(p, nsys, w, sbs, 0, 1, p.m, -1, st));
         TR_TRY(launch_cg_update(w.X, w.Rv, w.X2, w.S2, in.beta_sq, in.beta_bs, add_ridge, n, 1.0, cst, its,
                                 nsys, st, p.q));
@@ -1254,7 +1294,28 @@ int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine,
   const long long C = (long long)p.rows * p.N;
   const int cap = (int)std::min<long long>(refine_cg, C / 32);
   const int cg = refine > 0 && refine_cg > 0 && C >= 4096 && cap >= CG_BLOCK;
+  // TR_PHASE_TIMES=1: device time of the direct phase and of the refinement (stderr)
+  static const bool ptimes = getenv("TR_PHASE_TIMES") != nullptr;
+  static cudaEvent_t pe[3] = {nullptr, nullptr, nullptr};
+  if (ptimes && !pe[0])
+    for (auto& e : pe) TR_CUDA_CHECK(cudaEventCreate(&e));
+  if (ptimes) TR_CUDA_CHECK(cudaEventRecord(pe[0], st));
   TR_TRY(run_phase(p, gs, nsys, PH_DIRECT, cg, st, ws));
+  if (ptimes) TR_CUDA_CHECK(cudaEventRecord(pe[1], st));
+  struct PhaseReport {
+    bool on;
+    cudaEvent_t* e;
+    cudaStream_t s;
+    ~PhaseReport() {
+      if (!on) return;
+      cudaEventRecord(e[2], s);
+      cudaEventSynchronize(e[2]);
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, e[0], e[1]);
+      cudaEventElapsedTime(&b, e[1], e[2]);
+      fprintf(stderr, "[phases] direct %.3f ms, refinement + final %.3f ms\n", a, b);
+    }
+  } report{ptimes, pe, st};
   if (!cg) {
     for (int r = 0; r < refine; ++r) TR_TRY(run_phase(p, gs, nsys, PH_REFINE, 0, st, ws));
     TR_TRY(run_phase(p, gs, nsys, PH_FINAL, 0, st, ws));
