@@ -1625,6 +1625,7 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
       int cd[P];
 #pragma unroll
       for (int i = 0; i < P; ++i) cd[i] = cd0[i];
+      int nabs = 0, ndef = 0;  // absorbed / deferred conditions (the chain epilogue, kept on the fly)
       for (int b = 0; b < H; ++b) {
         if (b > 0) {
           while (ld_acquire(&flag[1]) < b) {
@@ -1665,7 +1666,18 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
           }
 #pragma unroll
           for (int i = 0; i < P; ++i) cd[i] += (i == j);
+          nabs += j >= 0;
+          if (j == -1) {  // deferred, in step order (ref tanint.py:200-206)
+            if (lane == 0) dtry[ndef] = make_int2((int)cond_node(a, t, att), t % rows);
+            ++ndef;
+          }
         }
+      }
+      if (lane == 0) {
+        bk.nd_try = ndef;
+        bk.len_try = 1 + nabs;
+#pragma unroll
+        for (int i = 0; i < P; ++i) bk.cd_try[i] = cd[i];
       }
       if (lane == 0) tsm[12] = clock64();
     } else if (hold) {
@@ -1752,29 +1764,8 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
     }
     __syncthreads();
     if (tid == 0) tsm[13] = clock64();
-    // ---- chain epilogue (warp 0): length, ledger, deferrals in step order (ref tanint.py:200-206)
-    if (warp == 0) {
-      int len = 1, nd = 0;
-      int cdf[P];
-#pragma unroll
-      for (int i = 0; i < P; ++i) cdf[i] = cd0[i];
-      for (int base = 0; base < K; base += 32) {
-        const int t = base + lane;
-        const int j = t < K ? lj[t] : -2;
-        const unsigned def = __ballot_sync(FULL, j == -1);
-        len += __popc(__ballot_sync(FULL, j >= 0));
-        if (j == -1) dtry[nd + __popc(def & ((1u << lane) - 1u))] = make_int2((int)cond_node(a, t, att), t % rows);
-        nd += __popc(def);
-#pragma unroll
-        for (int i = 0; i < P; ++i) cdf[i] += __popc(__ballot_sync(FULL, j == i));
-      }
-      if (lane == 0) {
-        bk.nd_try = nd;
-        bk.len_try = len;
-#pragma unroll
-        for (int i = 0; i < P; ++i) bk.cd_try[i] = cdf[i];
-      }
-    } else if (tid < 32 + P && tid >= 32) {
+    // ---- column scales (the chain epilogue was kept by the decider) ----
+    if (tid < 32 + P && tid >= 32) {
       const int i = tid - 32;
       double m = 0.0;
       for (int k = 0; k < P; ++k) m = fmax(m, red[k][i]);
@@ -1782,6 +1773,7 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
       csafe[i] = m > 0.0 ? m : 1.0;
     }
     __syncthreads();
+    if (tid == 0) tsm[22] = clock64();
     // ---- normalise and write the attempt's basis (round 0: out, else scratch) ----
     cplx* dst = (round == 0 ? a.out : a.scratch) + (long long)sys * a.out_sys;
     if (brow >= 0) {
@@ -1798,6 +1790,7 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
         }
       }
     }
+    if (tid == 0) tsm[23] = clock64();
     if (cap > CAPR) {
       const int tail = cap - CAPR;
       for (int e = tid; e < PP * tail; e += nt) dst[(long long)(e / tail) * cap + CAPR + e % tail] = cmk(0.0, 0.0);
