@@ -164,10 +164,12 @@ def hbm_peak_gbs():
 
 
 def ncu_traffic(cfg, cls):
-    """dram__bytes_read+write per launch of the class's top kernel from the
-    committed ncu capture (profiles/r1_traffic.json), or None."""
+    """dram__bytes_read+write per launch of the class, averaged over the
+    class's launches in the committed ncu launch list of the same bench
+    command (profiles/traffic.json, written by tools/profile_summary.py for the
+    latest capture), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             return json.load(f)[cfg][cls]["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
         return None

@@ -5,11 +5,13 @@ import collections, csv, glob, json, os, subprocess, sys
 R = sys.argv[1] if len(sys.argv) > 1 else "r1"
 SRC = f"gpurun_out/{R}"
 OUT = "profiles"
-CLASS = [("leaf_chain", "leaf_pivot"), ("leaf_pivot", "leaf_pivot"), ("need_reset", "leaf_pivot"),
+CLASS = [("leaf_fused", "leaf_pivot"), ("leaf_chain", "leaf_pivot"), ("leaf_pivot", "leaf_pivot"), ("need_reset", "leaf_pivot"),
+         ("cg_", "normal"), ("spec_mul", "normal"), ("mask_scale", "normal"), ("accum", "normal"),
+         ("residual", "normal"), ("norm_", "normal"), ("nudft", "assemble"),
          ("leaf_basis", "leaf_build"), ("leaf_build", "leaf_build"), ("leaf_check", "leaf_check"),
          ("leaf_kernel", "leaf_exact"), ("fft", "fft"), ("trim", "combine"), ("pointwise", "combine"),
          ("twist_fold", "update"), ("apply_update", "update"), ("assemble", "assemble"),
-         ("emb_col", "assemble"), ("spec_mul", "assemble"), ("ext_seq", "assemble")]
+         ("emb_col", "assemble"), ("ext_seq", "assemble")]
 
 
 def cls(name):
@@ -69,6 +71,15 @@ for cfg in ("c2", "c5"):
     traffic[cfg] = {c: {"dram_bytes_per_launch": v[2] / max(v[0], 1), "launches": v[0], "ms": v[1] / 1e3}
                     for c, v in by_c.items()}
 json.dump(traffic, open(f"{OUT}/{R}_traffic.json", "w"), indent=1)
+if traffic:  # the capture bench.py's roofline "traffic" reads
+    old = {}
+    try:
+        old = json.load(open(f"{OUT}/traffic.json"))
+    except (OSError, ValueError):
+        pass
+    old.update(traffic)
+    old["_source"] = f"{R}: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over bench.py's timed region"
+    json.dump(old, open(f"{OUT}/traffic.json", "w"), indent=1)
 
 KEYS = ["Duration", "Elapsed Cycles", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput",
         "Executed Ipc Active", "Issue Slots Busy", "Achieved Occupancy", "Theoretical Occupancy",
