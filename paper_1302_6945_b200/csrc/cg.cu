@@ -5,6 +5,8 @@
 // rho' = |r|^2, the stopping test, d = r + (rho'/rho) d -- is one kernel with
 // one CTA per system (two block reductions), so an iteration costs the
 // operator's transforms plus one launch and nothing syncs with the host.
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 namespace {
@@ -151,6 +153,107 @@ __global__ void add_masked_kernel(cplx* X, const cplx* D, const double* st, long
   X[o] = cadd(X[o], D[o]);
 }
 
+// The same iteration tail with a cluster of C CTAs per system (each owns a
+// contiguous slice of the vectors; the two reductions combine the CTAs'
+// partial sums through DSMEM in rank order: deterministic for a given n).
+constexpr int CGC_T = 256;
+template <int C>
+__global__ void __launch_bounds__(CGC_T) cg_update_cl_kernel(cplx* X, cplx* R, cplx* D, const cplx* AD,
+                                                             long long ad_ls, const double* beta_sq,
+                                                             long long beta_bs, int ridge, long long n, double tol,
+                                                             double* st, int* it) {
+  namespace cg = cooperative_groups;
+  __shared__ double wsum[CGC_T / 32];
+  __shared__ double part[2];
+  const long long sys = blockIdx.x / C;
+  const int rank = C > 1 ? (int)cg::this_cluster().block_rank() : 0;
+  const bool active = st[sys * 4 + 2] == 1.0;  // uniform over the cluster
+  if (!active) return;
+  const long long per = (n + C - 1) / C;
+  const long long lo = rank * per, hi = min(n, lo + per);
+  cplx* x = X + sys * n;
+  cplx* r = R + sys * n;
+  cplx* d = D + sys * n;
+  const cplx* ad = AD + sys * ad_ls;
+  const double b2 = ridge ? beta_sq[sys * beta_bs] : 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto csum = [&](double v, int slot) -> double {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) wsum[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < CGC_T / 32; ++w) t += wsum[w];
+      part[slot] = t;
+    }
+    double tot;
+    if constexpr (C > 1) {
+      cg::cluster_group cl = cg::this_cluster();
+      cl.sync();
+      tot = 0.0;
+      for (int q = 0; q < C; ++q) tot += cl.map_shared_rank(part, q)[slot];
+    } else {
+      __syncthreads();
+      tot = part[slot];
+    }
+    return tot;
+  };
+  double s = 0.0;
+  for (long long i = lo + threadIdx.x; i < hi; i += CGC_T) {
+    const cplx dv = d[i], av = ad[i];
+    s += dv.x * (av.x + b2 * dv.x) + dv.y * (av.y + b2 * dv.y);
+  }
+  const double dad = csum(s, 0);
+  const double rho = st[sys * 4 + 0];
+  const double alpha = rho / dad;
+  s = 0.0;
+  for (long long i = lo + threadIdx.x; i < hi; i += CGC_T) {
+    const cplx dv = d[i], av = ad[i];
+    const cplx adv = cmk(av.x + b2 * dv.x, av.y + b2 * dv.y);
+    x[i] = cmk(x[i].x + alpha * dv.x, x[i].y + alpha * dv.y);
+    const cplx rv = cmk(r[i].x - alpha * adv.x, r[i].y - alpha * adv.y);
+    r[i] = rv;
+    s += cabs2(rv);
+  }
+  const double rho_next = csum(s, 1);
+  const bool stop = sqrt(rho_next) <= tol * st[sys * 4 + 1];
+  if (!stop) {
+    const double beta = rho_next / rho;
+    for (long long i = lo + threadIdx.x; i < hi; i += CGC_T) {
+      const cplx rv = r[i], dv = d[i];
+      d[i] = cmk(rv.x + beta * dv.x, rv.y + beta * dv.y);
+    }
+  }
+  if constexpr (C > 1) cg::this_cluster().sync();  // all ranks read st / the partials before rank 0 writes
+  else __syncthreads();
+  if (rank == 0 && threadIdx.x == 0) {
+    it[sys] += 1;
+    st[sys * 4 + 0] = rho_next;
+    if (stop) st[sys * 4 + 2] = 0.0;
+  }
+}
+
+template <int C>
+int launch_cg_cl(cplx* X, cplx* R, cplx* D, const cplx* AD, long long ad_ls, const double* beta_sq,
+                 long long beta_bs, int ridge, long long n, double tol, double* st, int* it, long long nsys,
+                 cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(C * nsys));
+  cfg.blockDim = dim3(CGC_T);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = C > 1 ? 1 : 0;
+  TrKTimer _kt(TRK_NORMAL, s);
+  TR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, cg_update_cl_kernel<C>, X, R, D, AD, ad_ls, beta_sq, beta_bs, ridge, n,
+                                   tol, st, it));
+  return 0;
+}
+
 __global__ void cg_active_kernel(const double* st, long long nsys, int* any) {
   long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int a = (s < nsys && st[s * 4 + 2] == 1.0) ? 1 : 0;
@@ -170,11 +273,18 @@ int launch_cg_init(cplx* X, cplx* R, cplx* D, const cplx* Y, long long n, double
 int launch_cg_update(cplx* X, cplx* R, cplx* D, const cplx* AD, const double* beta_sq, long long beta_bs,
                      int ridge, long long n, double tol, double* st, int* it, long long nsys, cudaStream_t s,
                      long long ad_ls) {
-  {
+  // CTAs per system from n alone (the reduction order must not depend on the batch)
+  const long long ls = ad_ls > 0 ? ad_ls : n;
+  const long long c = n / 4096;
+  int rc = 0;
+  if (c >= 8) rc = launch_cg_cl<8>(X, R, D, AD, ls, beta_sq, beta_bs, ridge, n, tol, st, it, nsys, s);
+  else if (c >= 4) rc = launch_cg_cl<4>(X, R, D, AD, ls, beta_sq, beta_bs, ridge, n, tol, st, it, nsys, s);
+  else if (c >= 2) rc = launch_cg_cl<2>(X, R, D, AD, ls, beta_sq, beta_bs, ridge, n, tol, st, it, nsys, s);
+  else {  // one 1024-thread CTA per system
     TrKTimer _kt(TRK_NORMAL, s);
-    cg_update_kernel<<<(unsigned)nsys, CGT, 0, s>>>(X, R, D, AD, ad_ls > 0 ? ad_ls : n, beta_sq, beta_bs, ridge, n,
-                                                    tol, st, it);
+    cg_update_kernel<<<(unsigned)nsys, CGT, 0, s>>>(X, R, D, AD, ls, beta_sq, beta_bs, ridge, n, tol, st, it);
   }
+  if (rc) return rc;
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
