@@ -54,6 +54,11 @@ int launch_twist_fold(cplx* G, const cplx* B, long long b_sys, long long b_cap, 
 int launch_apply_update(cplx* W, long long w_sys, const cplx* G, int rows, int P, long long o0,
                         long long o1, int noff, long long stride, long long cnt, long long nsys,
                         cudaStream_t st);
+// the three steps above in one launch for cosets of at most update_small_max() nodes
+int update_small_max();
+int launch_update_small(cplx* W, long long w_sys, const cplx* B, long long b_sys, long long b_cap, long long L,
+                        int P, long long o0, long long o1, int noff, long long stride, long long cnt, long long N,
+                        int rows, const cplx* twN, long long nsys, cudaStream_t st);
 // FA[sys][f] <- FA[sys][f] @ FB[sys][f]  (P x P per frequency f < R)
 int launch_pointwise_matmul(cplx* FA, const cplx* FB, int P, long long R, long long nsys,
                             cudaStream_t st);
