@@ -406,3 +406,24 @@ def test_direct_refinement_path(gpu, name):
     ex = d["x_exact"]
     ra, rb = rel(a, ex), rel(b, ex)
     assert ra < 1e-11 and rb < 1e-11, (ra, rb)
+
+
+def test_run_accuracy_matches_reference(gpu):
+    """GPU run_accuracy on the reference's seeded cells: same rows, errors at
+    least as small as the reference's (refinement) and tiny in absolute terms."""
+    import json
+    from paper_1302_6945_b200 import experiments as ex
+    g = json.load(open(os.path.join(GOLDEN, "stages", "experiments.json")))
+    rows = ex.run_accuracy(ex.ExperimentConfig(sizes=(16, 32), trials=2, seed=2024))
+    assert [(r["variant"], r["n"]) for r in rows] == [(r["variant"], r["n"]) for r in g["accuracy"]]
+    for ours, ref in zip(rows, g["accuracy"]):
+        assert ours["max_err"] <= max(ref["max_err"], 1e-12), (ours, ref)
+
+
+def test_run_cg_equivalence_and_complexity_rows(gpu):
+    from paper_1302_6945_b200 import experiments as ex
+    cfg = ex.ExperimentConfig(variants=("l2",), sizes=(64, 128), trials=1)
+    rows = ex.run_cg_equivalence(cfg)
+    assert len(rows) == 2 and all(r["mean_iters"] >= 1 and r["direct_max_err"] < 1e-9 for r in rows)
+    rows, fits = ex.run_complexity(cfg)
+    assert len(rows) == 2 and rows[0]["params"] == 127 and "l2" in fits

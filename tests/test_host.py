@@ -79,3 +79,24 @@ def test_json_formats_roundtrip_like_the_reference():
     v = np.array([1.0 - 1j, 2.0, 1e-300j])
     assert np.array_equal(tb.vector_from_json(json.dumps(tb.vector_to_json(v))), v)
     assert np.array_equal(tb.vector_from_json({"re": [1.0, 2.0]}), np.array([1.0, 2.0], dtype=complex))
+
+
+def test_experiment_drivers_host_parts_match_reference():
+    """Seeded streams, generators and the complexity fit of the experiment
+    drivers against the reference (tests/golden/make_golden_experiments.py)."""
+    import json
+    import os
+    import numpy as np
+    from paper_1302_6945_b200 import experiments as ex
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "stages", "experiments.json")))
+    for variant in ex.VARIANTS:
+        rng = ex._trial_rng(2024, "accuracy", variant, 16, 1)
+        p = ex.random_problem(variant, 16, rng)
+        x = ex.complex_normal(rng, 16)
+        parts = [p.T.gen if p.T is not None else np.zeros(0), p.L.gen if p.L is not None else np.zeros(0),
+                 p.G.gen if p.G is not None else np.zeros(0), p.b if p.b is not None else np.zeros(0), x]
+        assert float(np.abs(np.concatenate([np.ravel(q) for q in parts])).sum()) == g["draws"][variant][0]
+        assert (float(abs(p.beta)) if p.beta is not None else 0.0) == g["draws"][variant][1]
+    fit = ex.fit_complexity([256, 512, 1024, 2048], [0.011, 0.026, 0.060, 0.135])
+    assert np.allclose([fit.c1, fit.c2, fit.r_squared], g["fit"], rtol=1e-12, atol=0)
+    assert {v: ex.free_parameters(v, 100) for v in ex.VARIANTS} == g["free_parameters"]
