@@ -180,6 +180,9 @@ int tr_kernel_stats(int32_t cls, double* total_ms, int64_t* launches);
  * (minimal HBM traffic and useful FP64 flops, SURVEY 8(d) counting). */
 int tr_kernel_work_stats(int32_t cls, double* alg_bytes, double* alg_flops);
 int tr_fp64_peak(double* tflops);
+/* FFT device time by (length, lines) while timing was enabled, largest
+ * first: rows[3k..3k+2] = {n, lines, launches}, ms[k]; returns the count. */
+int tr_fft_breakdown(int64_t* rows, double* ms, int cap);
 
 /* Last error message of the calling thread. */
 const char* tr_last_error(void);
