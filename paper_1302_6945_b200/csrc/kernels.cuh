@@ -59,12 +59,17 @@ int update_small_max();
 int launch_update_small(cplx* W, long long w_sys, const cplx* B, long long b_sys, long long b_cap, long long L,
                         int P, long long o0, long long o1, int noff, long long stride, long long cnt, long long N,
                         int rows, const cplx* twN, long long nsys, cudaStream_t st);
+// wrapped product (transform length R = La + Lb - 2): F[e][0] -= R T_e, F[e][R] = R T_e with
+// T = A[:, :, La-1] B[:, :, Lb-1]; F lines of stride Rs = R + 1
+int launch_wrap_fix(cplx* F, long long Rs, long long R, const cplx* A, long long a_cap, long long La,
+                    const cplx* B, long long b_cap, long long Lb, int P, long long nsys, cudaStream_t st);
 // FA[sys][f] <- FA[sys][f] @ FB[sys][f]  (P x P per frequency f < R)
 int launch_pointwise_matmul(cplx* FA, const cplx* FB, int P, long long R, long long nsys,
                             cudaStream_t st);
 struct TrimArgs {
-  const cplx* F;       // [sys][PP][R] unnormalised product (x R)
-  long long R;
+  const cplx* F;       // [sys][PP][Rs] unnormalised product (x R)
+  long long R;         // transform length (the product's scale)
+  long long Rs = 0;    // line stride of F (0: R)
   long long L;         // untrimmed product length (<= R)
   int P;
   double* prof;        // [sys][L] scratch

@@ -237,6 +237,7 @@ struct Op {
   long long stride = 1;
   int slot_out = -1, slot_a = -1, slot_b = -1;
   long long cap_a = 0, cap_b = 0, cap_out = 0, R = 0;
+  int wrap = 0;  // combine: R = La + Lb - 2, the top coefficient folded onto index 0 and corrected
   int K = 0, count = 0, M = 0, depth = 0;
   int dbound = 0;  // leaf: structural basis degree under water-filling, no deferrals
   int nattempts = 1;
@@ -432,7 +433,24 @@ struct Builder {
     long long full = ca + cb - 1;
     cm.cap_out = std::min(bound + TRIM_SLACK, full);
     cm.R = fft_good_len(full);
-    pl.Rmax = std::max(pl.Rmax, cm.R);
+    // product lengths 2^k + 1 (equal-tau columns) would need a transform past
+    // 2^(k+1): transform at La + Lb - 2 instead when that length is cheaper and
+    // correct the single wrapped coefficient (wrap_fix_kernel)
+    static const bool wrap_ok = [] {
+      const char* e = getenv("TR_WRAP");
+      return !(e && e[0] == '0');
+    }();
+    if (wrap_ok && full >= 3 && ca >= 2 && cb >= 2) {
+      const long long rw = fft_good_len(full - 1);
+      if (rw < cm.R) {
+        cm.R = rw;
+        cm.wrap = 1;
+      }
+    }
+    pl.Rmax = std::max(pl.Rmax, cm.R + cm.wrap);
+    if (getenv("TR_PLAN_DEBUG"))
+      fprintf(stderr, "combine depth %d: La %lld Lb %lld -> %lld, R %lld%s\n", depth, ca, cb, cm.cap_out, cm.R,
+              cm.wrap ? " (wrapped)" : "");
     pl.Lmax = std::max(pl.Lmax, full);
     pl.ops.push_back(cm);
     pl.slot_cap[slot] = std::max(pl.slot_cap[slot], cm.cap_out);
@@ -940,10 +958,21 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
         TR_TRY(fft_exec(fp, w.slot[op.slot_a] + s0 * PP * ca, ca, op.cap_a, w.S1, R, w.S3, ns * PP, -1, st));
         TR_TRY(fft_exec(fp, w.slot[op.slot_b] + s0 * PP * cb, cb, op.cap_b, w.S2, R, w.S3, ns * PP, -1, st));
         TR_TRY(launch_pointwise_matmul(w.S1, w.S2, P, R, ns, st));
-        TR_TRY(fft_exec(fp, w.S1, R, R, w.S1, R, w.S3, ns * PP, +1, st));
+        const cplx* prod = w.S1;
+        long long Rs = R;
+        if (op.wrap) {  // lines of R + 1: the coefficient at index R is the product of the top ones
+          Rs = R + 1;
+          TR_TRY(fft_exec(fp, w.S1, R, R, w.S2, Rs, w.S3, ns * PP, +1, st));
+          TR_TRY(launch_wrap_fix(w.S2, Rs, R, w.slot[op.slot_a] + s0 * PP * ca, ca, op.cap_a,
+                                 w.slot[op.slot_b] + s0 * PP * cb, cb, op.cap_b, P, ns, st));
+          prod = w.S2;
+        } else {
+          TR_TRY(fft_exec(fp, w.S1, R, R, w.S1, R, w.S3, ns * PP, +1, st));
+        }
         TrimArgs ta;
-        ta.F = w.S1;
+        ta.F = prod;
         ta.R = R;
+        ta.Rs = Rs;
         ta.L = op.cap_a + op.cap_b - 1;
         ta.P = P;
         ta.prof = w.prof;

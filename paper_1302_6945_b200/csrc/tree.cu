@@ -292,7 +292,8 @@ __global__ void __launch_bounds__(TC) trim_cl_kernel(TrimArgs a) {
   const int rank = C > 1 ? (int)cg::this_cluster().block_rank() : 0;
   const long long sys = blockIdx.x / C;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const cplx* F = a.F + sys * PP * a.R;
+  const long long Rs = a.Rs > 0 ? a.Rs : a.R;
+  const cplx* F = a.F + sys * PP * Rs;
   double* prof = a.prof + sys * a.L;
   const long long per = (a.L + C - 1) / C;
   const long long lo = rank * per, hi = min(a.L, lo + per);
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(TC) trim_cl_kernel(TrimArgs a) {
     for (int i = 0; i < P; ++i)
 #pragma unroll
       for (int j = 0; j < P; ++j) {
-        const double q = cabs2(F[(long long)(i * P + j) * a.R + l]);
+        const double q = cabs2(F[(long long)(i * P + j) * Rs + l]);
         m = fmax(m, q);
         v[2 + j] = fmax(v[2 + j], q);
       }
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(TC) trim_cl_kernel(TrimArgs a) {
 #pragma unroll
       for (int j = 0; j < P; ++j)
 #pragma unroll
-        for (int i = 0; i < P; ++i) w[j] = fmax(w[j], cabs2(F[(long long)(i * P + j) * a.R + l]));
+        for (int i = 0; i < P; ++i) w[j] = fmax(w[j], cabs2(F[(long long)(i * P + j) * Rs + l]));
     reduce(w, P);
 #pragma unroll
     for (int j = 0; j < P; ++j) cm2[j] = glob[j];
@@ -383,7 +384,7 @@ __global__ void __launch_bounds__(TC) trim_cl_kernel(TrimArgs a) {
         cplx val = cmk(0.0, 0.0);
         if (l < lw) {
           const double safe = cm[j] > 0.0 ? cm[j] : 1.0;
-          const cplx f = F[(long long)(i * P + j) * a.R + l];
+          const cplx f = F[(long long)(i * P + j) * Rs + l];
           val = cmk(f.x / safe, f.y / safe);
         }
         o[(long long)(i * P + j) * a.cap + l] = val;
@@ -545,6 +546,35 @@ int launch_update_small(cplx* W, long long w_sys, const cplx* B, long long b_sys
   return 0;
 }
 
+namespace {
+template <int P>
+__global__ void wrap_fix_kernel(cplx* F, long long Rs, long long R, const cplx* A, long long a_cap, long long La,
+                                const cplx* B, long long b_cap, long long Lb) {
+  const long long sys = blockIdx.x;
+  const int e = threadIdx.x;
+  if (e >= P * P) return;
+  const int i = e / P, j = e - i * P;
+  const cplx* a = A + sys * P * P * a_cap;
+  const cplx* b = B + sys * P * P * b_cap;
+  cplx t = cmk(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < P; ++k) t = cfma(a[(i * P + k) * a_cap + La - 1], b[(k * P + j) * b_cap + Lb - 1], t);
+  t = cscale(t, (double)R);  // the inverse transform is unnormalised
+  cplx* f = F + (sys * P * P + e) * Rs;
+  f[0] = csub(f[0], t);
+  f[R] = t;
+}
+}  // namespace
+
+int launch_wrap_fix(cplx* F, long long Rs, long long R, const cplx* A, long long a_cap, long long La,
+                    const cplx* B, long long b_cap, long long Lb, int P, long long nsys, cudaStream_t st) {
+  TrKTimer _kt(TRK_COMBINE, st);
+  if (P == 5) wrap_fix_kernel<5><<<(unsigned)nsys, 32, 0, st>>>(F, Rs, R, A, a_cap, La, B, b_cap, Lb);
+  else wrap_fix_kernel<7><<<(unsigned)nsys, 64, 0, st>>>(F, Rs, R, A, a_cap, La, B, b_cap, Lb);
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
 int launch_twist_fold(cplx* G, const cplx* B, long long b_sys, long long b_cap, int PP, long long L,
                       long long o0, long long o1, int noff, long long cnt, long long N,
                       const cplx* twN, long long nsys, cudaStream_t st) {
@@ -584,7 +614,7 @@ int launch_pointwise_matmul(cplx* FA, const cplx* FB, int P, long long R, long l
 int launch_trim_normalize(const TrimArgs& a, long long nsys, cudaStream_t st) {
   tr_kernel_work(TRK_COMBINE, 16.0 * nsys * a.P * a.P * (double)(a.L + a.cap), 0.0);
   static const char* tv = getenv("TR_TRIM");  // TR_TRIM=old: one CTA per system / four kernels
-  if (!(tv && tv[0] == 'o')) {
+  if (!(tv && tv[0] == 'o') || (a.Rs > 0 && a.Rs != a.R)) {
     const int rc = a.P == 5 ? dispatch_trim_cl<5>(a, nsys, st) : dispatch_trim_cl<7>(a, nsys, st);
     if (rc) return rc;
     TR_CUDA_CHECK(cudaGetLastError());
