@@ -144,6 +144,16 @@ __global__ void cg_restore_kernel(cplx* X, const cplx* X0, const double* st, lon
   X[sys * n + i] = X0[sys * n + i];
 }
 
+// x += d where the refinement solve succeeded (status 0) and, after CG, for
+// systems CG did not converge on
+__global__ void refine_apply_kernel(cplx* X, const cplx* D, const int* status, const double* st, long long n) {
+  const long long sys = blockIdx.y;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n || status[sys] != 0 || (st && st[sys * 4 + 2] == 0.0)) return;
+  const long long o = sys * n + i;
+  X[o] = cadd(X[o], D[o]);
+}
+
 // x += d for systems CG did not converge on
 __global__ void add_masked_kernel(cplx* X, const cplx* D, const double* st, long long n) {
   const long long sys = blockIdx.y;
@@ -319,6 +329,14 @@ int launch_cg_restore(cplx* X, const cplx* X0, const double* st, long long n, lo
 int launch_add_masked(cplx* X, const cplx* D, const double* st, long long n, long long nsys, cudaStream_t s) {
   dim3 g((unsigned)((n + 255) / 256), (unsigned)nsys);
   { TrKTimer _kt(TRK_FINISH, s); add_masked_kernel<<<g, 256, 0, s>>>(X, D, st, n); }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int launch_refine_apply(cplx* X, const cplx* D, const int* status, const double* st, long long n, long long nsys,
+                        cudaStream_t s) {
+  dim3 g((unsigned)((n + 255) / 256), (unsigned)nsys);
+  { TrKTimer _kt(TRK_FINISH, s); refine_apply_kernel<<<g, 256, 0, s>>>(X, D, status, st, n); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }

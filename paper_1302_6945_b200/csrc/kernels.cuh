@@ -137,3 +137,5 @@ int launch_nudft_forward(const double* f, const cplx* x, long long K, long long 
 int launch_cg_check(double* st, const int* it, long long nsys, int cap, cudaStream_t s);
 int launch_cg_restore(cplx* X, const cplx* X0, const double* st, long long n, long long nsys, cudaStream_t s);
 int launch_add_masked(cplx* X, const cplx* D, const double* st, long long n, long long nsys, cudaStream_t s);
+int launch_refine_apply(cplx* X, const cplx* D, const int* status, const double* st, long long n, long long nsys,
+                        cudaStream_t s);

@@ -574,6 +574,8 @@ struct WS {
   double* prof;
   unsigned long long* red;
   int *cd, *dcount, *retried, *status, *trim_over, *blen, *cgit;
+  int* diag_save;        // [5][nsys] + [8 nsys]: the direct solve's ledger/diagnostics across a refinement
+  double* scale_save;    // [nsys]
   int2* defer;
   double *max_scale, *partial, *nrm, *res_out;
   int* len_out;
@@ -618,6 +620,8 @@ size_t layout(const Plan& p, long long nsys, char* base, WS* w) {
   w->trim_over = c.take<int>((size_t)nsys);
   w->blen = c.take<int>((size_t)nsys);
   w->cgit = c.take<int>((size_t)nsys);
+  w->diag_save = c.take<int>((size_t)nsys * 12);
+  w->scale_save = c.take<double>((size_t)nsys);
   w->len_out = c.take<int>((size_t)nsys);
   w->defer = c.take<int2>((size_t)nsys * DMAX);
   w->max_scale = c.take<double>((size_t)nsys);
@@ -1093,12 +1097,28 @@ int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
   if (phase == PH_REFINE || phase == PH_REFINE_CG) {
     // r = y - A x ; solve A d = r ; x += d   (after CG: only the systems CG
     // did not converge on, restarting from their direct solution)
+    // The report describes the direct solve (the reference's single pass):
+    // its ledger and diagnostics are kept across the refinement solve, and a
+    // refinement solve that fails (singular residual problem) leaves x as is.
     if (phase == PH_REFINE_CG) TR_TRY(launch_cg_restore(w.X, w.X0, cst, n, nsys, st));
+    int* sv = w.diag_save;
+    const size_t ib = sizeof(int) * nsys;
+    TR_CUDA_CHECK(cudaMemcpyAsync(sv, w.cd, 8 * ib, cudaMemcpyDeviceToDevice, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(sv + 8 * nsys, w.dcount, ib, cudaMemcpyDeviceToDevice, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(sv + 9 * nsys, w.retried, ib, cudaMemcpyDeviceToDevice, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(sv + 10 * nsys, w.status, ib, cudaMemcpyDeviceToDevice, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(sv + 11 * nsys, w.trim_over, ib, cudaMemcpyDeviceToDevice, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(w.scale_save, w.max_scale, sizeof(double) * nsys, cudaMemcpyDeviceToDevice, st));
     TR_TRY(normal_apply(p, nsys, w, sbs, w.X, st));
     TR_TRY(launch_residual(w.Rv, w.AX, w.X, w.Y, n, in.beta_sq, in.beta_bs, add_ridge, nsys, st));
     TR_TRY(solve_core(p, in, nsys, w, w.Rv, w.X2, st));
-    if (phase == PH_REFINE_CG) TR_TRY(launch_add_masked(w.X, w.X2, cst, n, nsys, st));
-    else TR_TRY(launch_add_inplace(w.X, w.X2, n, nsys, st));
+    TR_TRY(launch_refine_apply(w.X, w.X2, w.status, phase == PH_REFINE_CG ? cst : nullptr, n, nsys, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(w.cd, sv, 8 * ib, cudaMemcpyDeviceToDevice, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(w.dcount, sv + 8 * nsys, ib, cudaMemcpyDeviceToDevice, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(w.retried, sv + 9 * nsys, ib, cudaMemcpyDeviceToDevice, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(w.status, sv + 10 * nsys, ib, cudaMemcpyDeviceToDevice, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(w.trim_over, sv + 11 * nsys, ib, cudaMemcpyDeviceToDevice, st));
+    TR_CUDA_CHECK(cudaMemcpyAsync(w.max_scale, w.scale_save, sizeof(double) * nsys, cudaMemcpyDeviceToDevice, st));
     return 0;
   }
   // residual for the report (ref solver.py:72-75)
