@@ -13,6 +13,8 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtoepreg_b200.so")
+# TR_LIB_PATH: load an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("TR_LIB_PATH", LIB_PATH)
 
 VARIANTS = {"general": 0, "l2": 1, "gramian": 2}
 FILLS = {"auto": 0, "zero": 1, "echo": 2}
