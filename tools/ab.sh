@@ -1,4 +1,6 @@
-TAG=default python tools/c4_check.py 2>&1 | grep refine
-TAG=wrap0 TR_WRAP=0 python tools/c4_check.py 2>&1 | grep refine
-TAG=f3off TR_F3=0 python tools/c4_check.py 2>&1 | grep refine
-TAG=exact TR_LEAF_MODE=exact python tools/c4_check.py 2>&1 | grep refine
+timeout 600 python -m pytest tests -m gpu -q 2>&1 | tail -1
+python tools/fft_compare.py 8192 16384 32768 65536 4608 9216 18432 12288 2>&1 | tail -9
+for c in "" "--config c5 --batch 256"; do
+  python bench.py --steps 5 --no-cpu-baseline $c | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['config'], 'solves/s %.1f'%d['value'])"
+done
