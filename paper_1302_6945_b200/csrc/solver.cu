@@ -933,6 +933,8 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
         }
       }
     } else if (op.kind == OP_UPDATE) {
+      static const bool skip_u = getenv("TR_DIAG_SKIP_UPDATES") != nullptr;  // timing diagnostic only (wrong x)
+      if (skip_u) continue;
       long long cnt = N / op.stride;
       long long scap = p.slot_cap[op.slot_a];
       if (cnt <= update_small_max()) {
@@ -951,6 +953,8 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
                                    cnt, ns, st));
       }
     } else {
+      static const bool skip_c = getenv("TR_DIAG_SKIP_COMBINES") != nullptr;  // timing diagnostic only (wrong x)
+      if (skip_c) continue;
       long long R = op.R;
       long long ca = p.slot_cap[op.slot_a], cb = p.slot_cap[op.slot_b];
       const FftPlan& fp = F(p, R);
