@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round profile artifacts for tag $R: bench lines (no profiler), ncu launch
 # list of the default bench (timed region), --set full captures of the top kernels.
-R=${R:-s3}
+R=${R:-s4}
 O=gpurun_out/$R
 mkdir -p $O
 python bench.py > $O/bench_c2.json 2> $O/bench_c2.err || exit 1
