@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(CGT) cg_warm_kernel(const cplx* X, cplx* R, cp
   __shared__ double sh[CGT / 32];
   const long long sys = blockIdx.x;
   const double b2 = ridge ? beta_sq[sys * beta_bs] : 0.0;
-  double s = 0.0;
+  double s = 0.0, sy = 0.0;
   for (long long i = threadIdx.x; i < n; i += CGT) {
     const long long o = sys * n + i;
     const cplx x = X[o], ax = AX[o], y = Y[o];
@@ -109,10 +109,14 @@ __global__ void __launch_bounds__(CGT) cg_warm_kernel(const cplx* X, cplx* R, cp
     R[o] = r;
     D[o] = r;
     s += cabs2(r);
+    sy += cabs2(y);
   }
   s = blk_sum(s, sh);
+  sy = blk_sum(sy, sh);
   if (threadIdx.x == 0) {
-    const double target = 1e-8 * sqrt(s);
+    // 1e-8 of the initial residual, but not below the FP64 floor of the
+    // residual itself (~1e-15 |y|): iterations past it no longer improve x
+    const double target = fmax(1e-8 * sqrt(s), 1e-15 * sqrt(sy));
     st[sys * 4 + 0] = s;
     st[sys * 4 + 1] = target;
     st[sys * 4 + 2] = sqrt(s) > target;

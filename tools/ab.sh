@@ -1,3 +1,6 @@
-for v in "X=1" "TR_DIAG_SKIP_UPDATES=1" "TR_DIAG_SKIP_COMBINES=1" "TR_DIAG_SKIP_UPDATES=1 TR_DIAG_SKIP_COMBINES=1"; do
-  echo "$v"; env $v TR_PHASE_TIMES=1 REFINE=0 python tools/ab_check.py c2 64 /tmp/a.npz 2>&1 | grep phases | tail -1
+timeout 600 python -m pytest tests -m gpu -q 2>&1 | tail -1
+python tools/cg_iterations.py 2>&1 | tail -5
+for c in "" "--config c5 --batch 256"; do
+  python bench.py --steps 5 --no-cpu-baseline $c | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['config'], 'solves/s %.1f'%d['value'])"
 done

@@ -9,7 +9,7 @@ CLASS = [("leaf_fused", "leaf_pivot"), ("leaf_chain", "leaf_pivot"), ("leaf_pivo
          ("cg_", "normal"), ("spec_mul", "normal"), ("mask_scale", "normal"), ("accum", "normal"),
          ("residual", "normal"), ("norm_", "normal"), ("nudft", "assemble"),
          ("leaf_basis", "leaf_build"), ("leaf_build", "leaf_build"), ("leaf_check", "leaf_check"),
-         ("leaf_kernel", "leaf_exact"), ("fft", "fft"), ("trim", "combine"), ("pointwise", "combine"),
+         ("leaf_kernel", "leaf_exact"), ("fft", "fft"), ("trim", "combine"), ("pointwise", "combine"), ("wrap_fix", "combine"),
          ("twist_fold", "update"), ("apply_update", "update"), ("assemble", "assemble"),
          ("emb_col", "assemble"), ("ext_seq", "assemble")]
 
