@@ -1199,7 +1199,7 @@ int batch_groups(long long batch) {
   static const char* e = getenv("TR_GROUPS");
   int g = 1;
   if (e) g = atoi(e);
-  else if (batch >= 32 && batch <= 296) g = 2;  // groups of <= 148: one CTA per SM in the fused leaf
+  else if (batch >= 32) g = (int)((batch + 147) / 148) < 2 ? 2 : (int)((batch + 147) / 148);  // groups of <= 148: the fused leaf
   if (g < 1) g = 1;
   if (g > 4) g = 4;
   if (g > batch) g = (int)batch;
