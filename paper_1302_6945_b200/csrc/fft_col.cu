@@ -155,104 +155,11 @@ __global__ void __launch_bounds__(NTH, 3) fft_col_kernel(ColArgs a) {
   }
 }
 
-// Persistent, software-pipelined variant: a CTA loops over tiles and the
-// next tile's inputs stream into a second shared-memory buffer by cp.async
-// (16 B per copy, zero fill past in_len) while the current tile is
-// transformed, so the HBM latency hides behind the butterflies instead of
-// needing more resident CTAs.  Same math and output layout as fft_col_kernel.
-TR_D void cp_async16(void* dst, const void* src, bool valid) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  const int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
-}
-TR_D void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-TR_D void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-template <int LOG2, int Q, bool PASSA, int TLX>
-__global__ void __launch_bounds__(NTH, 2) fft_col_pipe_kernel(ColArgs a, long long ntiles) {
-  using G = CPlan<LOG2, Q, TLX>;
-  constexpr int TL = G::TL, R = G::R, TR = TL * R;
-  extern __shared__ __align__(16) unsigned char fsm[];
-  cplx* tile = reinterpret_cast<cplx*>(fsm);
-  cplx* stg = tile + (size_t)TL * G::LS;  // [2][R][TL]
-  const int sl = threadIdx.x % TL, tb = threadIdx.x / TL;
-  auto prefetch = [&](long long t, cplx* dst) {
-    const long long sub0 = t * TL;
-    const long long line = sub0 / a.subs;
-    const int s0 = (int)(sub0 - line * a.subs);
-    const cplx* src = a.in + line * a.in_ls;
-    for (int idx = threadIdx.x; idx < TR; idx += NTH) {
-      const int e = idx / TL;  // idx % TL == sl (TL divides NTH)
-      const long long gi = s0 + sl + (long long)e * a.in_es;
-      const bool ok = gi < a.in_len;
-      cp_async16(dst + idx, ok ? (const void*)(src + gi) : (const void*)a.in, ok);
-    }
-  };
-  int buf = 0;
-  if (blockIdx.x < ntiles) prefetch(blockIdx.x, stg);
-  cp_commit();
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const long long tn = t + gridDim.x;
-    if (tn < ntiles) prefetch(tn, stg + (size_t)(buf ^ 1) * TR);
-    cp_commit();
-    cp_wait1();
-    __syncthreads();
-    const long long sub0 = t * TL;
-    const long long line = sub0 / a.subs;
-    const int s0 = (int)(sub0 - line * a.subs);
-    const long long lin = line * a.in_ls, lout = line * a.out_ls;
-    const cplx* mrow = (PASSA && a.mul) ? a.mul + line * a.mul_ls : nullptr;
-    col_stage<LOG2, Q, PASSA, 0, TLX>(tile + (size_t)sl * G::LS, a, lin, lout, s0 + sl, true, tb, mrow,
-                                      stg + (size_t)buf * TR);
-    if constexpr (PASSA) {
-      __syncthreads();
-      for (int e = threadIdx.x; e < TR; e += NTH) {
-        const int tt = e / R, k = e - tt * R;
-        a.out[lout + (long long)(s0 + tt) * R + k] = tile[(size_t)tt * G::LS + k];
-      }
-    }
-    __syncthreads();
-    buf ^= 1;
-  }
-}
-
-template <int LOG2, int Q, bool PASSA, int TLX>
-int launch_pipe(const ColArgs& a, cudaStream_t st) {
-  using G = CPlan<LOG2, Q, TLX>;
-  if (a.subs % G::TL) return -1;
-  const size_t smem = sizeof(cplx) * ((size_t)G::TL * G::LS + 2 * (size_t)G::TL * G::R);
-  static int ctas = 0;
-  if (!ctas) {
-    cudaFuncSetAttribute(fft_col_pipe_kernel<LOG2, Q, PASSA, TLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    int per = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fft_col_pipe_kernel<LOG2, Q, PASSA, TLX>, NTH, smem);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    ctas = (per > 0 ? per : 1) * sms;
-  }
-  const long long ntiles = a.lines * a.subs / G::TL;
-  const long long grid = ntiles < ctas ? ntiles : ctas;
-  TrKTimer _kt(TRK_FFT, st);
-  fft_col_pipe_kernel<LOG2, Q, PASSA, TLX><<<(unsigned)grid, NTH, smem, st>>>(a, ntiles);
-  return 0;
-}
-
 template <int LOG2, int Q, bool PASSA>
 int launch(const ColArgs& a, cudaStream_t st) {
   if constexpr ((Q << LOG2) > 1024 || (Q << LOG2) < 2) {
     return -1;
   } else {
-    // TR_FFT_PIPE=1: persistent cp.async-pipelined variant (measured slower
-    // at the solver's shapes than more resident CTAs; kept as an option)
-    static const bool pipe = [] {
-      const char* e = getenv("TR_FFT_PIPE");
-      return e && e[0] == '1';
-    }();
-    if constexpr ((Q << LOG2) <= 128 && (Q << LOG2) >= 16) {
-      if (pipe) return launch_pipe<LOG2, Q, PASSA, 0>(a, st);
-    }
     using G = CPlan<LOG2, Q>;
     if (a.subs % G::TL) return -1;
     const size_t smem = sizeof(cplx) * (size_t)G::TL * G::LS;

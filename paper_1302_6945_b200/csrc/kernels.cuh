@@ -54,11 +54,6 @@ int launch_twist_fold(cplx* G, const cplx* B, long long b_sys, long long b_cap, 
 int launch_apply_update(cplx* W, long long w_sys, const cplx* G, int rows, int P, long long o0,
                         long long o1, int noff, long long stride, long long cnt, long long nsys,
                         cudaStream_t st);
-// the three steps above in one launch for cosets of at most update_small_max() nodes
-int update_small_max();
-int launch_update_small(cplx* W, long long w_sys, const cplx* B, long long b_sys, long long b_cap, long long L,
-                        int P, long long o0, long long o1, int noff, long long stride, long long cnt, long long N,
-                        int rows, const cplx* twN, long long nsys, cudaStream_t st);
 // wrapped product (transform length R = La + Lb - 2): F[e][0] -= R T_e, F[e][R] = R T_e with
 // T = A[:, :, La-1] B[:, :, Lb-1]; F lines of stride Rs = R + 1
 int launch_wrap_fix(cplx* F, long long Rs, long long R, const cplx* A, long long a_cap, long long La,

@@ -937,11 +937,6 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
       if (skip_u) continue;
       long long cnt = N / op.stride;
       long long scap = p.slot_cap[op.slot_a];
-      if (cnt <= update_small_max()) {
-        TR_TRY(launch_update_small(w.W, w_sys, w.slot[op.slot_a], PP * scap, scap, op.cap_a, P, op.o0, op.o1,
-                                   op.noff, op.stride, cnt, N, rows, twN, nsys, st));
-        continue;
-      }
       // systems in chunks whose folded values stay in L2 between the three kernels
       const long long cs = l2_chunk(nsys, (long long)op.noff * PP * cnt * 2);
       for (long long s0 = 0; s0 < nsys; s0 += cs) {

@@ -441,112 +441,6 @@ inline dim3 g2(long long n, long long nsys, int th = 256) {
 }  // namespace
 
 namespace {
-// Coset update for small cosets in one launch (ref tanint.py:387-393,
-// fftpoly.py:64-89): one CTA per (coset, system) folds the twisted left
-// basis into shared memory, evaluates it at the coset's cnt nodes by a direct
-// cnt-point DFT (node powers by a recurrence re-anchored from the table
-// every 16 terms) and applies w <- w . B(sigma) to the coset's weight rows.
-// Replaces twist_fold + the cnt-point FFT + apply_update (three launches on
-// the tree's critical path) where cnt is small.
-template <int P>
-__global__ void __launch_bounds__(256) update_small_kernel(cplx* W, long long w_sys, const cplx* B, long long b_sys,
-                                                          long long b_cap, long long L, long long o0, long long o1,
-                                                          long long stride, int cnt, long long N, int rows,
-                                                          const cplx* twN) {
-  constexpr int PP = P * P;
-  extern __shared__ __align__(16) unsigned char usm[];
-  cplx* G = reinterpret_cast<cplx*>(usm);  // [PP][cnt] folded, then evaluated in place via V
-  cplx* V = G + (size_t)PP * cnt;          // [PP][cnt]
-  cplx* wt = V + (size_t)PP * cnt;         // [cnt] omega^q
-  const int c = blockIdx.x;
-  const long long sys = blockIdx.y;
-  const long long oc = c ? o1 : o0;
-  const cplx* src = B + sys * b_sys;
-  for (int q = threadIdx.x; q < cnt; q += blockDim.x) wt[q] = __ldg(&twN[(long long)q * stride]);
-  // fold (same summation order as twist_fold_kernel)
-  for (int e2 = threadIdx.x; e2 < PP * cnt; e2 += blockDim.x) {
-    const int e = e2 / cnt, q = e2 - e * cnt;
-    const cplx* s = src + (long long)e * b_cap;
-    cplx acc = cmk(0.0, 0.0);
-    if (oc == 0) {
-      for (long long l = q; l < L; l += cnt) acc = cadd(acc, s[l]);
-    } else {
-      long long idx = (oc * q) % N;
-      const long long step = (oc * cnt) % N;
-      for (long long l = q; l < L; l += cnt) {
-        acc = cfma(s[l], __ldg(&twN[idx]), acc);
-        idx += step;
-        if (idx >= N) idx -= N;
-      }
-    }
-    G[e2] = acc;
-  }
-  __syncthreads();
-  // V[e][t] = sum_q G[e][q] omega^(q t)
-  for (int e2 = threadIdx.x; e2 < PP * cnt; e2 += blockDim.x) {
-    const int e = e2 / cnt, t = e2 - e * cnt;
-    const cplx* g = G + (size_t)e * cnt;
-    const cplx w1 = wt[t];
-    cplx acc = cmk(0.0, 0.0), w = cmk(1.0, 0.0);
-    int kk = 0;
-    for (int q = 0; q < cnt; ++q) {
-      if ((q & 15) == 0) w = wt[kk];
-      acc = cfma(g[q], w, acc);
-      w = cmul(w, w1);
-      kk += t;
-      if (kk >= cnt) kk -= cnt;
-    }
-    V[e2] = acc;
-  }
-  __syncthreads();
-  // w[r][:] <- w[r][:] . V(t) for the coset's nodes oc + stride t
-  for (int e2 = threadIdx.x; e2 < cnt * rows; e2 += blockDim.x) {
-    const int t = e2 / rows, r = e2 - t * rows;
-    cplx* w = W + sys * w_sys + ((oc + stride * t) * rows + r) * P;
-    cplx old[P];
-#pragma unroll
-    for (int i = 0; i < P; ++i) old[i] = w[i];
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      cplx acc = cmk(0.0, 0.0);
-#pragma unroll
-      for (int i = 0; i < P; ++i) acc = cfma(old[i], V[(size_t)(i * P + k) * cnt + t], acc);
-      w[k] = acc;
-    }
-  }
-}
-}  // namespace
-
-int update_small_max() {
-  static const int m = [] {
-    const char* e = getenv("TR_UPD_SMALL");  // largest coset handled by the fused update (0: off)
-    return e ? atoi(e) : 0;  // measured: no faster than the three launches in a graph
-  }();
-  return m;
-}
-
-int launch_update_small(cplx* W, long long w_sys, const cplx* B, long long b_sys, long long b_cap, long long L,
-                        int P, long long o0, long long o1, int noff, long long stride, long long cnt, long long N,
-                        int rows, const cplx* twN, long long nsys, cudaStream_t st) {
-  const size_t smem = sizeof(cplx) * ((size_t)2 * P * P * cnt + cnt);
-  tr_kernel_work(TRK_UPDATE, 16.0 * nsys * P * P * (double)L + 32.0 * nsys * noff * (double)cnt * rows * P,
-                 8.0 * nsys * noff * P * P * ((double)L + (double)cnt * cnt + (double)cnt * rows * P));
-  dim3 grid((unsigned)noff, (unsigned)nsys);
-  TrKTimer _kt(TRK_UPDATE, st);
-  if (P == 5) {
-    static bool set = false;
-    if (!set) { cudaFuncSetAttribute(update_small_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); set = true; }
-    update_small_kernel<5><<<grid, 256, smem, st>>>(W, w_sys, B, b_sys, b_cap, L, o0, o1, stride, (int)cnt, N, rows, twN);
-  } else {
-    static bool set = false;
-    if (!set) { cudaFuncSetAttribute(update_small_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); set = true; }
-    update_small_kernel<7><<<grid, 256, smem, st>>>(W, w_sys, B, b_sys, b_cap, L, o0, o1, stride, (int)cnt, N, rows, twN);
-  }
-  TR_CUDA_CHECK(cudaGetLastError());
-  return 0;
-}
-
-namespace {
 template <int P>
 __global__ void wrap_fix_kernel(cplx* F, long long Rs, long long R, const cplx* A, long long a_cap, long long La,
                                 const cplx* B, long long b_cap, long long Lb) {
