@@ -16,6 +16,8 @@ Printed JSON (rank 0): the contract keys plus
   roofline     the dominant kernel class: leaf classes FP64-bound against the
                FP64 FMA peak measured by tr_fp64_peak(); FFT / combine /
                update HBM-bound against MEASURED_PEAKS.json hbm_gbs
+  chain        the sequential absorption chain: conditions per
+               solve and the leaf time per absorbed condition
   kernels      per-class device time from CUDA events (separate pass)
   cpu_baseline the oracle port of the reference, timed on this host's cores
   clocks       nvidia-smi samples taken during the timed region
@@ -313,6 +315,21 @@ def main():
     roof["avg_launch_ms"] = ms / max(nl, 1)
     roof["share_of_step"] = ms / tot_k
 
+    # the sequential absorption chain: every condition of a solve passes
+    # through one leaf sweep in order (SURVEY 8(d) chain bound C x t_step);
+    # groups of <= 148 systems (solver.cu batch_groups) run one after the
+    # other in this eager timing pass, their systems in parallel
+    rows = 3 if raw.get("variant", "") == "general" else 2
+    n_cond = rows * info["order"]
+    groups = 1 if count < 32 else min(4, max(2, -(-count // 148)))
+    leaf_ms = sum(kst[k][0] for k in ("leaf_pivot", "leaf_build", "leaf_check", "leaf_exact") if k in kst) / nk
+    leaf_launches = kst.get("leaf_pivot", (0, 0))[1] / nk
+    solves = max(1.0, round(leaf_launches / max(groups * info["leaves"], 1)))
+    chain = {"conditions_per_solve": n_cond, "groups": groups, "direct_solves_per_system": solves,
+             "leaf_ms_per_step": leaf_ms,
+             "ns_per_condition": leaf_ms * 1e6 / (groups * solves * n_cond),
+             "bound": "latency of the pivot chain (one CTA per system and leaf)"}
+
     out = {
         "metric": METRIC,
         "value": value,
@@ -335,6 +352,7 @@ def main():
                 "d2h_bytes_per_step": db.d2h_bytes,
                 "path": "DeviceBatch.stage (pinned H2D) -> run -> x D2H"},
         "roofline": roof,
+        "chain": chain,
         "kernels": {k: {"ms_per_step": v[0] / nk, "launches_per_step": v[1] / nk,
                         "share": v[0] / tot_k,
                         "alg_GBps": v[2] / (v[0] * 1e-3) / 1e9 if v[0] else None,
@@ -374,6 +392,21 @@ def run_reference(args, rank):
         walls.append(wall)
     total = time.perf_counter() - t0
     value = nsolve * args.steps / total
+    # the sequential absorption chain: every condition of a solve passes
+    # through one leaf sweep in order (SURVEY 8(d) chain bound C x t_step);
+    # groups of <= 148 systems (solver.cu batch_groups) run one after the
+    # other in this eager timing pass, their systems in parallel
+    rows = 3 if raw.get("variant", "") == "general" else 2
+    n_cond = rows * info["order"]
+    groups = 1 if count < 32 else min(4, max(2, -(-count // 148)))
+    leaf_ms = sum(kst[k][0] for k in ("leaf_pivot", "leaf_build", "leaf_check", "leaf_exact") if k in kst) / nk
+    leaf_launches = kst.get("leaf_pivot", (0, 0))[1] / nk
+    solves = max(1.0, round(leaf_launches / max(groups * info["leaves"], 1)))
+    chain = {"conditions_per_solve": n_cond, "groups": groups, "direct_solves_per_system": solves,
+             "leaf_ms_per_step": leaf_ms,
+             "ns_per_condition": leaf_ms * 1e6 / (groups * solves * n_cond),
+             "bound": "latency of the pivot chain (one CTA per system and leaf)"}
+
     out = {
         "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
