@@ -57,7 +57,7 @@ constexpr int RESCALE_PERIOD = 8;
 constexpr int NT = 256;  // threads per CTA of both kernels
 constexpr int NW = NT / 32;
 #ifndef TR_SPIN_NS
-#define TR_SPIN_NS 64
+#define TR_SPIN_NS 0  // pure acquire polling measured ~1% better than back-off (16-256 ns)
 #endif
 
 TR_D long long node_of(const LeafArgs& a, int p) {
@@ -96,7 +96,7 @@ TR_D int ld_acquire(const int* p) {
 TR_D int wait_steps(const int* flag, int t, int avail) {
   while (avail <= t) {
     avail = ld_acquire(flag);
-    if (avail <= t) __nanosleep(TR_SPIN_NS);
+    if (TR_SPIN_NS > 0 && avail <= t) __nanosleep(TR_SPIN_NS);
   }
   return avail;
 }
@@ -1693,7 +1693,7 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
         }
       };
       auto hand_over = [&](int b, const cplx (&rr)[P]) {
-        while (ld_acquire(&flag[1]) < b - 1) __nanosleep(TR_SPIN_NS);
+        while (ld_acquire(&flag[1]) < b - 1) if (TR_SPIN_NS > 0) __nanosleep(TR_SPIN_NS);
 #pragma unroll
         for (int i = 0; i < P; ++i) xfer[lane * P + i] = rr[i];
         __syncwarp();

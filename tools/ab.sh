@@ -1,6 +1,8 @@
-timeout 600 python -m pytest tests -m gpu -q 2>&1 | tail -1
-for c in "" "--config c5 --batch 256"; do
-  python bench.py --steps 5 --no-cpu-baseline $c | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['config'], 'solves/s %.1f'%d['value'])"
+for rep in 1 2; do
+for v in s0 s16 s64 s256; do
+ for c in "" "--config c5 --batch 256"; do
+  TR_LIB_PATH=tools/libvar/lib_$v.so python bench.py --steps 5 --no-cpu-baseline $c | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$v', d['config']['config'], 'solves/s %.1f'%d['value'], 'ns/cond %.0f'%d['chain']['ns_per_condition'])"
+ done
 done
-python -c "import __graft_entry__ as g; g.smoke()"
+done
