@@ -113,6 +113,34 @@ def test_shared_operator_batch(gpu):
         assert rel(r.x_hat, x) < 1e-12
 
 
+@pytest.mark.parametrize("count", [40, 300])
+def test_batch_groups_invariant(gpu, count):
+    """Batches split into 2-4 stream groups (>= 32 systems), with the leaf
+    attempts paired in 2-CTA clusters (40: 20 systems per group) and
+    unpaired (300: 3 groups of 100, 200 CTAs > 148 SMs), give bit-identical
+    solutions to one-system solves, and match the dense solution."""
+    tb = gpu
+    raw = wl.c5_random(n=256, count=count, seed=29)
+    probs = [wl.to_problem(raw, tb, i) for i in range(count)]
+    reps = tb.solve_tikhonov_batch(probs)
+    for i in sorted({0, 1, count // 4, count // 2 - 1, count // 2, count - 1}):
+        single = tb.solve_tikhonov(probs[i])
+        assert np.array_equal(reps[i].x_hat, single.x_hat), i
+        assert np.array_equal(reps[i].final_col_degrees, single.final_col_degrees)
+        assert rel(reps[i].x_hat, O.dense_solution(probs[i])) < 1e-10
+
+
+def test_shared_operator_groups(gpu):
+    """Config-2 shape (one T, many right-hand sides) across stream groups."""
+    tb = gpu
+    raw = wl.c2_rect(m=1024, n=512, nrhs=40, seed=8)
+    probs = [wl.to_problem(raw, tb, i) for i in range(40)]
+    reps = tb.solve_tikhonov_batch(probs)
+    for i in (0, 19, 20, 39):
+        assert np.array_equal(reps[i].x_hat, tb.solve_tikhonov(probs[i]).x_hat), i
+        assert rel(reps[i].x_hat, O.dense_solution(probs[i])) < 1e-12
+
+
 @pytest.mark.parametrize("variant", ["general", "l2", "gramian"])
 def test_small_corpus_against_dense(gpu, variant):
     """The reference acceptance gate (ref tests/test_acceptance.py:107-113):
