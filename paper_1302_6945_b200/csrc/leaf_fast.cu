@@ -1800,6 +1800,11 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
     // ---- self-residual (ref tanint.py:262-270): fold + M-point DFT per coset ----
     const int len = min(min(bk.len_try, cap), CAPR);
     double resm = 0.0;
+    int M1 = 1;  // DFT factor M = M1 * M2 (M1 <= M2; 1: direct sums)
+    if (M > 12)
+      for (int d = 2; d * d <= M; ++d)
+        if (M % d == 0) M1 = d;
+    const int M2 = M / M1;
     for (int cs = 0; cs < a.noff; ++cs) {
       const cplx* tw = twl + cs * CAPR;
       for (int e = tid; e < PP * M; e += nt) {
@@ -1816,28 +1821,80 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
       }
       __syncthreads();
       if (tid == 0) tsm[16 + 3 * cs] = clock64();
-      // M-point DFT of every folded entry: the node power w = omega^(q t)
-      // runs as a recurrence (re-anchored from the table every 16 terms), so
-      // the loop reads only the broadcast fold values from shared memory
-      for (int e = tid; e < P * M; e += nt) {
-        const int k = e / M, t = e % M;
-        const cplx* g = gbuf + (size_t)k * P * M;
-        const cplx wt = wtab[t];
-        cplx acc[P];
+      // M-point DFT of every folded entry (omega^e = wtab[e mod M]).  The
+      // check is FP64-throughput-bound, so M = M1 * M2 runs as two passes
+      // of M1- and M2-term sums (Cooley-Tukey, twiddle folded into the first
+      // pass): P^2 M (M1 + M2) instead of P^2 M^2 complex FMAs.  Node powers
+      // run as recurrences re-anchored from the table every 16 terms.
+      const cplx* X = vbuf;  // DFT output [P*P][M]
+      if (M1 > 1) {
+        for (int e = tid; e < P * M; e += nt) {
+          const int k = e / M, r = e % M;
+          const int n2 = r / M1, k1 = r - n2 * M1;
+          const cplx* g = gbuf + (size_t)k * P * M + n2;
+          const int st = M2 * k1;  // < M
+          const cplx ws = wtab[st];
+          int kk = n2 * k1;        // exponent of w (< M)
+          cplx w = wtab[kk];
+          cplx acc[P];
 #pragma unroll
-        for (int i = 0; i < P; ++i) acc[i] = cmk(0.0, 0.0);
-        cplx w = cmk(1.0, 0.0);
-        int kk = 0;
-        for (int q = 0; q < M; ++q) {
-          if ((q & 15) == 0) w = wtab[kk];
+          for (int i = 0; i < P; ++i) acc[i] = cmk(0.0, 0.0);
+          for (int n1 = 0; n1 < M1; ++n1) {
+            if (n1 && (n1 & 15) == 0) w = wtab[kk];
 #pragma unroll
-          for (int i = 0; i < P; ++i) acc[i] = cfma(g[i * M + q], w, acc[i]);
-          w = cmul(w, wt);
-          kk += t;
-          if (kk >= M) kk -= M;
+            for (int i = 0; i < P; ++i) acc[i] = cfma(g[i * M + M2 * n1], w, acc[i]);
+            w = cmul(w, ws);
+            kk += st;
+            if (kk >= M) kk -= M;
+          }
+#pragma unroll
+          for (int i = 0; i < P; ++i) vbuf[(k * P + i) * M + r] = acc[i];
         }
+        __syncthreads();
+        for (int e = tid; e < P * M; e += nt) {
+          const int k = e / M, t = e % M;
+          const int k2 = t / M1, k1 = t - k2 * M1;
+          const cplx* y = vbuf + (size_t)k * P * M + k1;
+          const int st = M1 * k2;  // < M
+          const cplx ws = wtab[st];
+          int kk = 0;
+          cplx w = cmk(1.0, 0.0);
+          cplx acc[P];
 #pragma unroll
-        for (int i = 0; i < P; ++i) vbuf[(k * P + i) * M + t] = acc[i];
+          for (int i = 0; i < P; ++i) acc[i] = cmk(0.0, 0.0);
+          for (int n2 = 0; n2 < M2; ++n2) {
+            if (n2 && (n2 & 15) == 0) w = wtab[kk];
+#pragma unroll
+            for (int i = 0; i < P; ++i) acc[i] = cfma(y[i * M + n2 * M1], w, acc[i]);
+            w = cmul(w, ws);
+            kk += st;
+            if (kk >= M) kk -= M;
+          }
+#pragma unroll
+          for (int i = 0; i < P; ++i) gbuf[(k * P + i) * M + t] = acc[i];
+        }
+        X = gbuf;
+      } else {
+        for (int e = tid; e < P * M; e += nt) {
+          const int k = e / M, t = e % M;
+          const cplx* g = gbuf + (size_t)k * P * M;
+          const cplx wt = wtab[t];
+          cplx acc[P];
+#pragma unroll
+          for (int i = 0; i < P; ++i) acc[i] = cmk(0.0, 0.0);
+          cplx w = cmk(1.0, 0.0);
+          int kk = 0;
+          for (int q = 0; q < M; ++q) {
+            if ((q & 15) == 0) w = wtab[kk];
+#pragma unroll
+            for (int i = 0; i < P; ++i) acc[i] = cfma(g[i * M + q], w, acc[i]);
+            w = cmul(w, wt);
+            kk += t;
+            if (kk >= M) kk -= M;
+          }
+#pragma unroll
+          for (int i = 0; i < P; ++i) vbuf[(k * P + i) * M + t] = acc[i];
+        }
       }
       __syncthreads();
       if (tid == 0) tsm[17 + 3 * cs] = clock64();
@@ -1847,7 +1904,7 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
         const cplx* wrow = wl + (cs * M + tt) * RP + rr * P;
         cplx acc = cmk(0.0, 0.0);
 #pragma unroll
-        for (int i = 0; i < P; ++i) acc = cfma(wrow[i], vbuf[(i * P + jj) * M + tt], acc);
+        for (int i = 0; i < P; ++i) acc = cfma(wrow[i], X[(i * P + jj) * M + tt], acc);
         resm = fmax(resm, cabs2(acc));
       }
       __syncthreads();
