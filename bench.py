@@ -392,21 +392,6 @@ def run_reference(args, rank):
         walls.append(wall)
     total = time.perf_counter() - t0
     value = nsolve * args.steps / total
-    # the sequential absorption chain: every condition of a solve passes
-    # through one leaf sweep in order (SURVEY 8(d) chain bound C x t_step);
-    # groups of <= 148 systems (solver.cu batch_groups) run one after the
-    # other in this eager timing pass, their systems in parallel
-    rows = 3 if raw.get("variant", "") == "general" else 2
-    n_cond = rows * info["order"]
-    groups = 1 if count < 32 else min(4, max(2, -(-count // 148)))
-    leaf_ms = sum(kst[k][0] for k in ("leaf_pivot", "leaf_build", "leaf_check", "leaf_exact") if k in kst) / nk
-    leaf_launches = kst.get("leaf_pivot", (0, 0))[1] / nk
-    solves = max(1.0, round(leaf_launches / max(groups * info["leaves"], 1)))
-    chain = {"conditions_per_solve": n_cond, "groups": groups, "direct_solves_per_system": solves,
-             "leaf_ms_per_step": leaf_ms,
-             "ns_per_condition": leaf_ms * 1e6 / (groups * solves * n_cond),
-             "bound": "latency of the pivot chain (one CTA per system and leaf)"}
-
     out = {
         "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,

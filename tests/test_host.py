@@ -2,6 +2,8 @@
 (ref: pkg/src/toepreg/toeplitz.py:37-233) and the reference's own
 ProblemSpec objects are accepted by duck typing."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -100,3 +102,20 @@ def test_experiment_drivers_host_parts_match_reference():
     fit = ex.fit_complexity([256, 512, 1024, 2048], [0.011, 0.026, 0.060, 0.135])
     assert np.allclose([fit.c1, fit.c2, fit.r_squared], g["fit"], rtol=1e-12, atol=0)
     assert {v: ex.free_parameters(v, 100) for v in ex.VARIANTS} == g["free_parameters"]
+
+
+def test_bench_reference_arm_runs_on_cpu():
+    """`bench.py --impl reference` (the driver's reference arm) needs no GPU:
+    it times the oracle on the host cores and prints one JSON line."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                         timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0
+    for key in ("metric", "unit", "cpu_baseline", "e2e", "config", "higher_is_better"):
+        assert key in line
