@@ -18,6 +18,10 @@
 #include "fft_bfly.cuh"
 #include "fft_fast.cuh"
 
+#ifndef FFT_COL_MINB
+#define FFT_COL_MINB 2  // resident CTAs per SM the register budget is sized for (3: spills, measured slower)
+#endif
+
 namespace {
 
 constexpr int NTH = 256;
@@ -131,7 +135,7 @@ TR_D void col_stage(cplx* sm, const ColArgs& a, long long lbase_in, long long lb
 }
 
 template <int LOG2, int Q, bool PASSA>
-__global__ void __launch_bounds__(NTH, 3) fft_col_kernel(ColArgs a) {
+__global__ void __launch_bounds__(NTH, FFT_COL_MINB) fft_col_kernel(ColArgs a) {
   using G = CPlan<LOG2, Q>;
   extern __shared__ __align__(16) unsigned char fsm[];
   cplx* tile = reinterpret_cast<cplx*>(fsm);

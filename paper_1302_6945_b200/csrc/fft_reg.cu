@@ -115,10 +115,14 @@ TR_D void run_stage(cplx* sm, const FastArgs& a, long long lin, long long lout, 
   }
 }
 
+#ifndef FFT_REG_MINB
+#define FFT_REG_MINB 2  // resident CTAs per SM the register budget is sized for (3: spills, measured slower)
+#endif
+
 // CTA = TL lines x T threads (TL chosen at launch so small batches still
 // spread over the SMs)
 template <int LOG2, int Q>
-__global__ void __launch_bounds__(NTH, 3) fft_reg_kernel(FastArgs a, int TL) {
+__global__ void __launch_bounds__(NTH, FFT_REG_MINB) fft_reg_kernel(FastArgs a, int TL) {
   using G = Plan<LOG2, Q>;
   extern __shared__ __align__(16) unsigned char fsm[];
   const int sl = threadIdx.x / G::T, tb = threadIdx.x % G::T;
