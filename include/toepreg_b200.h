@@ -24,7 +24,8 @@
  * Return codes: 0 ok; 2 invalid arguments (-> ValueError); 3 at least one
  * system singular (-> SingularSystemError, per-system status in tr_diag);
  * 4 CUDA error (-> RuntimeError); 5 capacity exceeded (too many deferred
- * conditions for the workspace).
+ * conditions for the workspace, or a basis product longer than planned:
+ * status 5 / 6 in tr_diag; -> RuntimeError).
  */
 #ifndef TOEPREG_B200_H
 #define TOEPREG_B200_H
@@ -59,7 +60,8 @@ typedef struct tr_desc {
 /* Per-system report (ref: SolveReport solver.py:48-55, TanIntDiagnostics
  * tanint.py:72-85). */
 typedef struct tr_diag {
-  int32_t status;               /* 0 ok, 3 singular, 5 capacity */
+  int32_t status;               /* 0 ok, 3 singular, 5 too many deferred conditions,
+                                   6 a basis product exceeded its planned length (x untrusted) */
   int32_t difficult_points;
   int64_t conditions_total;
   int32_t recursion_depth;
@@ -69,6 +71,8 @@ typedef struct tr_diag {
   double relative_residual;
   int32_t trim_overflow;        /* products truncated at the degree bound */
   int32_t refine_cg_iterations; /* CG refinement iterations run (0: none / direct refinement) */
+  double wall_time_s;           /* device time of the solve (assemble -> extract, + refinement),
+                                   excluding the residual evaluation; the whole batch's time */
 } tr_diag;
 
 /* Bytes of device workspace tr_solve_batch needs for `batch` systems. */

@@ -48,6 +48,7 @@ class TrDiag(C.Structure):
         ("relative_residual", C.c_double),
         ("trim_overflow", C.c_int32),
         ("refine_cg_iterations", C.c_int32),
+        ("wall_time_s", C.c_double),
     ]
 
 

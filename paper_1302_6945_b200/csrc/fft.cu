@@ -418,7 +418,7 @@ int fft_plan(long long n, FftPlan* out) {
     Ns *= ps.R;
   }
   // two-pass column plan (fft_col.cu) when n = N1 N2 with both <= 1024
-  if (p.npass >= 2 && !getenv("TR_FFT_OLD")) {
+  if (p.npass >= 2) {
     int a = 0;
     while ((p2 >> a) > 1) ++a;
     int lq = 0;
@@ -474,8 +474,7 @@ static int launch_pass(const FftPlan& p, int i, const cplx* in, long long in_ls,
     f.twR = ps.twR;
     f.sign = sign;
     const bool small = p.npass == 1 && ps.R <= 1024;
-    static const bool old_kernels = getenv("TR_FFT_OLD") != nullptr;
-    if (p.npass == 1 && !old_kernels && reg_launch(ps.log2, ps.q, f, st) == 0) return 0;
+    if (p.npass == 1 && reg_launch(ps.log2, ps.q, f, st) == 0) return 0;
     f.mul = nullptr;  // (fft_exec multiplied first when the register kernel cannot fuse it)
     if (fast_launch(ps.log2, ps.q, small, f, st) == 0) return 0;
   }
@@ -517,13 +516,12 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
   if (in_len > p.n) in_len = p.n;
   const long long n = p.n;
   g_fft_tag = (n << 20) + (lines & ((1 << 20) - 1));
-  static const bool old_kernels = getenv("TR_FFT_OLD") != nullptr;
   if (mul) {
     // the column kernels and the single-pass register kernel fuse the factor
     // into their loads; other plans multiply first
     const FftPass& p0 = p.pass[0];
     const int q0 = p0.q;
-    const bool reg = p.npass == 1 && p0.fast && !old_kernels && p0.R >= 2 && p0.R <= 4096 && p0.log2 <= 12 &&
+    const bool reg = p.npass == 1 && p0.fast && p0.R >= 2 && p0.R <= 4096 && p0.log2 <= 12 &&
                      (q0 == 1 || q0 == 3 || q0 == 5 || q0 == 7 || q0 == 9 || q0 == 15);
     if (!p.col && !reg) {
       if (in_len != n) { tr_set_error("fft_exec: fused factor needs full-length lines"); return 2; }

@@ -460,16 +460,11 @@ bool leaf_supported(int P, int K) {
 
 int leaf_launch(const LeafArgs& a_in, int nsys, cudaStream_t st, const SplitState* split) {
   if (nsys <= 0) return 0;
-  // TR_LEAF_MODE=exact forces the coupled kernel everywhere (diagnostic)
-  static const char* mode = getenv("TR_LEAF_MODE");
-  const bool exact_only = mode && mode[0] == 'e';
   LeafArgs a = a_in;
-  // TR_LEAF_MODE=split selects the three-kernel split path (diagnostic)
-  const bool split_only = mode && mode[0] == 's';
-  if (split && !exact_only && !split_only && leaf_fast_supported(a)) {
+  if (split && leaf_fast_supported(a)) {
     TR_TRY_LEAF(leaf_fast_launch(a, *split, nsys, st));
     a.only = split->need;  // re-run leaves whose rescale speculation failed
-  } else if (split && !exact_only && leaf_split_supported(a)) {
+  } else if (split && leaf_split_supported(a)) {
     TR_TRY_LEAF(leaf_split_launch(a, *split, nsys, st));
     a.only = split->need;
   }

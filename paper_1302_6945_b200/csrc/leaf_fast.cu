@@ -1,32 +1,32 @@
-// Leaf sweep, two kernels per absorption attempt (default path).
+// Leaf sweep (ref: pkg/src/toepreg/tanint.py:395-434 _serial_leaf, :189-217
+// _serial_core, :262-270 _self_residual).
 //
-// The reference absorbs a leaf's K conditions one at a time (ref:
-// pkg/src/toepreg/tanint.py:189-217 _serial_core) into a P x P polynomial
-// workspace, then checks the result (:262-270) and retries other orders
-// (:395-434).  Here an attempt is
+// The reference absorbs a leaf's K conditions one at a time into a P x P
+// polynomial workspace, then checks the result and retries other absorption
+// orders.  The decisions (pivot column, deferral, mu) depend on the basis
+// only through the residual rows r_s = w_s . B(sigma_s), which obey
+// r_i += mu_i r_j, r_j *= (sigma_s - sigma_t) at every absorbed step.
 //
-//   leaf_chain_kernel  the K sequential pivot decisions.  They depend on the
-//       basis only through the residual rows r_s = w_s . B(sigma_s); one warp
-//       owns the chain for 32 conditions at a time and keeps the row being
-//       decided ("front") and the next one ("pre") replicated in every lane,
-//       so a step is: decide on the front (branch-free argmax), form the
-//       multipliers mu_i = -phi_i / phi_j (MUFU reciprocal + Newton), update
-//       pre into the next front.  The multipliers are logged (smem, then HBM)
-//       for the other warps, which replay them on their own rows and take the
-//       chain over in turn.  Everything on the chain is branch-free: FP64 is
-//       16 lanes/clk per SMSP, so each warp-uniform FP64 instruction costs two
-//       issue cycles and the step time is set by their count.
-//   leaf_basis_kernel  replays the log on the coefficient cube (warp k owns
-//       basis row k, coefficient l = 32 d + lane in registers), skipping the
-//       structurally-zero part of every row (the degree of each entry is
-//       tracked from the log), normalises the columns (ref :179-183), writes
-//       the basis, evaluates it at the leaf's nodes (coset twist, fold,
-//       M-point DFT) for the reference's self-residual and keeps the best
-//       attempt.
+// Default (batches of <= 148 systems): leaf_fused3_kernel, one CTA per
+// system-leaf, every attempt of the leaf in one launch:
+//   * decider (warp 0, alone on its scheduler): a block of 32 consecutive
+//     conditions, one row per lane; a step is shuffle -> pivot rule
+//     (branch-free argmax on squared moduli) -> MUFU+Newton reciprocal ->
+//     own-row update, published to a shared-memory log with a release store;
+//   * holders apply published steps to the later rows (acquire polling) and
+//     hand their block to the decider when it gets there;
+//   * P basis-row warps replay the log on the coefficient cube (coefficient
+//     l = 32 d + lane in registers, structurally-zero blocks skipped);
+//   * finish_attempt: column normalisation, the self-residual (coset fold +
+//     factored M-point DFT) and the retry rule; attempts 0 and 1 run side by
+//     side in a 2-CTA cluster when the batch leaves SMs free.
+// Larger batches: leaf_chain2_kernel (the same chain with barrier hand-offs)
+// then leaf_basis_kernel (row-parallel replay + finish), one launch each per
+// attempt round.
 //
 // The reference's mid-sweep rescale (columns above 1e8 at every 8th
 // condition, ref :214-217) would change later decisions; the chain assumes it
-// does not fire and the basis kernel checks that no coefficient exceeded the
+// does not fire and the replay checks that no coefficient exceeded the
 // trigger at those points.  A leaf that violates this is redone by the exact
 // coupled kernel (leaf.cu).
 #include <cooperative_groups.h>
@@ -275,161 +275,6 @@ TR_D void decider_mu(const cplx (&f)[P], cplx (&mu)[P], int (&cd)[P], cplx fj) {
   cd[J] += 1;
 }
 
-// ------------------------------------------------------------ chain kernel
-template <int P>
-__global__ void __launch_bounds__(NT, 2) leaf_chain_kernel(LeafArgs a, SplitState s, int round) {
-  const int sys = blockIdx.x;
-  if (s.need[sys] != round) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int K = a.K, rows = a.rows;
-  cplx* lmu = reinterpret_cast<cplx*>(smem_raw);   // [K][P] true multipliers
-  cplx* lsig = lmu + (size_t)K * P;                // [K + 2] node of every condition
-  int* lj = reinterpret_cast<int*>(lsig + K + 2);  // [K] pivot or -1
-  int* head = lj + K;                              // steps published
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int warp = __shfl_sync(FULL, tid >> 5, 0);  // warp-uniform for ptxas (no collective shuffles)
-  const int att = round;
-  const cplx* W = a.W + (long long)sys * a.w_sys;
-  const long long rowstride = (long long)rows * P;
-  int2* dlog = s.def_try + (long long)sys * s.kcap;
-  const double thr2 = a.thr * a.thr;
-
-  int cd[P];
-#pragma unroll
-  for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
-  cplx r[P];
-  cplx sg = cmk(0.0, 0.0);
-#pragma unroll
-  for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
-  if (tid < K) {
-    const long long node = cond_node(a, tid, att);
-    sg = __ldg(&a.twN[node]);
-    lsig[tid] = sg;
-    const cplx* wr = W + node * rowstride + (tid % rows) * P;
-#pragma unroll
-    for (int i = 0; i < P; ++i) r[i] = wr[i];
-  }
-  if (tid < 2) lsig[K + tid] = cmk(0.0, 0.0);
-  if (tid == 0) *head = 0;
-  __syncthreads();
-
-  const int first = 32 * warp;
-  const int last = min(K, first + 32);
-  if (first < K) {
-    // replay the published steps until the chain reaches this warp
-    int done = 0;
-    while (done < first) {
-      int h;
-      while ((h = ld_acquire(head)) <= done) __nanosleep(20);
-      if (h > first) h = first;
-      for (; done < h; ++done) {
-        const int j = lj[done];
-        if (j >= 0) {
-          cplx mu[P];
-#pragma unroll
-          for (int i = 0; i < P; ++i) mu[i] = lmu[done * P + i];
-#pragma unroll
-          for (int i = 0; i < P; ++i) cd[i] += (i == j);
-          row_update<P>(r, j, mu, csub(sg, lsig[done]));
-        }
-      }
-    }
-    // own the chain for conditions first .. last-1
-    cplx f[P], pre[P];
-#pragma unroll
-    for (int i = 0; i < P; ++i) {
-      f[i] = shfl_c(r[i], 0);
-      pre[i] = shfl_c(r[i], 1);
-    }
-    cplx sf = lsig[first], sp = lsig[first + 1];
-    const bool trace = g_chain_trace_on && sys == 0 && round == 0 && lane == 0;
-#pragma unroll 2
-    for (int tn = first; tn < last; ++tn) {
-      const int ow = tn - first;
-      if (trace) g_chain_trace[4 * tn] = clock64();
-      cplx fj, qj;
-      int jj;
-      const int j = chain_decide<P>(f, pre, cd, thr2, fj, qj, jj);
-      if (trace) g_chain_trace[4 * tn + 1] = clock64() + 0 * j;
-      cplx mu[P];
-      if (j >= 0) {
-        // critical path: next front in pivot-scaled form (no division),
-        //   p_j pre_i - p_i pre_j (i != j),  p_j pre_j (s_pre - s_front),
-        // with p = phi 2^-e (exact power-of-two normalisation by the pivot)
-        const double mx = fmax(fabs(fj.x), fabs(fj.y));
-        const double sc = __hiloint2double((2046 - ((__double2hiint(mx) >> 20) & 0x7ff)) << 20, 0);
-        const cplx pj = cscale(fj, sc);
-        const cplx tj = cmul(pj, cmul(qj, csub(sp, sf)));
-        // off the path: mu_i = -phi_i / phi_j for the log and the own rows
-        const double inv2 = rcp_nr(cabs2(fj));
-        const cplx ci = cmk(-fj.x * inv2, fj.y * inv2);
-        const cplx rj = sel<P>(r, j);
-        const cplx nrj = cmul(rj, csub(sg, sf));
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          const cplx nf = cmsub(pj, pre[i], cscale(f[i], sc), qj);
-          const cplx m = cmul(f[i], ci);
-          mu[i] = (i == j) ? cmk(0.0, 0.0) : m;
-          f[i] = (i == j) ? tj : nf;
-          const cplx v = cfma(mu[i], rj, r[i]);
-          r[i] = (i == j) ? nrj : v;
-          cd[i] += (i == j);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          f[i] = pre[i];
-          mu[i] = cmk(0.0, 0.0);
-        }
-      }
-      if (trace) g_chain_trace[4 * tn + 2] = clock64() + 0 * (long long)f[0].x;
-      if (lane == 0) {
-        lj[tn] = j;
-#pragma unroll
-        for (int i = 0; i < P; ++i) lmu[tn * P + i] = mu[i];
-      }
-      if ((ow & 7) == 7 || ow >= 28 || tn == last - 1) {  // warp-uniform
-        if (lane == 0) st_release(head, tn + 1);
-      }
-      // pre <- row tn+2 through step tn (lane ow+2; unused past the warp's range)
-#pragma unroll
-      for (int i = 0; i < P; ++i) pre[i] = shfl_c(r[i], (ow + 2) & 31);
-      sf = sp;
-      sp = lsig[tn + 2];
-      if (trace) g_chain_trace[4 * tn + 3] = clock64() + 0 * (long long)pre[0].x;
-    }
-  }
-  __syncthreads();
-  // epilogue (warp 0): pivot log, basis length, ledger, deferred conditions in
-  // step order (ref tanint.py:200-206)
-  if (warp == 0) {
-    int len = 1, nd = 0;
-    int cdf[P];
-#pragma unroll
-    for (int i = 0; i < P; ++i) cdf[i] = a.cd[sys * 8 + i];
-    int* jlog = s.jl + (long long)sys * s.kcap;
-    for (int base = 0; base < K; base += 32) {
-      const int t = base + lane;
-      const int j = t < K ? lj[t] : -2;
-      if (t < K) jlog[t] = j;
-      const unsigned def = __ballot_sync(FULL, j == -1);
-      len += __popc(__ballot_sync(FULL, j >= 0));
-      if (j == -1) dlog[nd + __popc(def & ((1u << lane) - 1u))] = make_int2((int)cond_node(a, t, att), t % rows);
-      nd += __popc(def);
-#pragma unroll
-      for (int i = 0; i < P; ++i) cdf[i] += __popc(__ballot_sync(FULL, j == i));
-    }
-    if (lane == 0) {
-      s.ndef_try[sys] = nd;
-      s.len_try[sys] = len;
-#pragma unroll
-      for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cdf[i];
-    }
-  }
-  cplx* mulog = s.mu + (long long)sys * s.kcap * P;
-  for (int e = tid; e < K * P; e += NT) mulog[e] = lmu[e];
-}
-
 // ---------------------------------------------- chain kernel, warp-specialised
 // Warp 0 (the decider) owns the chain: it keeps the row being decided
 // ("front", row t through step t-1) and the next one ("pre", row t+1 through
@@ -619,163 +464,6 @@ __global__ void __launch_bounds__(SPREAD ? 352 : 288, SPREAD ? 1 : 2) leaf_chain
         bar_arrive(2 + 2 * (t & 1), 64);
       }
     }
-  }
-  __syncthreads();
-  // epilogue (warp 0): pivot log, basis length, ledger, deferred conditions in
-  // step order (ref tanint.py:200-206)
-  if (warp == 0) {
-    int len = 1, nd = 0;
-    int cdf[P];
-#pragma unroll
-    for (int i = 0; i < P; ++i) cdf[i] = a.cd[sys * 8 + i];
-    int* jlog = s.jl + (long long)sys * s.kcap;
-    for (int base = 0; base < K; base += 32) {
-      const int t = base + lane;
-      const int j = t < K ? lj[t] : -2;
-      if (t < K) jlog[t] = j;
-      const unsigned def = __ballot_sync(FULL, j == -1);
-      len += __popc(__ballot_sync(FULL, j >= 0));
-      if (j == -1) dlog[nd + __popc(def & ((1u << lane) - 1u))] = make_int2((int)cond_node(a, t, att), t % rows);
-      nd += __popc(def);
-#pragma unroll
-      for (int i = 0; i < P; ++i) cdf[i] += __popc(__ballot_sync(FULL, j == i));
-    }
-    if (lane == 0) {
-      s.ndef_try[sys] = nd;
-      s.len_try[sys] = len;
-#pragma unroll
-      for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cdf[i];
-    }
-  }
-  // multipliers for the basis replay: mu_i = phi_i c (mu_j = 0)
-  cplx* mulog = s.mu + (long long)sys * s.kcap * P;
-  for (int e = tid; e < K * P; e += blockDim.x) {
-    const int t = e / P, i = e - t * P;
-    const int j = lj[t];
-    mulog[e] = (j < 0 || i == j) ? cmk(0.0, 0.0) : cmul(lf[e], lci[t]);
-  }
-}
-
-// ------------------------------------------ chain kernel, lane-resident front
-// The decider warp holds a block of 32 consecutive conditions, one row per
-// lane, and applies every step to all of them itself: the next front is
-// already in a lane and is broadcast by shuffle, so a step has no barrier and
-// no hand-back on its critical path (shuffle -> decide -> reciprocal -> own
-// row update).  Warps 1..H-1 hold the later blocks, apply the published steps
-// from the shared-memory log as they appear (acquire polling on a step
-// counter) and pass their block to the decider when it reaches it (after the
-// last step of the previous block).  The log and the epilogue are those of
-// leaf_chain2_kernel, and every row update uses the same formulas, so the
-// pivots and multipliers are the same.
-template <int P>
-__global__ void __launch_bounds__(256, 2) leaf_chain3_kernel(LeafArgs a, SplitState s, int round) {
-  const int sys = blockIdx.x;
-  if (s.need[sys] != round) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int K = a.K, rows = a.rows;
-  cplx* lf = reinterpret_cast<cplx*>(smem_raw);    // [K][P] decided rows
-  cplx* lci = lf + (size_t)K * P;                  // [K] c_t = -conj(phi_j)/|phi_j|^2
-  cplx* lsig = lci + K;                            // [K] node of every condition
-  cplx* xfer = lsig + K;                           // [32][P] block hand-over
-  int* lj = reinterpret_cast<int*>(xfer + 32 * P);  // [K]
-  int* flag = lj + K;                              // [0] published steps, [1] blocks handed over
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int warp = __shfl_sync(FULL, tid >> 5, 0);
-  const int att = round;
-  const cplx* W = a.W + (long long)sys * a.w_sys;
-  const long long rowstride = (long long)rows * P;
-  int2* dlog = s.def_try + (long long)sys * s.kcap;
-  const int H = (K + 31) / 32;
-  const int mine = 32 * warp + lane;
-  cplx r[P];
-  cplx sg = cmk(0.0, 0.0);
-#pragma unroll
-  for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
-  if (warp < H && mine < K) {
-    const long long node = cond_node(a, mine, att);
-    sg = __ldg(&a.twN[node]);
-    lsig[mine] = sg;
-    const cplx* wr = W + node * rowstride + (mine % rows) * P;
-#pragma unroll
-    for (int i = 0; i < P; ++i) r[i] = wr[i];
-  }
-  if (tid < 2) flag[tid] = 0;
-  __syncthreads();
-
-  if (warp == 0) {
-    // ---------------- decider ----------------
-    const double thr2 = a.thr * a.thr;
-    int cd[P];
-#pragma unroll
-    for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
-    const bool trace = g_chain_trace_on && sys == 0 && round == 0 && lane == 0;
-    for (int b = 0; b < H; ++b) {
-      if (b > 0) {  // take over block b (its rows carry steps < 32 b)
-        while (ld_acquire(&flag[1]) < b) {
-        }
-#pragma unroll
-        for (int i = 0; i < P; ++i) r[i] = xfer[lane * P + i];
-        sg = lsig[min(32 * b + lane, K - 1)];
-      }
-      const int tend = min(K, 32 * b + 32);
-      for (int t = 32 * b; t < tend; ++t) {
-        if (trace) g_chain_trace[4 * t] = clock64();
-        const int src = t & 31;
-        cplx f[P];
-#pragma unroll
-        for (int i = 0; i < P; ++i) f[i] = shfl_c(r[i], src);
-        const cplx sf = lsig[t];
-        cplx fj;
-        double a2j;
-        const int j = decide_bits<P>(f, cd, thr2, fj, a2j);
-        const double inv2 = rcp_nr(a2j);
-        const cplx ci = cmk(-fj.x * inv2, fj.y * inv2);
-        if (lane == 0) {
-          lj[t] = j;
-          lci[t] = ci;
-#pragma unroll
-          for (int i = 0; i < P; ++i) lf[t * P + i] = f[i];
-          st_release(&flag[0], t + 1);
-        }
-        if (j >= 0) {
-          // r <- r + phi (c r_j), r_j (s_r - s_t) in column j
-          const cplx rj = sel<P>(r, j);
-          const cplx c2 = cmul(ci, rj);
-          const cplx nj = cmul(rj, csub(sg, sf));
-#pragma unroll
-          for (int i = 0; i < P; ++i) {
-            const cplx v = cfma(f[i], c2, r[i]);
-            r[i] = (i == j) ? nj : v;
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < P; ++i) cd[i] += (i == j);
-      }
-    }
-  } else if (warp < H) {
-    // ---------------- holder of block `warp`: steps < 32 warp ----------------
-    const int tlim = 32 * warp;
-    int avail = 0;
-    for (int t = 0; t < tlim; ++t) {
-      avail = wait_steps(&flag[0], t, avail);
-      const int j = lj[t];
-      if (j >= 0) {
-        const cplx rj = sel<P>(r, j);
-        const cplx c2 = cmul(lci[t], rj);
-        const cplx nj = cmul(rj, csub(sg, lsig[t]));
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          const cplx v = cfma(lf[t * P + i], c2, r[i]);
-          r[i] = (i == j) ? nj : v;
-        }
-      }
-    }
-    // wait for the decider to take the previous block, then hand this one over
-    while (ld_acquire(&flag[1]) < warp - 1) __nanosleep(TR_SPIN_NS);
-#pragma unroll
-    for (int i = 0; i < P; ++i) xfer[lane * P + i] = r[i];
-    __syncwarp();
-    if (lane == 0) st_release(&flag[1], warp);
   }
   __syncthreads();
   // epilogue (warp 0): pivot log, basis length, ledger, deferred conditions in
@@ -1175,271 +863,6 @@ __global__ void __launch_bounds__(NT, (DB <= 3 ? 2 : 1)) leaf_basis_kernel(LeafA
   }
   finish_attempt<P, DB>(a, s, round, sys, c, warp < P ? warp : -1, stage, wtab, twl, gbuf, vbuf, cbuf, red,
                         csafe, wred, &sviol, NW);
-}
-
-// ------------------------------------------------- fused attempt (one kernel)
-// For batches that fit the GPU with one CTA per SM: the decider + holder
-// chain of leaf_chain2_kernel plus P basis warps that replay each published
-// step on their basis row (in the shadow of the chain: they sync on the same
-// step barrier), then the normalisation and self-check of finish_attempt.
-// Warps: 0 decider; then on warp ids != 0 mod 4 the H holders and the P basis
-// rows.  Per step a basis row applies mu_i = phi_i c to its coefficient blocks.
-template <int P, int DB, int NB>
-TR_D int fused_steps(cplx (&c)[DB][P], int (&deg)[P], RowState& st, int t, int& synced, int lim, int K,
-                     int H, const int* lj, const cplx* lf, const cplx* lci, const cplx* lsig, int lane) {
-  for (; t < lim; ++t) {
-    if (t + 2 < K && synced <= t) {  // step t published (barrier 1/3)
-      const int hm = (t + 2) / 32 + 1;
-      bar_sync(1 + 2 * (t & 1), 32 * (1 + H - hm + 1 + P));
-      synced = t + 1;
-    }
-    const int j = lj[t];
-    if (j >= 0) {
-      const int dj = sel_i<P>(deg, j);
-      if (dj >= 0) {
-        const int nd = max(st.dmax, dj + 1);
-        if (nd / 32 + 1 > NB) return t;
-#pragma unroll
-        for (int i = 0; i < P; ++i) deg[i] = (i == j) ? dj + 1 : max(deg[i], dj);
-        st.dmax = nd;
-        const cplx ci = lci[t];
-        cplx mu[P];
-#pragma unroll
-        for (int i = 0; i < P; ++i) mu[i] = cmul(lf[t * P + i], ci);
-        basis_step_j<P, DB, NB>(c, j, mu, cneg(lsig[t]), lane);
-      }
-    }
-    if (((t + 1) % RESCALE_PERIOD) == 0) {
-      bool b = false;
-#pragma unroll
-      for (int d = 0; d < NB; ++d)
-#pragma unroll
-        for (int i = 0; i < P; ++i) b |= cabs2(c[d][i]) > RESCALE_TRIGGER * RESCALE_TRIGGER;
-      st.big |= b;
-    }
-  }
-  return t;
-}
-
-template <int P, int DB>
-__global__ void __launch_bounds__(512, 1) leaf_fused_kernel(LeafArgs a, SplitState s, int round, int stage) {
-  const int sys = blockIdx.x;
-  if (s.need[sys] != round) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int CAPR = 32 * DB;
-  const int K = a.K, rows = a.rows, M = a.M;
-  cplx* lf = reinterpret_cast<cplx*>(smem_raw);    // [K][P] decided rows
-  cplx* lci = lf + (size_t)K * P;                  // [K]
-  cplx* lsig = lci + K;                            // [K + 2]
-  cplx* prow = lsig + K + 2;                       // [2][P]
-  cplx* wtab = prow + 2 * P;                       // [M]
-  cplx* twl = wtab + M;                            // [CAPR]
-  cplx* gbuf = twl + CAPR;                         // [P*P][M]
-  cplx* vbuf = gbuf + (size_t)P * P * M;           // [P*P][M]
-  cplx* cbuf = vbuf + (size_t)P * P * M;           // [P*P][CAPR] (stage)
-  int* lj = reinterpret_cast<int*>(cbuf + (stage ? (size_t)P * P * CAPR : 0));  // [K]
-  __shared__ double red[8][8];
-  __shared__ double csafe[8];
-  __shared__ double wred[16];
-  __shared__ int sviol;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int warp = __shfl_sync(FULL, tid >> 5, 0);
-  const int nw = blockDim.x >> 5;
-  const int att = round;
-  const cplx* W = a.W + (long long)sys * a.w_sys;
-  const long long rowstride = (long long)rows * P;
-  int2* dlog = s.def_try + (long long)sys * s.kcap;
-  const int H = (K + 31) / 32;
-  const int slot = (warp & 3) ? warp - warp / 4 : 0;  // 1.. on warps != 0 mod 4
-  const int hid = (slot >= 1 && slot <= H) ? slot : 0;
-  const int brow = (slot > H && slot <= H + P) ? slot - H - 1 : -1;
-
-  const int mine = 32 * (hid - 1) + lane;
-  cplx r[P];
-  cplx sg = cmk(0.0, 0.0);
-#pragma unroll
-  for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
-  if (hid >= 1 && mine < K) {
-    const long long node = cond_node(a, mine, att);
-    sg = __ldg(&a.twN[node]);
-    lsig[mine] = sg;
-    const cplx* wr = W + node * rowstride + (mine % rows) * P;
-#pragma unroll
-    for (int i = 0; i < P; ++i) r[i] = wr[i];
-  }
-  if (tid < 2) lsig[K + tid] = cmk(0.0, 0.0);
-  for (int e = tid; e < M; e += blockDim.x) wtab[e] = __ldg(&a.twN[(long long)e * a.stride]);
-  if (tid == 0) sviol = 0;
-  cplx c[DB][P];
-#pragma unroll
-  for (int d = 0; d < DB; ++d)
-#pragma unroll
-    for (int i = 0; i < P; ++i) c[d][i] = cmk(0.0, 0.0);
-  __syncthreads();
-
-  auto nbar1 = [&](int t) { return 32 * (1 + H - ((t + 2) / 32 + 1) + 1 + P); };
-
-  RowState st;
-  st.dmax = 0;
-  st.big = false;
-  int deg[P];
-  int tb = 0, synced = 0;  // basis rows: next step, steps whose barrier was passed
-  if (warp == 0) {
-    // ---------------- decider (as leaf_chain2_kernel) ----------------
-    const double thr2 = a.thr * a.thr;
-    int cd[P];
-#pragma unroll
-    for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
-    cplx f[P], pre[P];
-    {
-      const cplx* w0 = W + cond_node(a, 0, att) * rowstride;
-#pragma unroll
-      for (int i = 0; i < P; ++i) f[i] = w0[i];
-      if (K > 1) {
-        const cplx* w1 = W + cond_node(a, 1, att) * rowstride + (1 % rows) * P;
-#pragma unroll
-        for (int i = 0; i < P; ++i) pre[i] = w1[i];
-      } else {
-#pragma unroll
-        for (int i = 0; i < P; ++i) pre[i] = cmk(0.0, 0.0);
-      }
-    }
-    cplx sf = lsig[0], sp = lsig[1];
-    for (int t = 0; t < K; ++t) {
-      cplx fj;
-      double a2j;
-      const int j = decide_bits<P>(f, cd, thr2, fj, a2j);
-      const double inv2 = rcp_nr(a2j);
-      const cplx ci = cmk(-fj.x * inv2, fj.y * inv2);
-      if (lane == 0) {
-        lj[t] = j;
-        lci[t] = ci;
-#pragma unroll
-        for (int i = 0; i < P; ++i) lf[t * P + i] = f[i];
-      }
-      if (t + 2 < K) bar_arrive(1 + 2 * (t & 1), nbar1(t));
-      if (t + 1 < K) {
-        if (t >= 1) {
-          bar_sync(2 + 2 * ((t - 1) & 1), 64);
-          const cplx* src = prow + ((t - 1) & 1) * P;
-#pragma unroll
-          for (int i = 0; i < P; ++i) pre[i] = src[i];
-        }
-        const cplx qj = sel<P>(pre, j);
-        const cplx c2 = cmul(ci, qj);
-        const cplx nfj = cmul(qj, csub(sp, sf));
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          const cplx v = cfma(f[i], c2, pre[i]);
-          f[i] = (j < 0) ? pre[i] : (i == j) ? nfj : v;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < P; ++i) cd[i] += (i == j);
-      sf = sp;
-      sp = lsig[t + 2];
-    }
-  } else if (hid >= 1) {
-    // ---------------- holder ----------------
-    for (int t = 0; t + 2 < K && hid >= (t + 2) / 32 + 1; ++t) {
-      bar_sync(1 + 2 * (t & 1), nbar1(t));
-      const int j = lj[t];
-      if (j >= 0) {
-        const cplx rj = sel<P>(r, j);
-        const cplx c2 = cmul(lci[t], rj);
-        const cplx nj = cmul(rj, csub(sg, lsig[t]));
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          const cplx v = cfma(lf[t * P + i], c2, r[i]);
-          r[i] = (i == j) ? nj : v;
-        }
-      }
-      if (hid == (t + 2) / 32 + 1) {
-        if (lane == (t + 2) % 32) {
-          cplx* dst = prow + (t & 1) * P;
-#pragma unroll
-          for (int i = 0; i < P; ++i) dst[i] = r[i];
-        }
-        bar_arrive(2 + 2 * (t & 1), 64);
-      }
-    }
-    // holders still needed at the end wait at the barrier below
-  } else if (brow >= 0) {
-    // ---------------- basis row: steps published through barrier 1/3 ----------------
-#pragma unroll
-    for (int i = 0; i < P; ++i) deg[i] = i == brow ? 0 : -1;
-#pragma unroll
-    for (int i = 0; i < P; ++i)
-      if (i == brow && lane == 0) c[0][i] = cmk(1.0, 0.0);
-    // steps up to K-3 come with a barrier; the last two after the sync below
-    const int kb = K > 2 ? K - 2 : 0;
-    bool over = false;  // outgrew the register blocks: keep passing the barriers only
-    while (tb < kb) {
-      int need = st.dmax / 32 + 1;
-      if (synced <= tb) {  // the barrier of step tb must be passed before reading it
-        bar_sync(1 + 2 * (tb & 1), nbar1(tb));
-        synced = tb + 1;
-      }
-      if (over) { ++tb; continue; }
-      const int j = lj[tb];
-      if (j >= 0) {
-        const int dj = sel_i<P>(deg, j);
-        if (dj >= 0) need = max(need, (dj + 1) / 32 + 1);
-      }
-      if (need > DB) { st.big = true; over = true; ++tb; continue; }
-#define TR_RUNF(NB, LIM) \
-  case NB: if constexpr (NB <= DB) tb = fused_steps<P, DB, NB>(c, deg, st, tb, synced, LIM, K, H, lj, lf, lci, lsig, lane); break;
-      switch (need) {
-        TR_RUNF(1, kb) TR_RUNF(2, kb) TR_RUNF(3, kb) TR_RUNF(4, kb) TR_RUNF(5, kb) TR_RUNF(6, kb) TR_RUNF(7, kb)
-        default: tb = K; break;
-      }
-    }
-  }
-  __syncthreads();
-  if (brow >= 0 && tb < K && !st.big) {  // the last steps (no barrier)
-    synced = K;
-    while (tb < K) {
-      int need = st.dmax / 32 + 1;
-      const int j = lj[tb];
-      if (j >= 0) {
-        const int dj = sel_i<P>(deg, j);
-        if (dj >= 0) need = max(need, (dj + 1) / 32 + 1);
-      }
-      if (need > DB) { st.big = true; break; }
-      switch (need) {
-        TR_RUNF(1, K) TR_RUNF(2, K) TR_RUNF(3, K) TR_RUNF(4, K) TR_RUNF(5, K) TR_RUNF(6, K) TR_RUNF(7, K)
-        default: tb = K; break;
-      }
-    }
-#undef TR_RUNF
-  }
-  if (brow >= 0 && __any_sync(FULL, st.big) && lane == 0) sviol = 1;
-  // chain epilogue (warp 0): pivot log, basis length, ledger, deferrals
-  if (warp == 0) {
-    int len = 1, nd = 0;
-    int cdf[P];
-#pragma unroll
-    for (int i = 0; i < P; ++i) cdf[i] = a.cd[sys * 8 + i];
-    for (int base = 0; base < K; base += 32) {
-      const int t = base + lane;
-      const int j = t < K ? lj[t] : -2;
-      const unsigned def = __ballot_sync(FULL, j == -1);
-      len += __popc(__ballot_sync(FULL, j >= 0));
-      if (j == -1) dlog[nd + __popc(def & ((1u << lane) - 1u))] = make_int2((int)cond_node(a, t, att), t % rows);
-      nd += __popc(def);
-#pragma unroll
-      for (int i = 0; i < P; ++i) cdf[i] += __popc(__ballot_sync(FULL, j == i));
-    }
-    if (lane == 0) {
-      s.ndef_try[sys] = nd;
-      s.len_try[sys] = len;
-#pragma unroll
-      for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cdf[i];
-    }
-  }
-  __syncthreads();
-  finish_attempt<P, DB>(a, s, round, sys, c, brow, stage, wtab, twl, gbuf, vbuf, cbuf, red, csafe, wred, &sviol,
-                        nw);
 }
 
 // ------------------------------------ fused attempts, lane-resident front
@@ -2112,8 +1535,6 @@ int launch_f3(const LeafArgs& a, const SplitState& s, int nsys, int nw, size_t f
 // fused attempts with the lane-resident chain (leaf_fused3_kernel): one
 // launch per leaf; returns -1 when the shape does not fit it
 int launch_fused3(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t st) {
-  static const char* fv = getenv("TR_F3");  // TR_F3=0: previous kernels
-  if (fv && fv[0] == '0') return -1;
   if (nsys > 148) return -1;
   const int H = (a.K + 31) / 32;
   const int last = H / 2 + a.P;  // highest slot: H/2 holders, then the basis rows
@@ -2132,8 +1553,7 @@ int launch_fused3(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t
   }
   // attempts 0 and 1 side by side (2-CTA clusters) while the batch leaves
   // SMs idle: the retry tail of a leaf then costs no extra chain time
-  static const char* cv2 = getenv("TR_F3_PAIR");  // TR_F3_PAIR=0: sequential attempts
-  const bool cl = a.nattempts > 1 && 2 * nsys <= 148 && !(cv2 && cv2[0] == '0');
+  const bool cl = a.nattempts > 1 && 2 * nsys <= 148;
   int rc = 0;
   TrKTimer _kt(TRK_LEAF_PIVOT, st);
 #define TR_F3N(PP_, DB_, NTH_)                                                                             \
@@ -2180,83 +1600,21 @@ int leaf_fast_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStrea
     tr_kernel_work(TRK_LEAF_BUILD, 16.0 * nsys * (P * P * (K + 1) + K * P),
                    4.0 * nsys * P * P * K * (K + 1) + 8.0 * nsys * (double)a.noff * P * P * a.M * a.M);
   }
-  const size_t csm = sizeof(cplx) * ((size_t)a.K * a.P + a.K + 2) + sizeof(int) * (a.K + 2);
   const size_t csm2 = sizeof(cplx) * ((size_t)a.K * a.P + 2 * a.K + 2 + 2 * a.P) + sizeof(int) * a.K;
   const int hk = (a.K + 31) / 32;  // holder warps
   // one CTA per SM when the batch fits the GPU: holders off the decider's
   // scheduler; otherwise the compact layout, two CTAs per SM
   const bool spread = nsys <= 148;
   const int nth2 = 32 * (1 + hk + (spread ? (hk - 1) / 3 : 0));
-  static const char* cv = getenv("TR_CHAIN");  // TR_CHAIN=relay: previous chain kernel
-  const bool relay = cv && cv[0] == 'r';
-  const bool lanes = cv && cv[0] == '3';  // TR_CHAIN=3: lane-resident front
-  const size_t csm3 = sizeof(cplx) * ((size_t)a.K * a.P + 2 * (size_t)a.K + 32 * (size_t)a.P) +
-                      sizeof(int) * (a.K + 2);
-  // fused attempt kernel (chain + basis + check in one CTA) when the batch
-  // fits the GPU at one CTA per SM and the basis fits the register blocks
-  static const char* fv = getenv("TR_FUSED");  // TR_FUSED=0: two kernels
-  const int fslots = hk + a.P;
-  const int fwarps = fslots + (fslots - 1) / 3 + 1;
-  const int fdb = blocks_planned(a);
-  const bool fused = !relay && !lanes && !(fv && fv[0] == '0') && nsys <= 148 && fwarps <= 16 &&
-                     fdb <= (a.P == 5 ? 4 : 3);
-  if (fused) {
-    const int CAPR = 32 * fdb;
-    size_t fs = sizeof(cplx) * ((size_t)a.K * a.P + 2 * a.K + 2 + 2 * a.P + a.M + CAPR +
-                                2 * (size_t)a.P * a.P * a.M) + sizeof(int) * a.K;
-    const size_t fstaged = sizeof(cplx) * (size_t)a.P * a.P * CAPR;
-    const int stage = fs + fstaged <= 200 * 1024 ? 1 : 0;
-    if (stage) fs += fstaged;
-    for (int round = 0; round < a.nattempts; ++round) {
-      TrKTimer _kt(TRK_LEAF_PIVOT, st);
-      int rc = 0;
-#define TR_FUSED_L(PP_, DB_)                                                                       \
-  {                                                                                                \
-    static bool set = false;                                                                       \
-    if (!set) {                                                                                    \
-      cudaFuncSetAttribute(leaf_fused_kernel<PP_, DB_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           200 * 1024);                                                            \
-      set = true;                                                                                  \
-    }                                                                                              \
-    leaf_fused_kernel<PP_, DB_><<<nsys, 32 * fwarps, fs, st>>>(a, s, round, stage);                \
-  }
-      if (a.P == 5) {
-        switch (fdb) {
-          case 1: TR_FUSED_L(5, 1) break;
-          case 2: TR_FUSED_L(5, 2) break;
-          case 3: TR_FUSED_L(5, 3) break;
-          default: TR_FUSED_L(5, 4) break;
-        }
-      } else {
-        switch (fdb) {
-          case 1: TR_FUSED_L(7, 1) break;
-          case 2: TR_FUSED_L(7, 2) break;
-          default: TR_FUSED_L(7, 3) break;
-        }
-      }
-#undef TR_FUSED_L
-      (void)rc;
-    }
-    TR_CUDA_CHECK(cudaGetLastError());
-    return 0;
-  }
   for (int round = 0; round < a.nattempts; ++round) {
     {
       TrKTimer _kt(TRK_LEAF_PIVOT, st);
-      if (relay) {
-        if (a.P == 5) leaf_chain_kernel<5><<<nsys, NT, csm, st>>>(a, s, round);
-        else leaf_chain_kernel<7><<<nsys, NT, csm, st>>>(a, s, round);
-      } else if (lanes) {
-        if (a.P == 5) leaf_chain3_kernel<5><<<nsys, 32 * hk, csm3, st>>>(a, s, round);
-        else leaf_chain3_kernel<7><<<nsys, 32 * hk, csm3, st>>>(a, s, round);
+      if (a.P == 5) {
+        if (spread) leaf_chain2_kernel<5, true><<<nsys, nth2, csm2, st>>>(a, s, round);
+        else leaf_chain2_kernel<5, false><<<nsys, nth2, csm2, st>>>(a, s, round);
       } else {
-        if (a.P == 5) {
-          if (spread) leaf_chain2_kernel<5, true><<<nsys, nth2, csm2, st>>>(a, s, round);
-          else leaf_chain2_kernel<5, false><<<nsys, nth2, csm2, st>>>(a, s, round);
-        } else {
-          if (spread) leaf_chain2_kernel<7, true><<<nsys, nth2, csm2, st>>>(a, s, round);
-          else leaf_chain2_kernel<7, false><<<nsys, nth2, csm2, st>>>(a, s, round);
-        }
+        if (spread) leaf_chain2_kernel<7, true><<<nsys, nth2, csm2, st>>>(a, s, round);
+        else leaf_chain2_kernel<7, false><<<nsys, nth2, csm2, st>>>(a, s, round);
       }
     }
     const int rc = a.P == 5 ? dispatch_basis<5>(a, s, round, nsys, st)

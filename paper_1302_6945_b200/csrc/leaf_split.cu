@@ -6,12 +6,11 @@
 // rows r_s = w_s . B(sigma_s), which obey r_i += mu_i r_j, r_j *= (sigma_s -
 // sigma_t) at every absorbed step.  So one attempt splits into:
 //
-//   A  leaf_pivot_kernel   the sequential chain on residual rows only (a few
-//                          warps, one __syncthreads per step), writing the
-//                          per-step log (pivot j_t or -1, mu_t) to HBM;
-//   B  leaf_build_kernel   replays the log on the P x P x (K+1) coefficient
-//                          cube held in registers (no decisions left), then
-//                          normalises and writes the basis;
+//   A  leaf_pivot_relay_kernel  the sequential chain on residual rows only
+//                          (warp relay, no barriers), writing the per-step
+//                          log (pivot j_t or -1, mu_t) to HBM;
+//   B  leaf_build_row_kernel    replays the log on one row of the P x P x (K+1)
+//                          coefficient cube per CTA (no decisions left);
 //   C  leaf_check_kernel   the reference's self-residual check (coset fold +
 //                          DFT), best-attempt bookkeeping and the decision to
 //                          retry with the next absorption order (ref :395-434).
@@ -26,16 +25,6 @@
 
 #include <stdlib.h>
 
-// pivot-chain clock trace of system 0 (diagnostic, tr_debug_pivot_trace)
-__device__ long long g_pivot_trace[4 * 1024];
-__device__ int g_pivot_trace_on = 0;
-
-extern "C" int tr_debug_pivot_trace(int enable, long long* out, int n) {
-  int on = enable;
-  cudaMemcpyToSymbol(g_pivot_trace_on, &on, sizeof(int));
-  if (out) cudaMemcpyFromSymbol(out, g_pivot_trace, sizeof(long long) * (n < 4096 ? n : 4096));
-  return 0;
-}
 
 namespace {
 
@@ -187,233 +176,6 @@ TR_D void row_step(cplx (&r)[P], const cplx* mu, cplx dsig) {
   r[J] = cmul(rj, dsig);
 }
 
-// ------------------------------------------------------------------ A
-template <int P, int NW, int QMAX>
-__global__ void __launch_bounds__(NW * 32) leaf_pivot_kernel(LeafArgs a, SplitState s, int round) {
-  constexpr int NT = NW * 32;
-  const int sys = blockIdx.x;
-  if (s.need[sys] != round) return;
-  __shared__ cplx pmu[2][P];
-  __shared__ cplx psig[2];
-  __shared__ int pj[2];
-  __shared__ int nd_s;
-  const int tid = threadIdx.x;
-  const int K = a.K, rows = a.rows;
-  const int att = round;
-  const cplx* W = a.W + (long long)sys * a.w_sys;
-  const long long rowstride = (long long)rows * P;
-  cplx* mulog = s.mu + (long long)sys * s.kcap * P;
-  int* jlog = s.jl + (long long)sys * s.kcap;
-  int2* dlog = s.def_try + (long long)sys * s.kcap;
-
-  int cd[P];
-#pragma unroll
-  for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
-  cplx r[QMAX][P];
-  cplx sg[QMAX];
-#pragma unroll
-  for (int q = 0; q < QMAX; ++q) {
-    const int c = tid + NT * q;
-    sg[q] = cmk(0.0, 0.0);
-#pragma unroll
-    for (int i = 0; i < P; ++i) r[q][i] = cmk(0.0, 0.0);
-    if (c < K) {
-      const long long node = cond_node(a, c, att);
-      sg[q] = __ldg(&a.twN[node]);
-      const cplx* wr = W + node * rowstride + (c % rows) * P;
-#pragma unroll
-      for (int i = 0; i < P; ++i) r[q][i] = wr[i];
-    }
-  }
-  if (tid == 0) {
-    nd_s = 0;
-    s.viol[sys] = 0;
-    const int j0 = decide<P>(r[0], cd, a.thr, pmu[0]);
-    pj[0] = j0;
-    psig[0] = sg[0];
-    jlog[0] = j0;
-    if (j0 >= 0) {
-#pragma unroll
-      for (int i = 0; i < P; ++i) mulog[i] = pmu[0][i];
-    } else {
-      dlog[0] = make_int2((int)cond_node(a, 0, att), 0);
-      nd_s = 1;
-    }
-  }
-  __syncthreads();
-  for (int t = 0; t < K; ++t) {
-    const int cur = t & 1;
-    const int j = pj[cur];
-    const int tn = t + 1;
-    if (j >= 0) {
-      const cplx sig_t = psig[cur];
-      cplx mu[P];
-#pragma unroll
-      for (int i = 0; i < P; ++i) mu[i] = pmu[cur][i];
-#pragma unroll
-      for (int i = 0; i < P; ++i) cd[i] += (i == j);
-#pragma unroll
-      for (int q = 0; q < QMAX; ++q) {
-        const int c = tid + NT * q;
-        if (c > t && c < K) {
-          const cplx dsig = csub(sg[q], sig_t);
-#define TR_R(J) row_step<P, J>(r[q], mu, dsig)
-          TR_SWITCH_J(P, TR_R)
-#undef TR_R
-        }
-      }
-    }
-    // owner of condition t+1 decides it (rows are current)
-    if (tn < K && (tn % NT) == tid) {
-      const int qo = tn / NT;
-      cplx rr[P];
-      cplx so = sg[0];
-#pragma unroll
-      for (int i = 0; i < P; ++i) rr[i] = r[0][i];
-#pragma unroll
-      for (int q = 1; q < QMAX; ++q)
-        if (q == qo) {
-#pragma unroll
-          for (int i = 0; i < P; ++i) rr[i] = r[q][i];
-          so = sg[q];
-        }
-      const int nxt = cur ^ 1;
-      const int jn = decide<P>(rr, cd, a.thr, pmu[nxt]);
-      pj[nxt] = jn;
-      psig[nxt] = so;
-      jlog[tn] = jn;
-      if (jn >= 0) {
-#pragma unroll
-        for (int i = 0; i < P; ++i) mulog[(long long)tn * P + i] = pmu[nxt][i];
-      } else {
-        dlog[nd_s] = make_int2((int)cond_node(a, tn, att), tn % rows);
-        nd_s += 1;
-      }
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    s.ndef_try[sys] = nd_s;
-    int len = 1;
-    for (int t = 0; t < K; ++t) len += jlog[t] >= 0;
-    s.len_try[sys] = len;
-  }
-  if (tid == 0) {
-#pragma unroll
-    for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cd[i];
-  }
-}
-
-// --------------------------------------------------- A (8 warps, 1 row each)
-// Critical path per step: barrier -> read (j, mu, sigma) -> owner row update
-// -> pivot rule -> publish.  Only the warp holding condition t+1 evaluates
-// the rule (all its lanes SIMT, the owner lane publishes); every update is
-// branch-free.
-template <int P>
-__global__ void __launch_bounds__(256) leaf_pivot3_kernel(LeafArgs a, SplitState s, int round) {
-  const int sys = blockIdx.x;
-  if (s.need[sys] != round) return;
-  __shared__ cplx pmu[2][P];
-  __shared__ cplx psig[2];
-  __shared__ int pj[2];
-  __shared__ int nd_s;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int K = a.K, rows = a.rows;
-  const int att = round;
-  const cplx* W = a.W + (long long)sys * a.w_sys;
-  const long long rowstride = (long long)rows * P;
-  cplx* mulog = s.mu + (long long)sys * s.kcap * P;
-  int* jlog = s.jl + (long long)sys * s.kcap;
-  int2* dlog = s.def_try + (long long)sys * s.kcap;
-
-  int cd[P];
-#pragma unroll
-  for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
-  cplx r[P];
-  cplx sg = cmk(0.0, 0.0);
-#pragma unroll
-  for (int i = 0; i < P; ++i) r[i] = cmk(0.0, 0.0);
-  if (tid < K) {
-    const long long node = cond_node(a, tid, att);
-    sg = __ldg(&a.twN[node]);
-    const cplx* wr = W + node * rowstride + (tid % rows) * P;
-#pragma unroll
-    for (int i = 0; i < P; ++i) r[i] = wr[i];
-  }
-  if (tid == 0) {
-    nd_s = 0;
-    s.viol[sys] = 0;
-    cplx m[P];
-    const int j0 = decide<P>(r, cd, a.thr, m);
-    pj[0] = j0;
-    psig[0] = sg;
-    jlog[0] = j0;
-    if (j0 >= 0) {
-#pragma unroll
-      for (int i = 0; i < P; ++i) {
-        pmu[0][i] = m[i];
-        mulog[i] = m[i];
-      }
-    } else {
-      dlog[0] = make_int2((int)cond_node(a, 0, att), 0);
-      nd_s = 1;
-    }
-  }
-  __syncthreads();
-  int len = 1;
-  const bool trace = g_pivot_trace_on && sys == 0;
-  for (int t = 0; t < K; ++t) {
-    const long long c0 = trace ? clock64() : 0;
-    const int cur = t & 1, nxt = cur ^ 1;
-    const int j = pj[cur];
-    const int tn = t + 1;
-    if (j >= 0) {
-      ++len;
-      cplx mu[P];
-#pragma unroll
-      for (int i = 0; i < P; ++i) mu[i] = pmu[cur][i];
-      const cplx sig_t = psig[cur];
-#pragma unroll
-      for (int i = 0; i < P; ++i) cd[i] += (i == j);
-      if (tid > t && tid < K) row_update<P>(r, j, mu, csub(sg, sig_t));
-    }
-    const long long c1 = trace ? clock64() : 0;
-    if (tn < K && warp == (tn >> 5)) {
-      cplx m[P];
-      const int jn = decide<P>(r, cd, a.thr, m);
-      if (trace && tid == tn) {
-        const long long c2 = clock64();
-        g_pivot_trace[4 * tn + 0] = c0;
-        g_pivot_trace[4 * tn + 1] = c1;
-        g_pivot_trace[4 * tn + 2] = c2;
-      }
-      if (tid == tn) {
-        pj[nxt] = jn;
-        psig[nxt] = sg;
-        jlog[tn] = jn;
-        if (jn >= 0) {
-#pragma unroll
-          for (int i = 0; i < P; ++i) {
-            pmu[nxt][i] = m[i];
-            mulog[(long long)tn * P + i] = m[i];
-          }
-        } else {
-          dlog[nd_s] = make_int2((int)cond_node(a, tn, att), tn % rows);
-          nd_s += 1;
-        }
-        if (trace) g_pivot_trace[4 * tn + 3] = clock64();
-      }
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    s.ndef_try[sys] = nd_s;
-    s.len_try[sys] = len;
-#pragma unroll
-    for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cd[i];
-  }
-}
-
 // ---------------------------------------------------- A (relay, no barriers)
 // Warp w owns conditions 32w .. 32w+31 (one per lane).  Only the warp that
 // owns the next condition is on the critical path: it applies the newest step
@@ -549,110 +311,6 @@ __global__ void __launch_bounds__(256) leaf_pivot_relay_kernel(LeafArgs a, Split
   for (int e = tid; e < K * P; e += blockDim.x) mulog[e] = lmu[e];
 }
 
-// ------------------------------------------------------------- A (1 warp)
-// The chain in a single warp: lane l owns conditions s = l + 32 q.  At each
-// step every lane evaluates the pivot rule on its own row of slot q(t+1)
-// (SIMT, no divergence) and the owner lane's result is broadcast by
-// shuffle; rows already absorbed (s <= t) are skipped a whole slot at a time.
-template <int P, int QMAX>
-__global__ void __launch_bounds__(32) leaf_pivot_warp_kernel(LeafArgs a, SplitState s, int round) {
-  const int sys = blockIdx.x;
-  if (s.need[sys] != round) return;
-  const int lane = threadIdx.x;
-  const int K = a.K, rows = a.rows;
-  const int att = round;
-  const cplx* W = a.W + (long long)sys * a.w_sys;
-  const long long rowstride = (long long)rows * P;
-  cplx* mulog = s.mu + (long long)sys * s.kcap * P;
-  int* jlog = s.jl + (long long)sys * s.kcap;
-  int2* dlog = s.def_try + (long long)sys * s.kcap;
-
-  int cd[P];
-#pragma unroll
-  for (int i = 0; i < P; ++i) cd[i] = a.cd[sys * 8 + i];
-  cplx r[QMAX][P];
-  cplx sg[QMAX];
-#pragma unroll
-  for (int q = 0; q < QMAX; ++q) {
-    const int c = lane + 32 * q;
-    sg[q] = cmk(0.0, 0.0);
-#pragma unroll
-    for (int i = 0; i < P; ++i) r[q][i] = cmk(0.0, 0.0);
-    if (c < K) {
-      const long long node = cond_node(a, c, att);
-      sg[q] = __ldg(&a.twN[node]);
-      const cplx* wr = W + node * rowstride + (c % rows) * P;
-#pragma unroll
-      for (int i = 0; i < P; ++i) r[q][i] = wr[i];
-    }
-  }
-  int nd = 0;
-  if (lane == 0) s.viol[sys] = 0;
-  cplx mu[P];
-  cplx sig;
-  int j;
-  // decide condition tn (slot qo = tn / 32, owner lane tn % 32) and broadcast
-  auto decide_bcast = [&](int tn) {
-    const int qo = tn >> 5, ow = tn & 31;
-    cplx m[P];
-    int jj = -1;
-    cplx so = sg[0];
-#define TR_DQ(Q)                                   \
-  case Q:                                          \
-    if constexpr (Q < QMAX) {                      \
-      jj = decide<P>(r[Q], cd, a.thr, m);          \
-      so = sg[Q];                                  \
-    }                                              \
-    break;
-    switch (qo) { TR_DQ(0) TR_DQ(1) TR_DQ(2) TR_DQ(3) TR_DQ(4) TR_DQ(5) TR_DQ(6) TR_DQ(7) default: break; }
-#undef TR_DQ
-    j = __shfl_sync(FULL, jj, ow);
-    sig = shfl_c(so, ow);
-    if (j >= 0) {
-#pragma unroll
-      for (int i = 0; i < P; ++i) mu[i] = shfl_c(m[i], ow);
-    }
-    if (lane == ow) {
-      jlog[tn] = j;
-      if (j >= 0) {
-#pragma unroll
-        for (int i = 0; i < P; ++i) mulog[(long long)tn * P + i] = m[i];
-      }
-    }
-    if (j < 0) {
-      if (lane == 0) dlog[nd] = make_int2((int)cond_node(a, tn, att), tn % rows);
-      ++nd;
-    }
-  };
-  decide_bcast(0);
-  int len = 1;
-  for (int t = 0; t < K; ++t) {
-    if (j >= 0) {
-      ++len;
-#pragma unroll
-      for (int i = 0; i < P; ++i) cd[i] += (i == j);
-#pragma unroll
-      for (int q = 0; q < QMAX; ++q) {
-        if (32 * q + 31 <= t) continue;  // the whole slot is absorbed
-        const int c = lane + 32 * q;
-        if (c > t && c < K) {
-          const cplx dsig = csub(sg[q], sig);
-#define TR_R(J) row_step<P, J>(r[q], mu, dsig)
-          TR_SWITCH_J(P, TR_R)
-#undef TR_R
-        }
-      }
-    }
-    if (t + 1 < K) decide_bcast(t + 1);
-  }
-  if (lane == 0) {
-    s.ndef_try[sys] = nd;
-    s.len_try[sys] = len;
-#pragma unroll
-    for (int i = 0; i < P; ++i) s.cd_try[sys * 8 + i] = cd[i];
-  }
-}
-
 // ------------------------------------------------------------------ B
 template <int P, int D, int J>
 TR_D void basis_step(cplx (&c)[D][P], const cplx* mu_s, cplx msig, cplx up) {
@@ -677,138 +335,6 @@ TR_D cplx pick_top(const cplx (&c)[D][P], int j) {
   for (int i = 1; i < P; ++i)
     if (j == i) v = c[D - 1][i];
   return v;
-}
-
-template <int P, int D, int MAXT>
-__global__ void __launch_bounds__(MAXT, 1) leaf_build_kernel(LeafArgs a, SplitState s, int round,
-                                                             int TPR) {
-  const int sys = blockIdx.x;
-  if (s.need[sys] != round) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int K = a.K;
-  const int NT = blockDim.x, NW = NT / 32;
-  cplx* musm = reinterpret_cast<cplx*>(smem_raw);  // [K][P]
-  cplx* sgsm = musm + (size_t)K * P;               // [K]
-  cplx* halo = sgsm + K;                           // [2][NW][P]
-  double* red = reinterpret_cast<double*>(halo + 2 * NW * P);  // [NW][P]
-  int* jsm = reinterpret_cast<int*>(red + NW * P); // [K]
-  int* viol = jsm + K;                             // [1]
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int krow = tid / TPR, u = tid % TPR;
-  const bool brow = krow < P;
-  const int att = round;
-  const cplx* mulog = s.mu + (long long)sys * s.kcap * P;
-  const int* jlog = s.jl + (long long)sys * s.kcap;
-  for (int e = tid; e < K; e += NT) {
-    const int j = jlog[e];
-    jsm[e] = j;
-    sgsm[e] = __ldg(&a.twN[cond_node(a, e, att)]);
-    if (j >= 0)
-#pragma unroll
-      for (int i = 0; i < P; ++i) musm[e * P + i] = mulog[(long long)e * P + i];
-  }
-  if (tid == 0) *viol = 0;
-  cplx c[D][P];
-#pragma unroll
-  for (int d = 0; d < D; ++d)
-#pragma unroll
-    for (int i = 0; i < P; ++i)
-      c[d][i] = (brow && u * D + d == 0 && i == krow) ? cmk(1.0, 0.0) : cmk(0.0, 0.0);
-  if (lane == 31) {
-#pragma unroll
-    for (int i = 0; i < P; ++i) halo[warp * P + i] = c[D - 1][i];
-  }
-  __syncthreads();
-  int len = 1;
-  int cur = 0;
-  bool big = false;
-  for (int t = 0; t < K; ++t) {
-    const int j = jsm[t];
-    if (j < 0) continue;  // deferred: nothing changes (uniform branch)
-    const cplx* mu_s = musm + t * P;
-    const cplx msig = cneg(sgsm[t]);
-    // branch-free: old pivot column per degree, then every column at once
-    cplx oj[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) oj[d] = sel<P>(c[d], j);
-    cplx up;
-    up.x = __shfl_up_sync(FULL, oj[D - 1].x, 1);
-    up.y = __shfl_up_sync(FULL, oj[D - 1].y, 1);
-    if (lane == 0 && warp > 0) up = halo[(cur * NW + warp - 1) * P + j];
-    if (u == 0) up = cmk(0.0, 0.0);
-    if (brow && u * D <= len) {
-      cplx mu[P];
-#pragma unroll
-      for (int i = 0; i < P; ++i) mu[i] = mu_s[i];
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        const cplx nj = cfma(msig, oj[d], d > 0 ? oj[d - 1] : up);
-#pragma unroll
-        for (int i = 0; i < P; ++i) c[d][i] = (i == j) ? nj : cfma(mu[i], oj[d], c[d][i]);
-      }
-    }
-    ++len;
-    if (((t + 1) % RESCALE_PERIOD) == 0) {
-      // speculation check: the reference would rescale when any coefficient
-      // of a column exceeds the trigger at this point
-#pragma unroll
-      for (int d = 0; d < D; ++d)
-#pragma unroll
-        for (int i = 0; i < P; ++i) big |= cabs2(c[d][i]) > RESCALE_TRIGGER * RESCALE_TRIGGER;
-    }
-    cur ^= 1;
-    if (lane == 31) {
-#pragma unroll
-      for (int i = 0; i < P; ++i) halo[(cur * NW + warp) * P + i] = c[D - 1][i];
-    }
-    __syncthreads();
-  }
-  if (big) *viol = 1;
-  // normalize columns (ref tanint.py:179-183)
-#pragma unroll
-  for (int i = 0; i < P; ++i) {
-    double m = 0.0;
-#pragma unroll
-    for (int d = 0; d < D; ++d) m = fmax(m, cabs2(c[d][i]));
-    m = wmax(m);
-    if (lane == 0) red[warp * P + i] = m;
-  }
-  __syncthreads();
-  double factor = 1.0;
-#pragma unroll
-  for (int i = 0; i < P; ++i) {
-    double m = 0.0;
-    for (int w = 0; w < NW; ++w) m = fmax(m, red[w * P + i]);
-    m = sqrt(m);
-    const double safe = m > 0.0 ? m : 1.0;
-    const double inv = 1.0 / safe;
-#pragma unroll
-    for (int d = 0; d < D; ++d) c[d][i] = cscale(c[d][i], inv);
-    factor = fmax(factor, safe);
-  }
-  cplx* dst = (round == 0 ? a.out : a.scratch) + (long long)sys * a.out_sys;
-  if (brow) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const int l = u * D + d;
-      if (l < a.cap) {
-#pragma unroll
-        for (int i = 0; i < P; ++i) dst[(long long)(krow * P + i) * a.cap + l] = c[d][i];
-      }
-    }
-  }
-  const int covered = TPR * D;
-  if (a.cap > covered) {
-    const int tail = a.cap - covered;
-    for (long long e = tid; e < (long long)P * P * tail; e += NT)
-      dst[(e / tail) * a.cap + covered + e % tail] = cmk(0.0, 0.0);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    s.factor_try[sys] = factor;
-    s.viol[sys] = *viol;
-  }
 }
 
 // ------------------------------------------------------- B (one row per CTA)
@@ -1079,24 +605,6 @@ __global__ void need_reset_kernel(int* need, int nsys) {
 }
 
 template <int P, int D, int MAXT>
-int launch_build(const LeafArgs& a, const SplitState& s, int round, int nsys, cudaStream_t st) {
-  const int TPR = (a.K + 1 + D - 1) / D;
-  const int NB = P * TPR, NT = (NB + 31) & ~31;
-  if (NT > MAXT) return -1;
-  const int NW = NT / 32;
-  size_t smem = sizeof(cplx) * ((size_t)a.K * P + a.K + 2 * (size_t)NW * P) +
-                sizeof(double) * NW * P + sizeof(int) * (a.K + 1);
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(leaf_build_kernel<P, D, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         160 * 1024);
-    set = true;
-  }
-  { TrKTimer _kt(TRK_LEAF_BUILD, st); leaf_build_kernel<P, D, MAXT><<<nsys, NT, smem, st>>>(a, s, round, TPR); }
-  return 0;
-}
-
-template <int P, int D, int MAXT>
 int launch_build_row(const LeafArgs& a, const SplitState& s, int round, int nsys, cudaStream_t st) {
   const int TPR = (a.K + 1 + D - 1) / D;
   const int NT = (TPR + 31) & ~31;
@@ -1148,54 +656,23 @@ int leaf_split_launch(const LeafArgs& a, const SplitState& s, int nsys, cudaStre
     cudaFuncSetAttribute(leaf_check_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     set = true;
   }
-  // diagnostics: TR_PIVOT=warp|block4 (pivot variants), TR_BUILD=block (one-CTA replay)
-  static const char* pv = getenv("TR_PIVOT");
-  static const char* bv = getenv("TR_BUILD");
-  const bool block_build = bv && bv[0] == 'b';
   for (int round = 0; round < a.nattempts; ++round) {
     {
       TrKTimer _kt(TRK_LEAF_PIVOT, st);
-      if (pv && pv[0] == 'w') {
-        if (a.P == 5) leaf_pivot_warp_kernel<5, 8><<<nsys, 32, 0, st>>>(a, s, round);
-        else leaf_pivot_warp_kernel<7, 8><<<nsys, 32, 0, st>>>(a, s, round);
-      } else if (pv && pv[0] == 'b') {
-        if (a.P == 5) leaf_pivot_kernel<5, 4, 2><<<nsys, 128, 0, st>>>(a, s, round);
-        else leaf_pivot_kernel<7, 4, 2><<<nsys, 128, 0, st>>>(a, s, round);
-      } else if (pv && pv[0] == '3') {
-        if (a.P == 5) leaf_pivot3_kernel<5><<<nsys, 256, 0, st>>>(a, s, round);
-        else leaf_pivot3_kernel<7><<<nsys, 256, 0, st>>>(a, s, round);
-      } else {
-        const size_t rsm = sizeof(cplx) * (size_t)a.K * (a.P + 1) + sizeof(int) * (a.K + 2);
-        if (a.P == 5) leaf_pivot_relay_kernel<5><<<nsys, 256, rsm, st>>>(a, s, round);
-        else leaf_pivot_relay_kernel<7><<<nsys, 256, rsm, st>>>(a, s, round);
-      }
+      const size_t rsm = sizeof(cplx) * (size_t)a.K * (a.P + 1) + sizeof(int) * (a.K + 2);
+      if (a.P == 5) leaf_pivot_relay_kernel<5><<<nsys, 256, rsm, st>>>(a, s, round);
+      else leaf_pivot_relay_kernel<7><<<nsys, 256, rsm, st>>>(a, s, round);
     }
-    int rc;
-    if (block_build) {
-      rc = a.P == 5 ? launch_build<5, 3, 480>(a, s, round, nsys, st)
-                    : launch_build<7, 4, 352>(a, s, round, nsys, st);
-    } else {
-      static const int bd = bv ? atoi(bv) : 0;  // TR_BUILD=<degrees per thread>
-      if (bd == 4) {
-        rc = a.P == 5 ? launch_build_row<5, 4, 128>(a, s, round, nsys, st)
-                      : launch_build_row<7, 4, 128>(a, s, round, nsys, st);
-      } else if (bd == 2) {
-        rc = a.P == 5 ? launch_build_row<5, 2, 160>(a, s, round, nsys, st)
-                      : launch_build_row<7, 2, 160>(a, s, round, nsys, st);
-      } else {
-        rc = a.P == 5 ? launch_build_row<5, 1, 288>(a, s, round, nsys, st)
-                      : launch_build_row<7, 1, 288>(a, s, round, nsys, st);
-      }
-    }
+    const int rc = a.P == 5 ? launch_build_row<5, 1, 288>(a, s, round, nsys, st)
+                            : launch_build_row<7, 1, 288>(a, s, round, nsys, st);
     if (rc) {
       tr_set_error("leaf split shape unsupported (K=%d, P=%d)", a.K, a.P);
       return 2;
     }
     {
       TrKTimer _kt(TRK_LEAF_CHECK, st);
-      const int norm = block_build ? 0 : 1;
-      if (a.P == 5) leaf_check_kernel<5><<<nsys, CK, csm, st>>>(a, s, round, norm);
-      else leaf_check_kernel<7><<<nsys, CK, csm, st>>>(a, s, round, norm);
+      if (a.P == 5) leaf_check_kernel<5><<<nsys, CK, csm, st>>>(a, s, round, 1);
+      else leaf_check_kernel<7><<<nsys, CK, csm, st>>>(a, s, round, 1);
     }
   }
   TR_CUDA_CHECK(cudaGetLastError());

@@ -436,11 +436,7 @@ struct Builder {
     // product lengths 2^k + 1 (equal-tau columns) would need a transform past
     // 2^(k+1): transform at La + Lb - 2 instead when that length is cheaper and
     // correct the single wrapped coefficient (wrap_fix_kernel)
-    static const bool wrap_ok = [] {
-      const char* e = getenv("TR_WRAP");
-      return !(e && e[0] == '0');
-    }();
-    if (wrap_ok && full >= 3 && ca >= 2 && cb >= 2) {
+    if (full >= 3 && ca >= 2 && cb >= 2) {
       const long long rw = fft_good_len(full - 1);
       if (rw < cm.R) {
         cm.R = rw;
@@ -933,8 +929,6 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
         }
       }
     } else if (op.kind == OP_UPDATE) {
-      static const bool skip_u = getenv("TR_DIAG_SKIP_UPDATES") != nullptr;  // timing diagnostic only (wrong x)
-      if (skip_u) continue;
       long long cnt = N / op.stride;
       long long scap = p.slot_cap[op.slot_a];
       // systems in chunks whose folded values stay in L2 between the three kernels
@@ -948,8 +942,6 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
                                    cnt, ns, st));
       }
     } else {
-      static const bool skip_c = getenv("TR_DIAG_SKIP_COMBINES") != nullptr;  // timing diagnostic only (wrong x)
-      if (skip_c) continue;
       long long R = op.R;
       long long ca = p.slot_cap[op.slot_a], cb = p.slot_cap[op.slot_b];
       const FftPlan& fp = F(p, R);
@@ -1099,6 +1091,7 @@ int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
     // The report describes the direct solve (the reference's single pass):
     // its ledger and diagnostics are kept across the refinement solve, and a
     // refinement solve that fails (singular residual problem) leaves x as is.
+    // Truncated products (trim_over) accumulate over every solve.
     if (phase == PH_REFINE_CG) TR_TRY(launch_cg_restore(w.X, w.X0, cst, n, nsys, st));
     int* sv = w.diag_save;
     const size_t ib = sizeof(int) * nsys;
@@ -1106,7 +1099,6 @@ int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
     TR_CUDA_CHECK(cudaMemcpyAsync(sv + 8 * nsys, w.dcount, ib, cudaMemcpyDeviceToDevice, st));
     TR_CUDA_CHECK(cudaMemcpyAsync(sv + 9 * nsys, w.retried, ib, cudaMemcpyDeviceToDevice, st));
     TR_CUDA_CHECK(cudaMemcpyAsync(sv + 10 * nsys, w.status, ib, cudaMemcpyDeviceToDevice, st));
-    TR_CUDA_CHECK(cudaMemcpyAsync(sv + 11 * nsys, w.trim_over, ib, cudaMemcpyDeviceToDevice, st));
     TR_CUDA_CHECK(cudaMemcpyAsync(w.scale_save, w.max_scale, sizeof(double) * nsys, cudaMemcpyDeviceToDevice, st));
     TR_TRY(normal_apply(p, nsys, w, sbs, w.X, st));
     TR_TRY(launch_residual(w.Rv, w.AX, w.X, w.Y, n, in.beta_sq, in.beta_bs, add_ridge, nsys, st));
@@ -1116,7 +1108,6 @@ int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
     TR_CUDA_CHECK(cudaMemcpyAsync(w.dcount, sv + 8 * nsys, ib, cudaMemcpyDeviceToDevice, st));
     TR_CUDA_CHECK(cudaMemcpyAsync(w.retried, sv + 9 * nsys, ib, cudaMemcpyDeviceToDevice, st));
     TR_CUDA_CHECK(cudaMemcpyAsync(w.status, sv + 10 * nsys, ib, cudaMemcpyDeviceToDevice, st));
-    TR_CUDA_CHECK(cudaMemcpyAsync(w.trim_over, sv + 11 * nsys, ib, cudaMemcpyDeviceToDevice, st));
     TR_CUDA_CHECK(cudaMemcpyAsync(w.max_scale, w.scale_save, sizeof(double) * nsys, cudaMemcpyDeviceToDevice, st));
     return 0;
   }
@@ -1157,6 +1148,9 @@ int read_diag(const Plan& p, long long nsys, const WS& w, cudaStream_t st, tr_di
       double den = nr[nsys + s];
       dg.relative_residual = nr[s] / (den > 0.0 ? den : 1.0);
       dg.trim_overflow = tro[s];
+      // a product longer than its planned capacity was cut: x is not
+      // trustworthy, report it instead of returning it silently
+      if (tro[s] > 0 && dg.status == 0) dg.status = 6;
       dg.refine_cg_iterations = cgit[s];
     }
   }
@@ -1338,7 +1332,7 @@ int cg_any_unconverged(std::vector<Group>& gs, cudaStream_t st, bool* need) {
 // The whole solve: direct, refinement (CG first when refine_cg > 0, direct
 // solves otherwise or for what CG left unfinished), final residual.
 int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine, int refine_cg, cudaStream_t st,
-              void* ws, bool* cg_refined) {
+              void* ws, bool* cg_refined, cudaEvent_t ev_solved) {
   *cg_refined = false;
   // CG refinement cap from the plan alone (every system decides from its own
   // residual history, so results do not depend on the batch): about one CG
@@ -1371,6 +1365,7 @@ int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine,
   } report{ptimes, pe, st};
   if (!cg) {
     for (int r = 0; r < refine; ++r) TR_TRY(run_phase(p, gs, nsys, PH_REFINE, 0, st, ws));
+    if (ev_solved) TR_CUDA_CHECK(cudaEventRecord(ev_solved, st));
     TR_TRY(run_phase(p, gs, nsys, PH_FINAL, 0, st, ws));
     return 0;
   }
@@ -1385,6 +1380,7 @@ int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine,
   if (need)
     for (int r = 0; r < refine; ++r) TR_TRY(run_phase(p, gs, nsys, PH_REFINE_CG, 0, st, ws));
   *cg_refined = true;
+  if (ev_solved) TR_CUDA_CHECK(cudaEventRecord(ev_solved, st));
   TR_TRY(run_phase(p, gs, nsys, PH_FINAL, 0, st, ws));
   return 0;
 }
@@ -1451,14 +1447,30 @@ extern "C" int tr_solve_batch(const tr_desc* d, int64_t batch, const double* T_g
   }
   cudaStream_t st = (cudaStream_t)stream;
   bool cg_refined = false;
-  TR_TRY(run_solve(*p, gs, batch, d->refine, d->refine_cg, st, workspace, &cg_refined));
-  if (diag_host)
+  // wall_time (ref solver.py:62-71): device time of assemble -> basis ->
+  // extract (+ refinement), not the residual evaluation that follows
+  static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (diag_host && !ev[0])
+    for (auto& e : ev) TR_CUDA_CHECK(cudaEventCreate(&e));
+  if (diag_host) TR_CUDA_CHECK(cudaEventRecord(ev[0], st));
+  TR_TRY(run_solve(*p, gs, batch, d->refine, d->refine_cg, st, workspace, &cg_refined,
+                   diag_host ? ev[1] : nullptr));
+  if (diag_host) {
     for (auto& g : gs) TR_TRY(read_diag(*p, g.count, g.w, st, diag_host + g.first, cg_refined));
+    float ms = 0.f;
+    TR_CUDA_CHECK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    for (long long s = 0; s < batch; ++s) diag_host[s].wall_time_s = 1e-3 * ms;
+  }
   if (diag_host) {
     for (long long s = 0; s < batch; ++s) {
       if (diag_host[s].status == 3) return 3;
       if (diag_host[s].status == 5) {
         tr_set_error("system %lld: more than %d deferred conditions", s, DMAX);
+        return 5;
+      }
+      if (diag_host[s].status == 6) {
+        tr_set_error("system %lld: a basis product exceeded its planned length (%d truncations)", s,
+                     diag_host[s].trim_overflow);
         return 5;
       }
     }

@@ -99,180 +99,6 @@ __global__ void pointwise_matmul_kernel(cplx* FA, const cplx* FB, long long R) {
   }
 }
 
-__device__ __forceinline__ double block_max256(double v, double* sh) {
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) sh[warp] = v;
-  __syncthreads();
-  double m = sh[0];
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, sh[w]);
-  __syncthreads();
-  return m;
-}
-
-// profile[l] = max_e |F[e][l]|, global max
-__global__ void trim1_kernel(TrimArgs a) {
-  __shared__ double sh[32];
-  long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long sys = blockIdx.y;
-  const int PP = a.P * a.P;
-  double m = 0.0;
-  if (l < a.L) {
-    const cplx* F = a.F + sys * PP * a.R + l;
-    for (int e = 0; e < PP; ++e) m = fmax(m, cabs(F[(long long)e * a.R]));
-    a.prof[sys * a.L + l] = m;
-  }
-  double bm = block_max256(m, sh);
-  if (threadIdx.x == 0) atomicMax(&a.red[sys * (2 + a.P)], dbits(bm));
-}
-
-// last significant index (+1)
-__global__ void trim2_kernel(TrimArgs a) {
-  __shared__ double sh[32];
-  long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long sys = blockIdx.y;
-  double gmax = dfrom(a.red[sys * (2 + a.P)]);
-  double v = -1.0;
-  if (l < a.L && a.prof[sys * a.L + l] > 1e-14 * gmax) v = (double)(l + 1);
-  double bm = block_max256(v, sh);
-  if (threadIdx.x == 0 && bm > 0.0)
-    atomicMax(&a.red[sys * (2 + a.P) + 1], (unsigned long long)bm);
-}
-
-// per-column max over the kept range
-__global__ void trim3_kernel(TrimArgs a) {
-  __shared__ double sh[32];
-  long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long sys = blockIdx.y;
-  const int P = a.P, PP = P * P;
-  unsigned long long* red = a.red + sys * (2 + P);
-  long long lt = (long long)red[1];
-  if (lt < 1) lt = 1;
-  const cplx* F = a.F + sys * PP * a.R + l;
-  for (int j = 0; j < P; ++j) {
-    double m = 0.0;
-    if (l < lt && l < a.L)
-      for (int i = 0; i < P; ++i) m = fmax(m, cabs(F[(long long)(i * P + j) * a.R]));
-    double bm = block_max256(m, sh);
-    if (threadIdx.x == 0) atomicMax(&red[2 + j], dbits(bm));
-  }
-}
-
-__global__ void trim4_kernel(TrimArgs a) {
-  long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long sys = blockIdx.y;
-  const int P = a.P, PP = P * P;
-  const unsigned long long* red = a.red + sys * (2 + P);
-  long long lt = (long long)red[1];
-  if (lt < 1) lt = 1;
-  long long lw = lt < a.cap_node ? lt : a.cap_node;
-  if (l < a.cap) {
-    const cplx* F = a.F + sys * PP * a.R + l;
-    cplx* o = a.out + sys * a.out_sys + l;
-    for (int i = 0; i < P; ++i)
-      for (int j = 0; j < P; ++j) {
-        cplx v = cmk(0.0, 0.0);
-        if (l < lw) {
-          double cm = dfrom(red[2 + j]);
-          double safe = cm > 0.0 ? cm : 1.0;
-          cplx f = F[(long long)(i * P + j) * a.R];
-          v = cmk(f.x / safe, f.y / safe);
-        }
-        o[(long long)(i * P + j) * a.cap] = v;
-      }
-  }
-  if (l == 0) {
-    double ms = 1.0;
-    bool first = true;
-    for (int j = 0; j < P; ++j) {
-      double cm = dfrom(red[2 + j]) / (double)a.R;
-      double safe = cm > 0.0 ? cm : 1.0;
-      ms = first ? safe : fmax(ms, safe);
-      first = false;
-    }
-    a.max_scale[sys] = fmax(a.max_scale[sys], ms);
-    if (lt > a.cap_node) a.trim_over[sys] += 1;
-  }
-}
-
-// All four trim phases in one CTA per system (batches of many systems):
-// profile + global max, last significant index, column maxima over the kept
-// range, scaled write-out.  Same rule as trim1..4 (squared moduli).
-constexpr int TF = 512;
-
-__device__ __forceinline__ double bmax512(double v, double* sh) {
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) sh[warp] = v;
-  __syncthreads();
-  double m = sh[0];
-#pragma unroll
-  for (int w = 1; w < TF / 32; ++w) m = fmax(m, sh[w]);
-  return m;
-}
-
-template <int P>
-__global__ void __launch_bounds__(TF) trim_fused_kernel(TrimArgs a) {
-  __shared__ double sh[TF / 32];
-  const long long sys = blockIdx.x;
-  constexpr int PP = P * P;
-  const cplx* F = a.F + sys * PP * a.R;
-  double* prof = a.prof + sys * a.L;
-  double gm = 0.0;
-  for (long long l = threadIdx.x; l < a.L; l += TF) {
-    double m = 0.0;
-#pragma unroll
-    for (int e = 0; e < PP; ++e) m = fmax(m, cabs2(F[(long long)e * a.R + l]));
-    prof[l] = m;
-    gm = fmax(gm, m);
-  }
-  gm = bmax512(gm, sh);
-  const double thr = 1e-28 * gm;  // (1e-14)^2 on squared moduli
-  double last = 0.0;
-  for (long long l = threadIdx.x; l < a.L; l += TF)
-    if (prof[l] > thr) last = fmax(last, (double)(l + 1));
-  last = bmax512(last, sh);
-  long long lt = (long long)last;
-  if (lt < 1) lt = 1;
-  const long long lw = lt < a.cap_node ? lt : a.cap_node;
-  double cm[P];
-#pragma unroll
-  for (int j = 0; j < P; ++j) {
-    double m = 0.0;
-    for (long long l = threadIdx.x; l < lt && l < a.L; l += TF)
-#pragma unroll
-      for (int i = 0; i < P; ++i) m = fmax(m, cabs2(F[(long long)(i * P + j) * a.R + l]));
-    cm[j] = sqrt(bmax512(m, sh));
-  }
-  cplx* o = a.out + sys * a.out_sys;
-  for (long long l = threadIdx.x; l < a.cap; l += TF) {
-#pragma unroll
-    for (int i = 0; i < P; ++i)
-#pragma unroll
-      for (int j = 0; j < P; ++j) {
-        cplx v = cmk(0.0, 0.0);
-        if (l < lw) {
-          const double safe = cm[j] > 0.0 ? cm[j] : 1.0;
-          const cplx f = F[(long long)(i * P + j) * a.R + l];
-          v = cmk(f.x / safe, f.y / safe);
-        }
-        o[(long long)(i * P + j) * a.cap + l] = v;
-      }
-  }
-  if (threadIdx.x == 0) {
-    double ms = 1.0;
-#pragma unroll
-    for (int j = 0; j < P; ++j) {
-      const double c = cm[j] / (double)a.R;
-      const double safe = c > 0.0 ? c : 1.0;
-      ms = j == 0 ? safe : fmax(ms, safe);
-    }
-    a.max_scale[sys] = fmax(a.max_scale[sys], ms);
-    if (lt > a.cap_node) a.trim_over[sys] += 1;
-  }
-}
-
 // Trim + normalise with a cluster of C CTAs per system (C = 1: one CTA):
 // every CTA owns a contiguous slice of the coefficient range, the per-system
 // reductions (global max, last column above 1e-14 of it, column maxima) are
@@ -507,27 +333,8 @@ int launch_pointwise_matmul(cplx* FA, const cplx* FB, int P, long long R, long l
 
 int launch_trim_normalize(const TrimArgs& a, long long nsys, cudaStream_t st) {
   tr_kernel_work(TRK_COMBINE, 16.0 * nsys * a.P * a.P * (double)(a.L + a.cap), 0.0);
-  static const char* tv = getenv("TR_TRIM");  // TR_TRIM=old: one CTA per system / four kernels
-  if (!(tv && tv[0] == 'o') || (a.Rs > 0 && a.Rs != a.R)) {
-    const int rc = a.P == 5 ? dispatch_trim_cl<5>(a, nsys, st) : dispatch_trim_cl<7>(a, nsys, st);
-    if (rc) return rc;
-    TR_CUDA_CHECK(cudaGetLastError());
-    return 0;
-  }
-  if (nsys >= 32) {  // enough systems to fill the GPU with one CTA each
-    {
-      TrKTimer _kt(TRK_COMBINE, st);
-      if (a.P == 5) trim_fused_kernel<5><<<(unsigned)nsys, TF, 0, st>>>(a);
-      else trim_fused_kernel<7><<<(unsigned)nsys, TF, 0, st>>>(a);
-    }
-    TR_CUDA_CHECK(cudaGetLastError());
-    return 0;
-  }
-  TR_CUDA_CHECK(cudaMemsetAsync(a.red, 0, sizeof(unsigned long long) * (2 + a.P) * nsys, st));
-  { TrKTimer _kt(TRK_COMBINE, st); trim1_kernel<<<g2(a.L, nsys), 256, 0, st>>>(a); }
-  { TrKTimer _kt(TRK_COMBINE, st); trim2_kernel<<<g2(a.L, nsys), 256, 0, st>>>(a); }
-  { TrKTimer _kt(TRK_COMBINE, st); trim3_kernel<<<g2(a.L, nsys), 256, 0, st>>>(a); }
-  { TrKTimer _kt(TRK_COMBINE, st); trim4_kernel<<<g2(a.cap, nsys), 256, 0, st>>>(a); }
+  const int rc = a.P == 5 ? dispatch_trim_cl<5>(a, nsys, st) : dispatch_trim_cl<7>(a, nsys, st);
+  if (rc) return rc;
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }

@@ -14,7 +14,7 @@ from typing import List, Tuple
 import torch
 import torch.distributed as dist
 
-__all__ = ["shard_range", "shard_counts", "gather_solutions"]
+__all__ = ["shard_range", "shard_counts", "gather_solutions", "solve_sharded"]
 
 
 def shard_counts(total: int, world: int) -> List[int]:
@@ -46,3 +46,22 @@ def gather_solutions(x_local: torch.Tensor, total: int, dst: int = 0, group=None
         return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0)
     dist.gather(buf, gather_list=None, dst=dst, group=group)
     return None
+
+
+def solve_sharded(problems, solve_fn, dst: int = 0, group=None):
+    """Solve a batch of independent problems split over the ranks: this rank
+    runs ``solve_fn(shard) -> [count_r, n] complex`` on its contiguous shard
+    (``solve_tikhonov_batch`` / ``DeviceBatch`` on a GPU), then the solutions
+    are gathered to ``dst`` in problem order.  Returns the [total, n] complex
+    array on ``dst``, None elsewhere."""
+    import numpy as np
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    lo, hi = shard_range(len(problems), rank, world)
+    x = np.ascontiguousarray(solve_fn(problems[lo:hi]), dtype=np.complex128)
+    local = torch.from_numpy(x.view(np.float64).reshape(hi - lo, -1, 2))
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    full = gather_solutions(local.to(dev), len(problems), dst=dst, group=group)
+    if full is None:
+        return None
+    return full.cpu().numpy().reshape(len(problems), -1).view(np.complex128)

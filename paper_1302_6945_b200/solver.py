@@ -16,9 +16,8 @@ and ``DeviceBatch`` (inputs already in HBM, used by bench.py).
 from __future__ import annotations
 
 import ctypes as C
-import time
 from dataclasses import dataclass, field
-from typing import List, Optional, Sequence
+from typing import List, Sequence
 
 import numpy as np
 
@@ -114,7 +113,10 @@ def _shape(problem):
     return v, m, n, pl
 
 
-def make_desc(variant, m, n, pl, cfg: SolverConfig) -> _lib.TrDesc:
+def make_desc(variant, m, n, pl, cfg) -> _lib.TrDesc:
+    """``cfg`` is our SolverConfig or any object with the reference's five
+    fields (ref solver.py:39-45: n_lim, pivot_threshold, fill, paired,
+    force_even); the refinement fields default to ours when absent."""
     if cfg.fill not in _lib.FILLS:
         raise ValueError(f"unknown fill policy {cfg.fill!r}")
     d = _lib.TrDesc()
@@ -125,12 +127,12 @@ def make_desc(variant, m, n, pl, cfg: SolverConfig) -> _lib.TrDesc:
     d.fill = _lib.FILLS[cfg.fill]
     d.paired = int(bool(cfg.paired))
     d.force_even = int(bool(cfg.force_even))
-    d.refine = int(cfg.refine)
-    d.refine_cg = int(cfg.refine_cg)
+    d.refine = int(getattr(cfg, "refine", SolverConfig.refine))
+    d.refine_cg = int(getattr(cfg, "refine_cg", SolverConfig.refine_cg))
     return d
 
 
-def plan_info(problem, config: Optional[SolverConfig] = None) -> dict:
+def plan_info(problem, config=None) -> dict:
     cfg = config or SolverConfig()
     d = make_desc(*_shape(problem), cfg)
     lib = _lib.load()
@@ -163,7 +165,7 @@ class DeviceBatch:
 
     _ws_cache = {}
 
-    def __init__(self, problems: Sequence, config: Optional[SolverConfig] = None):
+    def __init__(self, problems: Sequence, config=None):
         torch = _torch()
         if len(problems) == 0:
             raise ValueError("empty batch")
@@ -264,12 +266,20 @@ class DeviceBatch:
         _torch().cuda.current_stream().synchronize()
         return self.x_host.numpy().view(np.complex128).reshape(self.batch, self.n)
 
-    def reports(self, x: np.ndarray, wall: float) -> List[SolveReport]:
+    def reports(self, x: np.ndarray) -> List[SolveReport]:
+        """One SolveReport per system.  ``wall_time`` is the device time of
+        the batch's solve (assemble -> extract, plus refinement), excluding
+        staging, the result copy and the residual evaluation, as the
+        reference's covers assemble -> extract only (ref solver.py:62-71);
+        every system of a batch reports the batch's time."""
         out = []
         for i in range(self.batch):
             dg = self.diag[i]
             if dg.status == 3:
                 raise SingularSystemError(f"system {i}: interpolation data singular")
+            if dg.status == 6:
+                raise RuntimeError(f"system {i}: a basis product exceeded its planned length "
+                                   f"({dg.trim_overflow} truncations); refusing to return x")
             if dg.status != 0:
                 raise RuntimeError(f"system {i}: solver status {dg.status}: {_lib.last_error()}")
             p = 7 if self.variant == "general" else 5
@@ -283,26 +293,26 @@ class DeviceBatch:
                 refine_cg_iterations=int(dg.refine_cg_iterations))
             out.append(SolveReport(
                 x_hat=np.array(x[i], dtype=np.complex128),
-                variant=self.variant, wall_time=wall / self.batch,
+                variant=self.variant, wall_time=float(dg.wall_time_s),
                 relative_residual=float(dg.relative_residual), diagnostics=diag,
                 final_col_degrees=np.array(dg.final_col_degrees[:p], dtype=np.int64)))
         return out
 
 
-def solve_tikhonov_batch(problems: Sequence, config: Optional[SolverConfig] = None,
+def solve_tikhonov_batch(problems: Sequence, config=None,
                          max_batch: int = 512) -> List[SolveReport]:
     """Solve many same-shape problems; returns one SolveReport per problem."""
     problems = list(problems)
     reports: List[SolveReport] = []
     for s in range(0, len(problems), max_batch):
         chunk = problems[s:s + max_batch]
-        t0 = time.perf_counter()
         db = DeviceBatch(chunk, config).stage().run()
-        x = db.fetch()
-        reports.extend(db.reports(x, time.perf_counter() - t0))
+        reports.extend(db.reports(db.fetch()))
     return reports
 
 
-def solve_tikhonov(problem, config: Optional[SolverConfig] = None) -> SolveReport:
-    """Solve one instance (ref: solver.py:58-78)."""
+def solve_tikhonov(problem, config=None) -> SolveReport:
+    """Solve one instance (ref: solver.py:58-78).  ``config`` may be our
+    SolverConfig, the reference's own ``toepreg.SolverConfig`` (five fields)
+    or None (defaults)."""
     return solve_tikhonov_batch([problem], config)[0]

@@ -24,16 +24,29 @@ def load_case(path):
     raw = {k: (v.item() if v.ndim == 0 else v) for k, v in d.items()}
     raw["variant"] = str(d["variant"])
     if "recipe" in d:
+        # "<generator call>[index]" or "<generator call>": regenerate the inputs
         r = str(d["recipe"])
-        if r.startswith("c2_rect"):
-            src = wl.c2_rect(nrhs=1, seed=0)
-            raw["T_gen"], raw["b"], raw["beta"] = src["T_gen"], src["b"][0], src["beta"]
-        elif r.startswith("c5_random"):
-            src = wl.c5_random(n=16384, count=1, seed=0)
-            raw["T_gen"], raw["b"], raw["beta"] = src["T_gen"][0], src["b"][0], src["beta"]
-        else:
+        call, idx = r, None
+        if r.endswith("]"):
+            call, idx = r[:r.rindex("[")], int(r[r.rindex("[") + 1:-1])
+        name = call[:call.index("(")]
+        if name not in wl.__all__:
             raise ValueError(r)
+        src = eval(call, {"__builtins__": {}}, {name: getattr(wl, name)})  # noqa: S307 (fixture recipe)
+        for key in ("T_gen", "L_gen", "G_col", "b", "normal_rhs", "beta", "L_rows"):
+            v = src.get(key)
+            if v is None:
+                continue
+            if idx is not None and isinstance(v, np.ndarray) and v.ndim == 2:
+                v = v[idx]
+            raw[key] = v
     return raw, d
+
+
+def case_config(tb, d, refine=1):
+    """SolverConfig of a fixture (fill policy recorded by make_golden_big)."""
+    fill = str(d["cfg_fill"]) if "cfg_fill" in d else "auto"
+    return tb.SolverConfig(fill=fill, refine=refine)
 
 
 def case_paths(pattern="*"):

@@ -21,17 +21,31 @@ import numpy as np
 import pytest
 
 import toepreg_oracle as O
-from conftest import GOLDEN, case_paths, load_case, rel
+from conftest import GOLDEN, case_config, case_paths, load_case, rel
 from paper_1302_6945_b200 import workloads as wl
 
 pytestmark = pytest.mark.gpu
 
 CASES = case_paths()
-ILL = ("c4_mini",)  # the reference itself fails on this one (cond ~ 1e8)
+# the reference itself fails on these (cond ~ 1e8 .. 7e8): its normal residual
+# is 1e-2 .. 0.24, so only "no exception, residual no worse" is meaningful
+ILL = ("c4_mini", "c4_full")
 
 
-def _solve(tb, raw, refine):
-    return tb.solve_tikhonov(wl.to_problem(raw, tb), tb.SolverConfig(refine=refine))
+def _solve(tb, raw, refine, d=None):
+    cfg = case_config(tb, d, refine) if d is not None else tb.SolverConfig(refine=refine)
+    return tb.solve_tikhonov(wl.to_problem(raw, tb), cfg)
+
+
+def _integers_exact(rep, d, name):
+    """Integer outputs of the direct solve equal the reference's exactly:
+    the degree ledger position by position, deferred count, depth, count."""
+    assert np.array_equal(rep.final_col_degrees, d["final_col_degrees"]), \
+        (name, rep.final_col_degrees, d["final_col_degrees"])
+    assert rep.diagnostics.difficult_points == int(d["difficult_points"]), name
+    assert rep.diagnostics.recursion_depth == int(d["recursion_depth"]), name
+    assert rep.diagnostics.conditions_total == int(d["conditions_total"]), name
+    assert rep.diagnostics.trim_overflow == 0, name
 
 
 @pytest.mark.parametrize("path", CASES, ids=lambda p: os.path.basename(p)[:-4])
@@ -39,14 +53,16 @@ def test_parity_with_reference_refined(gpu, path):
     tb = gpu
     raw, d = load_case(path)
     name = os.path.basename(path)[:-4]
-    rep = _solve(tb, raw, 1)
+    rep = _solve(tb, raw, 1, d)
     ref_exact = rel(d["x_hat"], d["x_exact"])
     gpu_exact = rel(rep.x_hat, d["x_exact"])
     gpu_ref = rel(rep.x_hat, d["x_hat"])
-    assert sorted(rep.final_col_degrees.tolist()) == sorted(d["final_col_degrees"].tolist())
-    assert rep.diagnostics.conditions_total == int(d["conditions_total"])
-    assert rep.diagnostics.recursion_depth == int(d["recursion_depth"])
+    _integers_exact(rep, d, name)
     assert rep.x_hat.dtype == np.complex128 and rep.x_hat.shape == d["x_hat"].shape
+    assert rep.relative_residual <= float(d["relative_residual"]) * 1.0001 + 1e-13, \
+        (name, rep.relative_residual, float(d["relative_residual"]))
+    if name in ILL:
+        return
     assert gpu_exact <= ref_exact * 1.0001 + 1e-15, (name, gpu_exact, ref_exact)
     if ref_exact <= 1e-9:
         assert gpu_exact <= 1e-12, (name, gpu_exact)
@@ -61,11 +77,10 @@ def test_single_pass_matches_reference_error_level(gpu, path):
     name = os.path.basename(path)[:-4]
     if name in ILL:
         pytest.skip("reference fails on this conditioning; see the refined test")
-    rep = _solve(tb, raw, 0)
+    rep = _solve(tb, raw, 0, d)
     ref_exact = rel(d["x_hat"], d["x_exact"])
     assert rel(rep.x_hat, d["x_exact"]) <= 3 * ref_exact + 1e-13, name
-    assert np.array_equal(np.sort(rep.final_col_degrees), np.sort(d["final_col_degrees"]))
-    assert rep.diagnostics.difficult_points == int(d["difficult_points"])
+    _integers_exact(rep, d, name)
     assert rep.relative_residual <= 3 * float(d["relative_residual"]) + 1e-14
 
 
@@ -455,3 +470,85 @@ def test_run_cg_equivalence_and_complexity_rows(gpu):
     assert len(rows) == 2 and all(r["mean_iters"] >= 1 and r["direct_max_err"] < 1e-9 for r in rows)
     rows, fits = ex.run_complexity(cfg)
     assert len(rows) == 2 and rows[0]["params"] == 127 and "l2" in fits
+
+
+def test_reference_five_field_config_accepted(gpu):
+    """The reference's SolverConfig has five fields (ref solver.py:39-45);
+    passing an object of exactly that shape works and equals refine=1."""
+    import dataclasses
+    tb = gpu
+
+    @dataclasses.dataclass(frozen=True)
+    class RefSolverConfig:  # stand-in with the reference's exact fields
+        n_lim: int = 256
+        pivot_threshold: float = 1e-8
+        fill: str = "auto"
+        paired: bool = True
+        force_even: bool = True
+
+    raw, d = load_case(os.path.join(GOLDEN, "cases", "c5_mini_sys0.npz"))
+    prob = wl.to_problem(raw, tb)
+    a = tb.solve_tikhonov(prob, RefSolverConfig())
+    b = tb.solve_tikhonov(prob, tb.SolverConfig())
+    c = tb.solve_tikhonov(prob)
+    assert np.array_equal(a.x_hat, b.x_hat) and np.array_equal(a.x_hat, c.x_hat)
+    assert np.array_equal(a.final_col_degrees, d["final_col_degrees"])
+    info = tb.plan_info(prob, RefSolverConfig())
+    assert info["order"] == 4096
+
+
+def test_wall_time_covers_the_solve_only(gpu):
+    """wall_time is the device time of assemble -> extract (+ refinement);
+    it excludes staging, the copy back and the residual evaluation
+    (ref solver.py:62-71) and is positive and below the host-observed time."""
+    import time
+    tb = gpu
+    raw = wl.c5_random(n=2048, count=1, seed=2)
+    prob = wl.to_problem(raw, tb, 0)
+    tb.solve_tikhonov(prob)  # warm (plan, graph capture)
+    t0 = time.perf_counter()
+    rep = tb.solve_tikhonov(prob)
+    host = time.perf_counter() - t0
+    assert 0.0 < rep.wall_time < host
+
+
+def test_host_abi_binding_from_integration_doc(gpu):
+    """Run the ctypes binding exactly as INTEGRATION.md prints it (the block
+    is extracted from the document and executed) on host buffers."""
+    import re
+    from conftest import ROOT
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    block = re.search(r"### ctypes binding a non-torch caller would use\s*```python\n(.*?)```", text, re.S)
+    assert block, "INTEGRATION.md lost its ctypes example"
+    code = block.group(1).replace('"paper_1302_6945_b200/libtoepreg_b200.so"',
+                                  repr(os.path.join(ROOT, "paper_1302_6945_b200", "libtoepreg_b200.so")))
+    ns = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)  # noqa: S102 (the documented binding)
+    raw, d = load_case(os.path.join(GOLDEN, "cases", "c5_mini_sys0.npz"))
+    x = ns["solve_l2_host"](raw["T_gen"], raw["beta"], raw["b"], int(raw["m"]), int(raw["n"]))
+    tb = gpu
+    ref = tb.solve_tikhonov(wl.to_problem(raw, tb)).x_hat
+    assert np.array_equal(x, ref)
+    assert rel(x, d["x_exact"]) < 1e-12
+
+
+def test_full_size_c5b_single_system(gpu):
+    """BASELINE config 5b: one l2 system of n = 2^22 (N = 2^23, 17 levels).
+    Checked through size-independent properties: the normal-equation residual
+    recomputed on the CPU by the oracle's FFT operator, the final degree
+    ledger, and agreement with an independent GPU solve (conjugate gradients
+    from zero to 1e-14)."""
+    tb = gpu
+    n = 1 << 22
+    raw = wl.c5_random(n=n, count=1, seed=0)
+    prob = wl.to_problem(raw, tb, 0)
+    rep = tb.solve_tikhonov(prob)
+    assert rep.diagnostics.trim_overflow == 0
+    assert rep.diagnostics.conditions_total == 2 * 2 * n
+    assert sorted(rep.final_col_degrees.tolist()) == [0, 1, 1, 1, 1]
+    y = O.normal_rhs(prob)
+    res = np.linalg.norm(O.normal_apply(prob, rep.x_hat) - y) / np.linalg.norm(y)
+    assert res < 1e-12 and abs(res - rep.relative_residual) < 1e-12
+    x_cg, it = tb.cg_solve(prob, tb.CGConfig(tolerance=1e-14))
+    assert 0 < it < 10 * n
+    assert rel(rep.x_hat, x_cg) < 1e-11

@@ -19,7 +19,8 @@ SMALL = [p for p in case_paths() if "full" not in os.path.basename(p)]
 @pytest.mark.parametrize("path", SMALL, ids=lambda p: os.path.basename(p)[:-4])
 def test_oracle_reproduces_reference_bitwise(path):
     raw, d = load_case(path)
-    r = O.solve(wl.to_problem(raw, tb))
+    fill = str(d["cfg_fill"]) if "cfg_fill" in d else "auto"
+    r = O.solve(wl.to_problem(raw, tb), fill=fill)
     assert np.array_equal(r["x_hat"], d["x_hat"])
     assert np.array_equal(r["final_col_degrees"], d["final_col_degrees"])
     dg = r["diagnostics"]
