@@ -73,6 +73,8 @@ typedef struct tr_diag {
   int32_t refine_cg_iterations; /* CG refinement iterations run (0: none / direct refinement) */
   double wall_time_s;           /* device time of the solve (assemble -> extract, + refinement),
                                    excluding the residual evaluation; the whole batch's time */
+  int32_t rescued;              /* 1: the direct solve failed under FP64 rounding (singular, or no
+                                   better than x = 0) and x comes from CG from zero (refine > 0) */
 } tr_diag;
 
 /* Bytes of device workspace tr_solve_batch needs for `batch` systems. */

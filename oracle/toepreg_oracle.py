@@ -49,6 +49,19 @@ TRIM_TOL = 1e-14             # ref:fftpoly.py:211
 GOLDEN = 0.6180339887498949  # ref:tanint.py:234
 
 
+# Test-only instrumentation (None = off; never changes the arithmetic):
+#   MARGINS: list receiving ("pivot", 1 - |phi_2nd| / |phi_1st|),
+#            ("defer", |phi_j| / (thr max|phi|)) per decision and
+#            ("check", self residual / tolerance) per leaf attempt, so the
+#            fixtures can record how close each discrete decision of the
+#            reference was to flipping under rounding;
+#   COMBINE_EXTENDED: False runs the tree products in float64 instead of
+#            long double (the reference's own rounding-path spread, SURVEY
+#            App. B "ref <-> ref with FP64 combine").
+MARGINS = None
+COMBINE_EXTENDED = True
+
+
 class OracleSingular(RuntimeError):
     """Mirror of ref:tanint.py:45 SingularSystemError."""
 
@@ -306,6 +319,11 @@ def sweep(cube, length, nodes, wrows, refs, degs, thr, may_defer, stats):
             cands = np.flatnonzero(degs == degs.min())
             j = int(cands[np.argmax(np.abs(phi[cands]))])
             bad = abs(phi[j]) < thr * amax
+            if MARGINS is not None:
+                a = np.sort(np.abs(phi[cands]))[::-1]
+                if a.size > 1:
+                    MARGINS.append(("pivot", float(1.0 - a[1] / a[0])))
+                MARGINS.append(("defer", float(abs(phi[j]) / (thr * amax))))
         if bad:
             if not may_defer:
                 raise OracleSingular("pivot underflow while absorbing a condition")
@@ -362,6 +380,8 @@ def leaf_basis(weights, nodes_all, idx, degs, thr):
         factor = max(factor, stats["scale"])
         coeffs = cube[:, :, :length].copy()
         res = self_residual(coeffs, nodes_all[idx], w_in, scale)
+        if MARGINS is not None:
+            MARGINS.append(("check", float(res / LEAF_CHECK_TOL)))
         if best is None or res < best[0]:
             best = (res, coeffs, d, deferred, factor)
         if best[0] <= LEAF_CHECK_TOL:
@@ -484,7 +504,7 @@ class _Run:
             vals = np.moveaxis(grid_eval(bl, a.order, offset=o, stride=st), -1, 0)
             self.w[:, idx, :] = np.einsum("rji,jik->rjk", self.w[:, idx, :], vals)
         br = self.node(right, st, depth + 1)
-        prod = trim_tail(matpoly_product(bl, br, extended=True)).copy()
+        prod = trim_tail(matpoly_product(bl, br, extended=COMBINE_EXTENDED)).copy()
         if self.trace is not None:
             self.trace.combines.append(dict(a=bl, b=br, out_untrimmed_len=bl.shape[2] + br.shape[2] - 1))
         cm = np.abs(prod).max(axis=(0, 2))

@@ -49,6 +49,7 @@ class TrDiag(C.Structure):
         ("trim_overflow", C.c_int32),
         ("refine_cg_iterations", C.c_int32),
         ("wall_time_s", C.c_double),
+        ("rescued", C.c_int32),
     ]
 
 

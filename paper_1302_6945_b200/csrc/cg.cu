@@ -94,11 +94,19 @@ __global__ void __launch_bounds__(CGT) cg_update_kernel(cplx* X, cplx* R, cplx* 
 
 // warm start from the direct solution x: r = y - A x, d = r; the target is
 // a 1e-8 reduction of the recursive residual, enough for the correction on
-// any system CG converges on (x error ~ cond(A) 1e-8 of the direct error)
-__global__ void __launch_bounds__(CGT) cg_warm_kernel(const cplx* X, cplx* R, cplx* D, const cplx* AX,
+// any system CG converges on (x error ~ cond(A) 1e-8 of the direct error).
+// Rescue: a system whose direct solve failed (status 3: singular under FP64
+// rounding where the reference's long-double products succeeded) or whose
+// direct solution is no better than zero (|y - A x| >= |y|, or not finite)
+// restarts from x = 0 instead; its CG is never abandoned for the direct
+// refinement and stops at the iteration cap (rescued = 1).  A system with a
+// zero right-hand side keeps status 3 (the operator itself is singular).
+__global__ void __launch_bounds__(CGT) cg_warm_kernel(cplx* X, cplx* R, cplx* D, const cplx* AX,
                                                       const cplx* Y, const double* beta_sq, long long beta_bs,
-                                                      int ridge, long long n, double* st, int* it) {
+                                                      int ridge, long long n, double* st, int* it, int* status,
+                                                      int* rescued) {
   __shared__ double sh[CGT / 32];
+  __shared__ int rescue_sh;
   const long long sys = blockIdx.x;
   const double b2 = ridge ? beta_sq[sys * beta_bs] : 0.0;
   double s = 0.0, sy = 0.0;
@@ -113,6 +121,19 @@ __global__ void __launch_bounds__(CGT) cg_warm_kernel(const cplx* X, cplx* R, cp
   }
   s = blk_sum(s, sh);
   sy = blk_sum(sy, sh);
+  if (threadIdx.x == 0) rescue_sh = sy > 0.0 && (status[sys] == 3 || !(s < sy));
+  __syncthreads();
+  const bool rescue = rescue_sh != 0;
+  if (rescue) {
+    for (long long i = threadIdx.x; i < n; i += CGT) {
+      const long long o = sys * n + i;
+      const cplx y = Y[o];
+      X[o] = cmk(0.0, 0.0);
+      R[o] = y;
+      D[o] = y;
+    }
+    s = sy;
+  }
   if (threadIdx.x == 0) {
     // 1e-8 of the initial residual, but not below the FP64 floor of the
     // residual itself (~1e-15 |y|): iterations past it no longer improve x
@@ -122,6 +143,8 @@ __global__ void __launch_bounds__(CGT) cg_warm_kernel(const cplx* X, cplx* R, cp
     st[sys * 4 + 2] = sqrt(s) > target;
     st[sys * 4 + 3] = s;  // initial rho (progress estimate on the host)
     it[sys] = 0;
+    rescued[sys] = rescue ? 1 : 0;
+    if (rescue) status[sys] = 0;
   }
 }
 
@@ -129,10 +152,14 @@ __global__ void __launch_bounds__(CGT) cg_warm_kernel(const cplx* X, cplx* R, cp
 // its own geometric rate so far projects past `cap` iterations (decided only
 // from its own residual history at fixed check points: deterministic and
 // independent of the batch it is solved in).
-__global__ void cg_check_kernel(double* st, const int* it, long long nsys, int cap) {
+__global__ void cg_check_kernel(double* st, const int* it, long long nsys, int cap, const int* rescued) {
   long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s >= nsys || st[s * 4 + 2] != 1.0) return;
   const int k = it[s];
+  if (rescued[s]) {  // CG is this system's solver: run to the cap, keep its x
+    if (k >= cap) st[s * 4 + 2] = 0.0;
+    return;
+  }
   const double r0 = sqrt(st[s * 4 + 3]), rk = sqrt(st[s * 4 + 0]), tgt = st[s * 4 + 1];
   const double rate = pow(rk / r0, 1.0 / k);
   const double need = rate < 1.0 ? log(tgt / rk) / log(rate) : 1e30;
@@ -310,15 +337,23 @@ int launch_cg_active(const double* st, long long nsys, int* any, cudaStream_t s)
   return 0;
 }
 
-int launch_cg_warm(const cplx* X, cplx* R, cplx* D, const cplx* AX, const cplx* Y, const double* beta_sq,
-                   long long beta_bs, int ridge, long long n, double* st, int* it, long long nsys, cudaStream_t s) {
-  { TrKTimer _kt(TRK_NORMAL, s); cg_warm_kernel<<<(unsigned)nsys, CGT, 0, s>>>(X, R, D, AX, Y, beta_sq, beta_bs, ridge, n, st, it); }
+int launch_cg_warm(cplx* X, cplx* R, cplx* D, const cplx* AX, const cplx* Y, const double* beta_sq,
+                   long long beta_bs, int ridge, long long n, double* st, int* it, long long nsys, int* status,
+                   int* rescued, cudaStream_t s) {
+  {
+    TrKTimer _kt(TRK_NORMAL, s);
+    cg_warm_kernel<<<(unsigned)nsys, CGT, 0, s>>>(X, R, D, AX, Y, beta_sq, beta_bs, ridge, n, st, it, status,
+                                                  rescued);
+  }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
 
-int launch_cg_check(double* st, const int* it, long long nsys, int cap, cudaStream_t s) {
-  { TrKTimer _kt(TRK_NORMAL, s); cg_check_kernel<<<(unsigned)((nsys + 127) / 128), 128, 0, s>>>(st, it, nsys, cap); }
+int launch_cg_check(double* st, const int* it, long long nsys, int cap, const int* rescued, cudaStream_t s) {
+  {
+    TrKTimer _kt(TRK_NORMAL, s);
+    cg_check_kernel<<<(unsigned)((nsys + 127) / 128), 128, 0, s>>>(st, it, nsys, cap, rescued);
+  }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }

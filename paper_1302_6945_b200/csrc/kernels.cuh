@@ -73,6 +73,7 @@ struct TrimArgs {
   long long out_sys, cap, cap_node;
   double* max_scale;   // [sys]
   int* trim_over;      // [sys] count of truncated (beyond bound) products
+  int debug = 0;       // TR_TRIM_DEBUG: print truncations (diagnostic)
 };
 int launch_trim_normalize(const TrimArgs& a, long long nsys, cudaStream_t st);
 
@@ -120,8 +121,9 @@ int launch_cg_update(cplx* X, cplx* R, cplx* D, const cplx* AD, const double* be
                      int ridge, long long n, double tol, double* st, int* it, long long nsys, cudaStream_t s,
                      long long ad_ls = 0);
 int launch_cg_active(const double* st, long long nsys, int* any, cudaStream_t s);
-int launch_cg_warm(const cplx* X, cplx* R, cplx* D, const cplx* AX, const cplx* Y, const double* beta_sq,
-                   long long beta_bs, int ridge, long long n, double* st, int* it, long long nsys, cudaStream_t s);
+int launch_cg_warm(cplx* X, cplx* R, cplx* D, const cplx* AX, const cplx* Y, const double* beta_sq,
+                   long long beta_bs, int ridge, long long n, double* st, int* it, long long nsys, int* status,
+                   int* rescued, cudaStream_t s);
 
 // ---- nonuniform Fourier sums (nufft.cu) ----
 // adjoint: y[d] = sum_k c_k exp(sign 2 pi i f_k d), d < n; forward: y[k] = sum_j x_j exp(sign 2 pi i f_k j)
@@ -129,7 +131,7 @@ int launch_nudft_adjoint(const double* f, const cplx* c, long long K, long long 
                          cudaStream_t st);
 int launch_nudft_forward(const double* f, const cplx* x, long long K, long long n, int sign, cplx* y,
                          cudaStream_t st);
-int launch_cg_check(double* st, const int* it, long long nsys, int cap, cudaStream_t s);
+int launch_cg_check(double* st, const int* it, long long nsys, int cap, const int* rescued, cudaStream_t s);
 int launch_cg_restore(cplx* X, const cplx* X0, const double* st, long long n, long long nsys, cudaStream_t s);
 int launch_add_masked(cplx* X, const cplx* D, const double* st, long long n, long long nsys, cudaStream_t s);
 int launch_refine_apply(cplx* X, const cplx* D, const int* status, const double* st, long long n, long long nsys,

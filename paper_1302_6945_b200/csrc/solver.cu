@@ -569,7 +569,7 @@ struct WS {
   cplx *S1, *S2, *S3;
   double* prof;
   unsigned long long* red;
-  int *cd, *dcount, *retried, *status, *trim_over, *blen, *cgit;
+  int *cd, *dcount, *retried, *status, *trim_over, *blen, *cgit, *rescued;
   int* diag_save;        // [5][nsys] + [8 nsys]: the direct solve's ledger/diagnostics across a refinement
   double* scale_save;    // [nsys]
   int2* defer;
@@ -616,6 +616,7 @@ size_t layout(const Plan& p, long long nsys, char* base, WS* w) {
   w->trim_over = c.take<int>((size_t)nsys);
   w->blen = c.take<int>((size_t)nsys);
   w->cgit = c.take<int>((size_t)nsys);
+  w->rescued = c.take<int>((size_t)nsys);
   w->diag_save = c.take<int>((size_t)nsys * 12);
   w->scale_save = c.take<double>((size_t)nsys);
   w->len_out = c.take<int>((size_t)nsys);
@@ -978,6 +979,8 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
         ta.cap_node = op.cap_out;
         ta.max_scale = w.max_scale + s0;
         ta.trim_over = w.trim_over + s0;
+        static const bool trim_dbg = getenv("TR_TRIM_DEBUG") != nullptr;
+        ta.debug = trim_dbg;
         TR_TRY(launch_trim_normalize(ta, ns, st));
       }
     }
@@ -1064,7 +1067,8 @@ int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
     if (cg_init) {
       TR_CUDA_CHECK(cudaMemcpyAsync(w.X0, w.X, sizeof(cplx) * nsys * n, cudaMemcpyDeviceToDevice, st));
       TR_TRY(normal_apply(p, nsys, w, sbs, w.X, st));
-      TR_TRY(launch_cg_warm(w.X, w.Rv, w.X2, w.AX, w.Y, in.beta_sq, in.beta_bs, add_ridge, n, cst, its, nsys, st));
+      TR_TRY(launch_cg_warm(w.X, w.Rv, w.X2, w.AX, w.Y, in.beta_sq, in.beta_bs, add_ridge, n, cst, its, nsys,
+                            w.status, w.rescued, st));
     }
     return 0;
   }
@@ -1082,7 +1086,7 @@ int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
                                 nsys, st));
       }
     }
-    TR_TRY(launch_cg_check(cst, its, nsys, cg_init, st));  // cg_init carries the iteration cap here
+    TR_TRY(launch_cg_check(cst, its, nsys, cg_init, w.rescued, st));  // cg_init carries the iteration cap here
     return 0;
   }
   if (phase == PH_REFINE || phase == PH_REFINE_CG) {
@@ -1131,9 +1135,11 @@ int read_diag(const Plan& p, long long nsys, const WS& w, cudaStream_t st, tr_di
     TR_CUDA_CHECK(cudaMemcpyAsync(tro.data(), w.trim_over, sizeof(int) * nsys, cudaMemcpyDeviceToHost, st));
     TR_CUDA_CHECK(cudaMemcpyAsync(ms.data(), w.max_scale, sizeof(double) * nsys, cudaMemcpyDeviceToHost, st));
     TR_CUDA_CHECK(cudaMemcpyAsync(nr.data(), w.nrm, sizeof(double) * 2 * nsys, cudaMemcpyDeviceToHost, st));
-    std::vector<int> cgit(nsys, 0);
-    if (cg_ran)
+    std::vector<int> cgit(nsys, 0), resc(nsys, 0);
+    if (cg_ran) {
       TR_CUDA_CHECK(cudaMemcpyAsync(cgit.data(), w.cgit, sizeof(int) * nsys, cudaMemcpyDeviceToHost, st));
+      TR_CUDA_CHECK(cudaMemcpyAsync(resc.data(), w.rescued, sizeof(int) * nsys, cudaMemcpyDeviceToHost, st));
+    }
     TR_CUDA_CHECK(cudaStreamSynchronize(st));
     for (long long s = 0; s < nsys; ++s) {
       tr_diag& dg = diag_host[s];
@@ -1152,6 +1158,10 @@ int read_diag(const Plan& p, long long nsys, const WS& w, cudaStream_t st, tr_di
       // trustworthy, report it instead of returning it silently
       if (tro[s] > 0 && dg.status == 0) dg.status = 6;
       dg.refine_cg_iterations = cgit[s];
+      dg.rescued = resc[s];
+      // a rescued system (direct solve singular or worse than x = 0, solved
+      // by CG from zero) must end better than x = 0, else it is singular
+      if (resc[s] && !(dg.relative_residual < 1.0)) dg.status = 3;
     }
   }
   return 0;

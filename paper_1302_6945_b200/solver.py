@@ -66,6 +66,7 @@ class TanIntDiagnostics:
     retried_leaves: int = 0
     trim_overflow: int = 0
     refine_cg_iterations: int = 0
+    rescued: bool = False
 
     def as_dict(self) -> dict:
         return {
@@ -290,7 +291,8 @@ class DeviceBatch:
                 max_column_scale=float(dg.max_column_scale),
                 retried_leaves=int(dg.retried_leaves),
                 trim_overflow=int(dg.trim_overflow),
-                refine_cg_iterations=int(dg.refine_cg_iterations))
+                refine_cg_iterations=int(dg.refine_cg_iterations),
+                rescued=bool(dg.rescued))
             out.append(SolveReport(
                 x_hat=np.array(x[i], dtype=np.complex128),
                 variant=self.variant, wall_time=float(dg.wall_time_s),

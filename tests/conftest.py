@@ -49,6 +49,25 @@ def case_config(tb, d, refine=1):
     return tb.SolverConfig(fill=fill, refine=refine)
 
 
+def decisions_robust(d):
+    """True when every discrete decision of the reference on this fixture is
+    far from its threshold (tests/golden/add_margins.py): no near-tie between
+    pivot candidates (exact structural ties, margin 0, are broken the same way
+    by both), no |phi_j| within 3x of the deferral threshold, no leaf
+    self-residual within 3x of the retry tolerance, and the reference's own
+    ledger survives a rounding change (float64 instead of long-double tree
+    products).  Then a run that differs from it only in rounding takes the
+    same decisions, and its integer outputs must equal the reference's."""
+    mp_ = float(d["margin_pivot"])
+    if not (mp_ == 0.0 or mp_ > 1e-6):
+        return False
+    if float(d["margin_defer"]) < 0.5 or float(d["margin_check"]) < 0.5:
+        return False
+    if "spread_col_degrees" in d and not np.array_equal(d["spread_col_degrees"], d["final_col_degrees"]):
+        return False
+    return True
+
+
 def case_paths(pattern="*"):
     return sorted(glob.glob(os.path.join(GOLDEN, "cases", pattern + ".npz")))
 

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import toepreg_oracle as O
-from conftest import GOLDEN, case_paths, load_case, rel
+from conftest import GOLDEN, case_paths, decisions_robust, load_case, rel
 import paper_1302_6945_b200 as tb
 from paper_1302_6945_b200 import workloads as wl
 
@@ -165,3 +165,16 @@ def test_oracle_nufft_setup_matches_reference():
     assert np.array_equal(nf.make_signal(256, 3, 0.02, rng), g["x"])
     reg = nf.second_difference_regularizer(5, 2.0)
     assert reg.gen[4] == 4.0 and reg.gen[3] == -2.0 and reg.gen[5] == -2.0
+
+
+def test_fixture_decision_margins_recorded():
+    """Every fixture carries the reference's decision margins
+    (tests/golden/add_margins.py); most are robust, so the GPU tests compare
+    their degree ledgers position by position."""
+    cases = case_paths()
+    for p in cases:
+        d = dict(np.load(p))
+        for key in ("margin_pivot", "margin_defer", "margin_check", "spread_exact"):
+            assert key in d, (p, key)
+    robust = [decisions_robust(dict(np.load(p))) for p in cases]
+    assert sum(robust) >= 0.6 * len(cases), sum(robust)
