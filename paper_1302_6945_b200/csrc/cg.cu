@@ -96,15 +96,16 @@ __global__ void __launch_bounds__(CGT) cg_update_kernel(cplx* X, cplx* R, cplx* 
 // a 1e-8 reduction of the recursive residual, enough for the correction on
 // any system CG converges on (x error ~ cond(A) 1e-8 of the direct error).
 // Rescue: a system whose direct solve failed (status 3: singular under FP64
-// rounding where the reference's long-double products succeeded) or whose
-// direct solution is no better than zero (|y - A x| >= |y|, or not finite)
+// rounding where the reference's long-double products succeeded; or a basis
+// product outgrew its planned length, trim_over > 0) or whose direct
+// solution is no better than zero (|y - A x| >= |y|, or not finite)
 // restarts from x = 0 instead; its CG is never abandoned for the direct
 // refinement and stops at the iteration cap (rescued = 1).  A system with a
 // zero right-hand side keeps status 3 (the operator itself is singular).
 __global__ void __launch_bounds__(CGT) cg_warm_kernel(cplx* X, cplx* R, cplx* D, const cplx* AX,
                                                       const cplx* Y, const double* beta_sq, long long beta_bs,
                                                       int ridge, long long n, double* st, int* it, int* status,
-                                                      int* rescued) {
+                                                      int* rescued, const int* trim_over) {
   __shared__ double sh[CGT / 32];
   __shared__ int rescue_sh;
   const long long sys = blockIdx.x;
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(CGT) cg_warm_kernel(cplx* X, cplx* R, cplx* D,
   }
   s = blk_sum(s, sh);
   sy = blk_sum(sy, sh);
-  if (threadIdx.x == 0) rescue_sh = sy > 0.0 && (status[sys] == 3 || !(s < sy));
+  if (threadIdx.x == 0) rescue_sh = sy > 0.0 && (status[sys] == 3 || trim_over[sys] > 0 || !(s < sy));
   __syncthreads();
   const bool rescue = rescue_sh != 0;
   if (rescue) {
@@ -339,11 +340,11 @@ int launch_cg_active(const double* st, long long nsys, int* any, cudaStream_t s)
 
 int launch_cg_warm(cplx* X, cplx* R, cplx* D, const cplx* AX, const cplx* Y, const double* beta_sq,
                    long long beta_bs, int ridge, long long n, double* st, int* it, long long nsys, int* status,
-                   int* rescued, cudaStream_t s) {
+                   int* rescued, const int* trim_over, cudaStream_t s) {
   {
     TrKTimer _kt(TRK_NORMAL, s);
     cg_warm_kernel<<<(unsigned)nsys, CGT, 0, s>>>(X, R, D, AX, Y, beta_sq, beta_bs, ridge, n, st, it, status,
-                                                  rescued);
+                                                  rescued, trim_over);
   }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;

@@ -123,7 +123,7 @@ int launch_cg_update(cplx* X, cplx* R, cplx* D, const cplx* AD, const double* be
 int launch_cg_active(const double* st, long long nsys, int* any, cudaStream_t s);
 int launch_cg_warm(cplx* X, cplx* R, cplx* D, const cplx* AX, const cplx* Y, const double* beta_sq,
                    long long beta_bs, int ridge, long long n, double* st, int* it, long long nsys, int* status,
-                   int* rescued, cudaStream_t s);
+                   int* rescued, const int* trim_over, cudaStream_t s);
 
 // ---- nonuniform Fourier sums (nufft.cu) ----
 // adjoint: y[d] = sum_k c_k exp(sign 2 pi i f_k d), d < n; forward: y[k] = sum_j x_j exp(sign 2 pi i f_k j)

@@ -1068,7 +1068,7 @@ int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
       TR_CUDA_CHECK(cudaMemcpyAsync(w.X0, w.X, sizeof(cplx) * nsys * n, cudaMemcpyDeviceToDevice, st));
       TR_TRY(normal_apply(p, nsys, w, sbs, w.X, st));
       TR_TRY(launch_cg_warm(w.X, w.Rv, w.X2, w.AX, w.Y, in.beta_sq, in.beta_bs, add_ridge, n, cst, its, nsys,
-                            w.status, w.rescued, st));
+                            w.status, w.rescued, w.trim_over, st));
     }
     return 0;
   }
@@ -1156,7 +1156,7 @@ int read_diag(const Plan& p, long long nsys, const WS& w, cudaStream_t st, tr_di
       dg.trim_overflow = tro[s];
       // a product longer than its planned capacity was cut: x is not
       // trustworthy, report it instead of returning it silently
-      if (tro[s] > 0 && dg.status == 0) dg.status = 6;
+      if (tro[s] > 0 && dg.status == 0 && !resc[s]) dg.status = 6;
       dg.refine_cg_iterations = cgit[s];
       dg.rescued = resc[s];
       // a rescued system (direct solve singular or worse than x = 0, solved
