@@ -92,7 +92,7 @@ def test_experiment_drivers_host_parts_match_reference():
     from paper_1302_6945_b200 import experiments as ex
     g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "stages", "experiments.json")))
     for variant in ex.VARIANTS:
-        rng = ex._trial_rng(2024, "accuracy", variant, 16, 1)
+        rng = ex._stream(2024, "accuracy", variant, 16, 1)
         p = ex.random_problem(variant, 16, rng)
         x = ex.complex_normal(rng, 16)
         parts = [p.T.gen if p.T is not None else np.zeros(0), p.L.gen if p.L is not None else np.zeros(0),
