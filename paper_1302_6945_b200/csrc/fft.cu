@@ -533,6 +533,18 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
   }
   tr_kernel_work(TRK_FFT, 16.0 * lines * (double)(in_len + n),
                  5.0 * lines * (double)n * std::log2((double)n));
+  // single pass on a cluster with TMA staging (fft_cl.cu): opt-in with
+  // TR_FFT_CL=1.  Measured (tools/fft_lines.py, B200): 0.9-1.1x the two-pass
+  // column kernels below (the DSMEM exchange and the cluster barriers cost
+  // more than the halved HBM traffic saves at these FP64-latency-bound
+  // rates), so the two-pass kernels stay the default.
+  static const bool cl_on = [] {
+    const char* e = getenv("TR_FFT_CL");
+    return e && e[0] == '1';
+  }();
+  if (cl_on && fft_cl_supported(n) &&
+      fft_cl_exec(n, in, in_ls, in_len, out, out_ls, lines, sign, p.twN, mul, mul_ls, mul_scale, st) == 0)
+    return 0;
   if (p.col) {
     // Lines go through both passes in chunks whose intermediate fits in L2
     // (the same scratch region for every chunk): pass B reads pass A's output

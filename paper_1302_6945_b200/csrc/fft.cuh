@@ -58,3 +58,11 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
 
 // Twiddle table exp(2 pi i k / n), k < n (cached, device memory).
 const cplx* twiddle_table(long long n);
+
+// Single-pass cluster / TMA transform (fft_cl.cu) for n in {8192, 12288,
+// 16384, 32768, 65536}: one HBM read and write per element.  Returns -1 when
+// the shape or device cannot use it (the caller falls back).
+bool fft_cl_supported(long long n);
+int fft_cl_exec(long long n, const cplx* in, long long in_ls, long long in_len, cplx* out, long long out_ls,
+                long long lines, int sign, const cplx* twN, const cplx* mul, long long mul_ls, double mul_scale,
+                cudaStream_t st);
