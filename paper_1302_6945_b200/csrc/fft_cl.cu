@@ -29,6 +29,7 @@
 
 #include "fft.cuh"
 #include "fft_bfly.cuh"
+#include "fft_smem.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -94,37 +95,6 @@ TR_D void tma_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: 
 TR_D void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 TR_D void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Length L = R1 R2 transforms of NL lines in shared memory, element e of
-// line l at base[l + e * ES] (lines contiguous: consecutive threads take
-// consecutive lines, conflict-free).
-//   stage1: radix R1 over e = j2 + R2 j1, times W_L^(j2 k1), in place; the
-//           value loaded for (l, e) passes through ld(l, e, x) first;
-//   stage2: radix R2 over e = R2 k1 + j2; after a barrier the outputs
-//           k = k1 + R1 k2 (natural order) go to st(l, k, v) -- any layout,
-//           since every read of the buffer is done by then.
-template <int R1, int R2, int NL, int ES, int NTH, class Ld>
-TR_D void stage1(cplx* base, int sign, const cplx* twL, Ld ld) {
-  constexpr int L = R1 * R2;
-  for (int g = threadIdx.x; g < NL * R2; g += NTH) {
-    const int l = g % NL, j2 = g / NL;
-    cplx v[R1];
-#pragma unroll
-    for (int j1 = 0; j1 < R1; ++j1) v[j1] = ld(l, j2 + R2 * j1, base[l + (j2 + R2 * j1) * ES]);
-    bfly_any<R1>(v, sign);
-    if (j2) {
-#pragma unroll
-      for (int k1 = 1; k1 < R1; ++k1) {
-        cplx w = __ldg(&twL[(j2 * k1) % L]);
-        if (sign < 0) w.y = -w.y;
-        v[k1] = cmul(v[k1], w);
-      }
-    }
-#pragma unroll
-    for (int k1 = 0; k1 < R1; ++k1) base[l + (j2 + R2 * k1) * ES] = v[k1];
-  }
-  __syncthreads();
-}
-
 // stage1 of pass B with the inter-pass twiddle W_n^(n2 k1), k1 = k0 + l:
 // for n2 = j2 + R2 j1 it is W_n^(k1 j2) W_n^(k1 R2 j1), the second factor a
 // product of at most log2(R1) table powers W_n^(k1 R2 2^b) (independent
@@ -163,32 +133,6 @@ TR_D void stage1w(cplx* base, int sign, const cplx* twL, const cplx* twN, int k0
     for (int k1b = 0; k1b < R1; ++k1b) base[l + (j2 + R2 * k1b) * ES] = v[k1b];
   }
   __syncthreads();
-}
-
-template <int R1, int R2, int NL, int ES, int NTH, class St>
-TR_D void stage2(const cplx* base, int sign, St st) {
-  constexpr int NG = (NL * R1 + NTH - 1) / NTH;
-  cplx v[NG][R2];
-#pragma unroll
-  for (int q = 0; q < NG; ++q) {
-    const int g = threadIdx.x + q * NTH;
-    if (NL * R1 % NTH == 0 || g < NL * R1) {
-      const int l = g % NL, k1 = g / NL;
-#pragma unroll
-      for (int j2 = 0; j2 < R2; ++j2) v[q][j2] = base[l + (R2 * k1 + j2) * ES];
-      bfly_any<R2>(v[q], sign);
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < NG; ++q) {
-    const int g = threadIdx.x + q * NTH;
-    if (NL * R1 % NTH == 0 || g < NL * R1) {
-      const int l = g % NL, k1 = g / NL;
-#pragma unroll
-      for (int k2 = 0; k2 < R2; ++k2) st(l, k1 + R1 * k2, v[q][k2]);
-    }
-  }
 }
 
 TR_D uint32_t mapa(uint32_t addr, int rank) {

@@ -77,6 +77,25 @@ struct TrimArgs {
 };
 int launch_trim_normalize(const TrimArgs& a, long long nsys, cudaStream_t st);
 
+// Fused combine of two leaf bases (combine_small.cu)
+struct CombineArgs {
+  const cplx* A;        // left basis [sys][PP][a_cap], La valid coefficients
+  long long a_sys, a_cap;
+  int La;
+  const cplx* B;        // right basis [sys][PP][b_cap], Lb valid coefficients
+  long long b_sys, b_cap;
+  int Lb;
+  cplx* out;            // [sys][PP][cap]
+  long long out_sys, cap, cap_node;
+  const cplx* twR;      // exp(2 pi i k / R)
+  double* max_scale;    // [sys]
+  int* trim_over;       // [sys]
+  int P, R;
+};
+// Transform length for a leaf pair of La, Lb coefficients (0: too large)
+int combine_small_R(int P, long long La, long long Lb);
+int launch_combine_small(const CombineArgs& a, long long nsys, cudaStream_t st);
+
 // ---- finish (finish.cu) ----
 struct CleanupArgs {
   cplx* B;             // root basis [sys][PP][cap] (normalized, len = Lroot bound)

@@ -411,6 +411,19 @@ __global__ void __launch_bounds__(P * TPR, 1) leaf_kernel(LeafArgs a) {
     if (best_res <= a.check_tol) break;
   }
 
+  // the parent's fused combine reads only len_eff coefficients: a nonzero
+  // coefficient past them is reported as a truncation (-> CG rescue)
+  if (a.len_eff > 0 && a.trim_over && best_len > a.len_eff) {
+    const cplx* o = a.out + (long long)sys * a.out_sys;
+    int nz = 0;
+    for (long long e = tid; e < (long long)P * P * (best_len - a.len_eff); e += NT) {
+      const long long ee = e / (best_len - a.len_eff), l = a.len_eff + e % (best_len - a.len_eff);
+      const cplx c = o[ee * a.cap + l];
+      nz |= (c.x != 0.0 || c.y != 0.0);
+    }
+    nz = __syncthreads_or(nz);
+    if (nz && tid == 0) a.trim_over[sys] += 1;
+  }
   if (tid == 0) {
 #pragma unroll
     for (int i = 0; i < P; ++i) a.cd[sys * 8 + i] = best_cd[i];

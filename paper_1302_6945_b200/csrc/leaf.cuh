@@ -41,6 +41,8 @@ struct LeafArgs {
   int* len_out;         // [sys] basis length (diagnostic), may be null
   long long* dbg = nullptr;  // [sys][16] clock64 trace (diagnostic), may be null
   const int* only = nullptr; // when set: only systems with only[sys] == -2 run (exact fallback)
+  int len_eff = 0;           // coefficients the parent's fused combine reads (0: all)
+  int* trim_over = nullptr;  // [sys] the exact kernel counts a basis longer than len_eff here
 };
 
 struct SplitState;

@@ -102,10 +102,16 @@ void tr_kernel_work(int cls, double bytes, double flops) {
 
 static void kernel_stats_drain() {
   std::lock_guard<std::mutex> lk(g_kmu);
+  // TR_LAUNCH_LOG=<path>: append every timed launch as "class tag ms" (diagnostic)
+  static FILE* log = [] {
+    const char* e = getenv("TR_LAUNCH_LOG");
+    return e ? fopen(e, "a") : (FILE*)nullptr;
+  }();
   for (KEvent& k : g_kpending) {
     cudaEventSynchronize(k.b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, k.a, k.b);
+    if (log) fprintf(log, "%d %lld %.6f\n", k.cls, k.tag, ms);
     g_kms[k.cls] += ms;
     g_kcount[k.cls] += 1;
     if (k.tag) {
@@ -117,6 +123,7 @@ static void kernel_stats_drain() {
     g_kpool.push_back(k.b);
   }
   g_kpending.clear();
+  if (log) fflush(log);
 }
 
 extern "C" int64_t tr_launch_count(void) { return g_launches.load(); }
@@ -240,6 +247,9 @@ struct Op {
   int wrap = 0;  // combine: R = La + Lb - 2, the top coefficient folded onto index 0 and corrected
   int K = 0, count = 0, M = 0, depth = 0;
   int dbound = 0;  // leaf: structural basis degree under water-filling, no deferrals
+  int len_eff = 0;  // leaf: coefficients its parent's fused combine reads (0: all); longer -> reported
+  int small = 0;    // combine of two leaves in one launch (combine_small.cu), transform length Rsm
+  int La_eff = 0, Lb_eff = 0, Rsm = 0;
   int nattempts = 1;
   int ord_stride[4] = {1, 1, 1, 1};
   int ord_rev[4] = {0, 0, 0, 0};
@@ -359,6 +369,23 @@ struct Builder {
     ns = stride;
     return true;
   }
+  // Coefficients a leaf's basis can have when the fused leaf kernel runs it:
+  // its register blocks (blocks_planned) hold 32 DB of them, and a leaf that
+  // outgrows them goes to the exact kernel, which reports a longer result.
+  int leaf_eff_len(const Op& op) const {
+    LeafArgs la{};
+    la.P = pl.P;
+    la.K = op.K;
+    la.M = op.M;
+    la.dbound = op.dbound;
+    la.noff = op.noff;
+    if (!leaf_fast_supported(la)) return 0;
+    const int full = (op.K + 1 + 31) / 32;
+    int b = op.dbound > 0 ? (op.dbound + 8) / 32 + 1 : full;
+    if (b > full) b = full;
+    return std::min(op.K + 1, 32 * b);
+  }
+  int last_leaf_op = -1;  // index of the op node() just planned when it was a leaf
   long long node(const std::vector<long long>& off, long long stride, int depth, int slot) {
     pl.depth = std::max(pl.depth, depth);
     long long count = (long long)pl.rows * (long long)off.size() * (pl.N / stride);
@@ -398,6 +425,7 @@ struct Builder {
       }
       op.dbound = leaf_dbound((int)count);
       pl.ops.push_back(op);
+      last_leaf_op = (int)pl.ops.size() - 1;
       pl.leaves += 1;
       pl.Kmax = std::max<long long>(pl.Kmax, count);
       waterfill(count);
@@ -408,7 +436,9 @@ struct Builder {
     }
     int start_min = ms.front();
     int sl = slot_for(depth + 1, 0), sr = slot_for(depth + 1, 1);
+    last_leaf_op = -1;
     long long ca = node(left, ns, depth + 1, sl);
+    const int leaf_a = last_leaf_op;
     Op up;
     up.kind = OP_UPDATE;
     up.o0 = right[0];
@@ -420,7 +450,10 @@ struct Builder {
     up.depth = depth;
     pl.ops.push_back(up);
     pl.cnt_max = std::max(pl.cnt_max, (long long)up.noff * (pl.N / ns));
+    last_leaf_op = -1;
     long long cb = node(right, ns, depth + 1, sr);
+    const int leaf_b = last_leaf_op;
+    last_leaf_op = -1;
     long long bound = (long long)ms.back() - start_min + 1;
     Op cm;
     cm.kind = OP_COMBINE;
@@ -444,6 +477,23 @@ struct Builder {
       }
     }
     pl.Rmax = std::max(pl.Rmax, cm.R + cm.wrap);
+    // two leaves: one fused launch on their effective lengths (TR_SMALL_COMBINE=0: off)
+    static const bool small_on = [] {
+      const char* e = getenv("TR_SMALL_COMBINE");
+      return !(e && e[0] == '0');
+    }();
+    if (small_on && leaf_a >= 0 && leaf_b >= 0) {
+      const int la = leaf_eff_len(pl.ops[leaf_a]), lb = leaf_eff_len(pl.ops[leaf_b]);
+      const int rs = (la > 0 && lb > 0) ? combine_small_R(pl.P, la, lb) : 0;
+      if (rs > 0) {
+        cm.small = 1;
+        cm.La_eff = la;
+        cm.Lb_eff = lb;
+        cm.Rsm = rs;
+        pl.ops[leaf_a].len_eff = la;
+        pl.ops[leaf_b].len_eff = lb;
+      }
+    }
     if (getenv("TR_PLAN_DEBUG"))
       fprintf(stderr, "combine depth %d: La %lld Lb %lld -> %lld, R %lld%s\n", depth, ca, cb, cm.cap_out, cm.R,
               cm.wrap ? " (wrapped)" : "");
@@ -536,6 +586,10 @@ int ensure_fft(Plan* p) {
   for (const Op& op : p->ops) {
     if (op.kind == OP_UPDATE) sizes.push_back(p->N / op.stride);
     if (op.kind == OP_COMBINE) sizes.push_back(op.R);
+    if (op.kind == OP_COMBINE && op.small && !twiddle_table(op.Rsm)) {
+      tr_set_error("twiddle table allocation failed (R=%d)", op.Rsm);
+      return 4;
+    }
   }
   for (long long s : sizes) {
     if (p->fft.count(s)) continue;
@@ -881,6 +935,7 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
       la.count = op.count;
       la.K = op.K;
       la.dbound = op.dbound;
+      la.len_eff = op.len_eff;
       la.nattempts = op.nattempts;
       for (int i = 0; i < 4; ++i) {
         la.ord_stride[i] = op.ord_stride[i];
@@ -902,6 +957,7 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
       la.status = w.status;
       la.res_out = w.res_out;
       la.len_out = w.len_out;
+      la.trim_over = w.trim_over;
       // TR_LEAF_TRACE=<file>: per-leaf clock64 traces of every CTA (diagnostic)
       static const char* trace_path = getenv("TR_LEAF_TRACE");
       static long long* trace_buf = nullptr;
@@ -942,6 +998,26 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
         TR_TRY(launch_apply_update(w.W + s0 * w_sys, w_sys, w.S1, rows, P, op.o0, op.o1, op.noff, op.stride,
                                    cnt, ns, st));
       }
+    } else if (op.small) {
+      CombineArgs cm;
+      cm.P = P;
+      cm.R = op.Rsm;
+      cm.A = w.slot[op.slot_a];
+      cm.a_cap = p.slot_cap[op.slot_a];
+      cm.a_sys = (long long)PP * cm.a_cap;
+      cm.La = op.La_eff;
+      cm.B = w.slot[op.slot_b];
+      cm.b_cap = p.slot_cap[op.slot_b];
+      cm.b_sys = (long long)PP * cm.b_cap;
+      cm.Lb = op.Lb_eff;
+      cm.cap = p.slot_cap[op.slot_out];
+      cm.out_sys = (long long)PP * cm.cap;
+      cm.out = w.slot[op.slot_out];
+      cm.cap_node = op.cap_out;
+      cm.twR = twiddle_table(op.Rsm);
+      cm.max_scale = w.max_scale;
+      cm.trim_over = w.trim_over;
+      TR_TRY(launch_combine_small(cm, nsys, st));
     } else {
       long long R = op.R;
       long long ca = p.slot_cap[op.slot_a], cb = p.slot_cap[op.slot_b];
