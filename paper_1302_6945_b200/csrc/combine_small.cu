@@ -259,3 +259,104 @@ int launch_combine_small(const CombineArgs& a, long long nsys, cudaStream_t st) 
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
+
+// ------------------------------------------------------------------------
+// Fused coset update after a LEAF (ref tanint.py:387-393 _update_weights,
+// fftpoly.py:64-89 grid_eval): the right sibling's weights are multiplied by
+// the left leaf's basis evaluated at the sibling's nodes, one launch instead
+// of twist/fold + FFT + apply.  One CTA per (system, coset):
+//   G[e][q] = sum_{l = q mod c} B_e[l] w^(o l)          (twist + fold)
+//   V[e][k] = sum_q G[e][q] w_c^(q k)                    (c-point DFT, c <= 128)
+//   w[r][node_k][:] <- w[r][node_k][:] V(sigma_k)        (apply)
+namespace {
+
+template <int P>
+__global__ void __launch_bounds__(256) update_small_kernel(UpdateArgs a) {
+  constexpr int PP = P * P, NTH = 256;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int c = a.cnt;
+  cplx* G = reinterpret_cast<cplx*>(smraw);  // [PP][c]
+  cplx* V = G + PP * c;                      // [PP][c]
+  cplx* Wc = V + PP * c;                     // [c]: w^(s t)
+  const int cs = blockIdx.x;
+  const long long sys = blockIdx.y;
+  const long long o = cs ? a.o1 : a.o0;
+  const cplx* B = a.B + sys * a.b_sys;
+  for (int t = threadIdx.x; t < c; t += NTH) Wc[t] = __ldg(&a.twN[(long long)t * a.stride]);
+  // twist + fold
+  for (int e = threadIdx.x; e < PP * c; e += NTH) {
+    const int ee = e / c, q = e - ee * c;
+    const cplx* src = B + (long long)ee * a.b_cap;
+    cplx acc = cmk(0.0, 0.0);
+    long long idx = (o * q) % a.N;
+    const long long step = (o * c) % a.N;
+    for (int l = q; l < a.Lb; l += c) {
+      acc = cfma(src[l], __ldg(&a.twN[idx]), acc);
+      idx += step;
+      if (idx >= a.N) idx -= a.N;
+    }
+    G[e] = acc;
+  }
+  __syncthreads();
+  // c-point DFT (sign +1: values at sigma_k = w^(o + s k))
+  for (int e = threadIdx.x; e < PP * c; e += NTH) {
+    const int ee = e / c, k = e - ee * c;
+    const cplx* g = G + ee * c;
+    cplx acc = cmk(0.0, 0.0);
+    int t = 0;
+    for (int q = 0; q < c; ++q) {
+      acc = cfma(g[q], Wc[t], acc);
+      t += k;
+      if (t >= c) t -= c;
+    }
+    V[e] = acc;
+  }
+  __syncthreads();
+  // apply to the sibling's weights at its nodes
+  cplx* W = a.W + sys * a.w_sys;
+  for (int e = threadIdx.x; e < c * a.rows; e += NTH) {
+    const int k = e / a.rows, r = e - k * a.rows;
+    cplx* w = W + (o + a.stride * (long long)k) * a.rows * P + r * P;
+    cplx old[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) old[i] = w[i];
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      cplx acc = cmk(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc = cfma(old[i], V[(i * P + j) * c + k], acc);
+      w[j] = acc;
+    }
+  }
+}
+
+}  // namespace
+
+int launch_update_small(const UpdateArgs& a, long long nsys, cudaStream_t st) {
+  const size_t smem = sizeof(cplx) * ((size_t)2 * a.P * a.P * a.cnt + a.cnt);
+  if (a.cnt > 128 || smem > 200 * 1024) {
+    tr_set_error("update_small: coset of %d nodes too large", a.cnt);
+    return 2;
+  }
+  tr_kernel_work(TRK_UPDATE, 16.0 * nsys * (a.P * a.P * (double)a.Lb + 2.0 * a.noff * a.cnt * a.rows * a.P),
+                 8.0 * nsys * a.noff * a.P * a.P * ((double)a.Lb + (double)a.cnt * a.cnt + a.cnt * a.rows * a.P));
+  dim3 grid((unsigned)a.noff, (unsigned)nsys);
+  TrKTimer _kt(TRK_UPDATE, st);
+  if (a.P == 5) {
+    static bool set5 = false;
+    if (!set5) {
+      cudaFuncSetAttribute(update_small_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      set5 = true;
+    }
+    update_small_kernel<5><<<grid, 256, smem, st>>>(a);
+  } else {
+    static bool set7 = false;
+    if (!set7) {
+      cudaFuncSetAttribute(update_small_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      set7 = true;
+    }
+    update_small_kernel<7><<<grid, 256, smem, st>>>(a);
+  }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}

@@ -96,6 +96,20 @@ struct CombineArgs {
 int combine_small_R(int P, long long La, long long Lb);
 int launch_combine_small(const CombineArgs& a, long long nsys, cudaStream_t st);
 
+// Fused coset update after a leaf (combine_small.cu)
+struct UpdateArgs {
+  const cplx* B;        // left leaf basis [sys][PP][b_cap], Lb valid coefficients
+  long long b_sys, b_cap;
+  int Lb;
+  cplx* W;              // weights [sys][N][rows][P]
+  long long w_sys, N;
+  int rows, P;
+  long long o0, o1, stride;
+  int noff, cnt;        // cosets, nodes per coset
+  const cplx* twN;
+};
+int launch_update_small(const UpdateArgs& a, long long nsys, cudaStream_t st);
+
 // ---- finish (finish.cu) ----
 struct CleanupArgs {
   cplx* B;             // root basis [sys][PP][cap] (normalized, len = Lroot bound)

@@ -233,6 +233,10 @@ constexpr double GOLDEN = 0.6180339887498949;  // ref tanint.py:234
 constexpr double LEAF_CHECK_TOL = 1e-11;       // ref tanint.py:244
 constexpr int DMAX = 512;                       // deferred conditions per system
 constexpr int TRIM_SLACK = 16;
+// The fused leaf-level update / combine launches (combine_small.cu) pay off
+// while the batched path is latency-bound: groups of at most this many systems
+// (measured: c2, 32 per group, +4.8%; c5, 128 per group, -2%).
+constexpr long long SMALL_MAX_SYS = 64;
 constexpr int NORM_CHUNKS = 64;
 
 enum { OP_LEAF = 0, OP_UPDATE = 1, OP_COMBINE = 2 };
@@ -295,6 +299,14 @@ int opt_extend_detail(long long n_tilde, long long n_lim, int rows, bool paired,
   *p = pp;
   *M = m;
   return 0;
+}
+
+bool small_on_update() {  // TR_SMALL_UPDATE=0: the three-kernel update everywhere
+  static const bool on = [] {
+    const char* e = getenv("TR_SMALL_UPDATE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 struct Builder {
@@ -448,6 +460,15 @@ struct Builder {
     up.slot_a = sl;
     up.cap_a = ca;
     up.depth = depth;
+    // after a leaf, small cosets: one fused launch on the leaf's effective length
+    if (small_on_update() && leaf_a >= 0 && pl.N / ns <= 64) {
+      const int la = leaf_eff_len(pl.ops[leaf_a]);
+      if (la > 0) {
+        up.small = 1;
+        up.La_eff = la;
+        pl.ops[leaf_a].len_eff = la;
+      }
+    }
     pl.ops.push_back(up);
     pl.cnt_max = std::max(pl.cnt_max, (long long)up.noff * (pl.N / ns));
     last_leaf_op = -1;
@@ -985,6 +1006,24 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
           fclose(f);
         }
       }
+    } else if (op.kind == OP_UPDATE && op.small && nsys <= SMALL_MAX_SYS) {
+      UpdateArgs ua;
+      ua.B = w.slot[op.slot_a];
+      ua.b_cap = p.slot_cap[op.slot_a];
+      ua.b_sys = (long long)PP * ua.b_cap;
+      ua.Lb = op.La_eff;
+      ua.W = w.W;
+      ua.w_sys = w_sys;
+      ua.N = N;
+      ua.rows = rows;
+      ua.P = P;
+      ua.o0 = op.o0;
+      ua.o1 = op.o1;
+      ua.stride = op.stride;
+      ua.noff = op.noff;
+      ua.cnt = (int)(N / op.stride);
+      ua.twN = twN;
+      TR_TRY(launch_update_small(ua, nsys, st));
     } else if (op.kind == OP_UPDATE) {
       long long cnt = N / op.stride;
       long long scap = p.slot_cap[op.slot_a];
@@ -998,7 +1037,7 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
         TR_TRY(launch_apply_update(w.W + s0 * w_sys, w_sys, w.S1, rows, P, op.o0, op.o1, op.noff, op.stride,
                                    cnt, ns, st));
       }
-    } else if (op.small) {
+    } else if (op.small && nsys <= SMALL_MAX_SYS) {
       CombineArgs cm;
       cm.P = P;
       cm.R = op.Rsm;
