@@ -118,8 +118,8 @@ int tr_solve_batch_host(const tr_desc* d, int64_t batch,
  * (replaces toepreg.solver.cg_solve, pkg/src/toepreg/solver.py:184-215).
  * Same inputs as tr_solve_batch; max_iterations <= 0 means the reference
  * default max(10 n, 100); systems stop individually at
- * ||r|| <= tolerance ||rhs||; time_budget > 0 is checked after completed
- * iterations.  x_out [batch][n] device, iterations [batch] host.  The
+ * ||r|| <= tolerance ||rhs||; time_budget >= 0 is checked after completed
+ * iterations (time_budget < 0: none).  x_out [batch][n] device, iterations [batch] host.  The
  * workspace is tr_cg_workspace_bytes(d, batch). */
 size_t tr_cg_workspace_bytes(const tr_desc* d, int64_t batch);
 int tr_cg_batch(const tr_desc* d, int64_t batch,

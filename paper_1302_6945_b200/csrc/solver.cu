@@ -1708,7 +1708,9 @@ extern "C" int tr_cg_batch(const tr_desc* d, int64_t batch, const double* T_gen,
   int* any = w.dcount;
   TR_TRY(launch_cg_init(w.X, w.Rv, w.X2, w.Y, n, cst, its, batch, st));
   const long long limit = max_iterations > 0 ? max_iterations : std::max<long long>(10 * n, 100);
-  const int chunk = time_budget > 0.0 ? 1 : 16;
+  // time_budget < 0: none; >= 0 is checked after every completed iteration
+  // (0 stops after the first one, as the reference, solver.py:211)
+  const int chunk = time_budget >= 0.0 ? 1 : 16;
   const int ridge = p->variant == TR_L2;
   const auto t0 = std::chrono::steady_clock::now();
   long long done = 0;
@@ -1725,7 +1727,7 @@ extern "C" int tr_cg_batch(const tr_desc* d, int64_t batch, const double* T_gen,
     TR_CUDA_CHECK(cudaMemcpyAsync(&host_any, any, sizeof(int), cudaMemcpyDeviceToHost, st));
     TR_CUDA_CHECK(cudaStreamSynchronize(st));
     if (!host_any) break;
-    if (time_budget > 0.0) {
+    if (time_budget >= 0.0) {
       const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       if (el >= time_budget) break;
     }

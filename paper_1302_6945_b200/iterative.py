@@ -103,7 +103,8 @@ def _cg(st: _Staged, cfg: CGConfig) -> Tuple[np.ndarray, np.ndarray]:
     rc = lib.tr_cg_batch(C.byref(db.desc), db.batch, *st.operands(),
                          st.ptr("rhs"), db.bs["rhs"], int(db.rhs_is_normal),
                          int(cfg.max_iterations or 0), float(cfg.tolerance),
-                         float(cfg.time_budget or 0.0), C.c_void_p(x.data_ptr()), its,
+                         -1.0 if cfg.time_budget is None else float(cfg.time_budget),
+                         C.c_void_p(x.data_ptr()), its,
                          C.c_void_p(st.ws.data_ptr()), C.c_size_t(st.ws_bytes), C.c_void_p(s))
     _check(rc)
     xh = x.cpu().numpy().view(np.complex128).reshape(db.batch, db.n).copy()
@@ -115,7 +116,10 @@ def cg_solve(problem, config: CGConfig = None, operator: NormalOperator = None):
     cfg = config or CGConfig()
     if cfg.max_iterations is not None and cfg.max_iterations <= 0:
         return np.zeros(problem.n, dtype=np.complex128), 0
-    st = operator._st if operator is not None else _Staged([problem])
+    # the operator's staged operands are reused only for the problem it was
+    # built on (ref solver.py:181-215 applies `operator` to `problem`'s rhs)
+    reuse = operator is not None and operator.problem is problem
+    st = operator._st if reuse else _Staged([problem])
     x, its = _cg(st, cfg)
     if operator is not None:
         operator.transforms += operator._per_apply * int(its[0])

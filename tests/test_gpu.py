@@ -400,6 +400,14 @@ def test_cg_edge_cases(gpu):
     raw = wl.random_problem("l2", 64, rng)
     x, it = tb.cg_solve(wl.to_problem(raw, tb), tb.CGConfig(time_budget=1e-9))
     assert it == 1  # the budget is checked after a completed iteration
+    x, it = tb.cg_solve(wl.to_problem(raw, tb), tb.CGConfig(time_budget=0.0))
+    assert it == 1  # a zero budget still runs one iteration (ref solver.py:211)
+    # an operator built on another problem does not replace this problem's data
+    other = wl.to_problem(wl.random_problem("l2", 64, rng), tb)
+    mine = wl.to_problem(raw, tb)
+    xa, ita = tb.cg_solve(mine, tb.CGConfig(max_iterations=7), operator=tb.NormalOperator(other))
+    xb, itb = tb.cg_solve(mine, tb.CGConfig(max_iterations=7))
+    assert ita == itb == 7 and np.array_equal(xa, xb)
     x, it = tb.cg_solve(wl.to_problem(raw, tb), tb.CGConfig(max_iterations=0))
     assert it == 0
 
