@@ -111,13 +111,25 @@ def _cg(st: _Staged, cfg: CGConfig) -> Tuple[np.ndarray, np.ndarray]:
     return xh, np.array(its[:], dtype=np.int64)
 
 
+def _same_matrix(p, q) -> bool:
+    def gen(spec):
+        return None if spec is None else (spec.rows if hasattr(spec, "rows") else spec.order,
+                                          np.asarray(spec.gen).tobytes())
+    return (p.variant == q.variant and gen(p.T) == gen(q.T) and gen(p.L) == gen(q.L)
+            and gen(p.G) == gen(q.G) and (p.beta or 0) == (q.beta or 0))
+
+
 def cg_solve(problem, config: CGConfig = None, operator: NormalOperator = None):
     """Plain conjugate gradients from a zero start.  Returns (x, iterations)."""
     cfg = config or CGConfig()
     if cfg.max_iterations is not None and cfg.max_iterations <= 0:
         return np.zeros(problem.n, dtype=np.complex128), 0
-    # the operator's staged operands are reused only for the problem it was
-    # built on (ref solver.py:181-215 applies `operator` to `problem`'s rhs)
+    # ref solver.py:181-215 applies `operator` to `problem`'s right-hand side:
+    # an operator of the same normal matrix (same T / L / G / beta) is
+    # equivalent to staging `problem` itself; another matrix is refused
+    if operator is not None and operator.problem is not problem:
+        if not _same_matrix(operator.problem, problem):
+            raise ValueError("operator was built for a different normal matrix")
     reuse = operator is not None and operator.problem is problem
     st = operator._st if reuse else _Staged([problem])
     x, its = _cg(st, cfg)

@@ -402,12 +402,17 @@ def test_cg_edge_cases(gpu):
     assert it == 1  # the budget is checked after a completed iteration
     x, it = tb.cg_solve(wl.to_problem(raw, tb), tb.CGConfig(time_budget=0.0))
     assert it == 1  # a zero budget still runs one iteration (ref solver.py:211)
-    # an operator built on another problem does not replace this problem's data
-    other = wl.to_problem(wl.random_problem("l2", 64, rng), tb)
+    # the operator applies to THIS problem's right-hand side (ref solver.py:181-215):
+    # an operator of the same matrix built for another rhs gives the same result,
+    # one of another matrix is refused
     mine = wl.to_problem(raw, tb)
-    xa, ita = tb.cg_solve(mine, tb.CGConfig(max_iterations=7), operator=tb.NormalOperator(other))
+    twin = dict(raw, b=np.asarray(raw["b"]) * 2.0)
+    xa, ita = tb.cg_solve(mine, tb.CGConfig(max_iterations=7), operator=tb.NormalOperator(wl.to_problem(twin, tb)))
     xb, itb = tb.cg_solve(mine, tb.CGConfig(max_iterations=7))
     assert ita == itb == 7 and np.array_equal(xa, xb)
+    other = wl.to_problem(wl.random_problem("l2", 64, rng), tb)
+    with pytest.raises(ValueError):
+        tb.cg_solve(mine, operator=tb.NormalOperator(other))
     x, it = tb.cg_solve(wl.to_problem(raw, tb), tb.CGConfig(max_iterations=0))
     assert it == 0
 
