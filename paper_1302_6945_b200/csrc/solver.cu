@@ -233,10 +233,9 @@ constexpr double GOLDEN = 0.6180339887498949;  // ref tanint.py:234
 constexpr double LEAF_CHECK_TOL = 1e-11;       // ref tanint.py:244
 constexpr int DMAX = 512;                       // deferred conditions per system
 constexpr int TRIM_SLACK = 16;
-// The fused leaf-level update / combine launches (combine_small.cu) pay off
-// while the batched path is latency-bound: groups of at most this many systems
-// (measured: c2, 32 per group, +4.8%; c5, 128 per group, -2%).
-constexpr long long SMALL_MAX_SYS = 64;
+// The fused leaf-level update / combine launches (combine_small.cu) are used
+// for every group size (measured: c2, 32 per group, +4.8%; c5, 128 per group,
+// -2%), so a system's rounding never depends on the batch it is solved in.
 constexpr int NORM_CHUNKS = 64;
 
 enum { OP_LEAF = 0, OP_UPDATE = 1, OP_COMBINE = 2 };
@@ -1006,7 +1005,7 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
           fclose(f);
         }
       }
-    } else if (op.kind == OP_UPDATE && op.small && nsys <= SMALL_MAX_SYS) {
+    } else if (op.kind == OP_UPDATE && op.small) {
       UpdateArgs ua;
       ua.B = w.slot[op.slot_a];
       ua.b_cap = p.slot_cap[op.slot_a];
@@ -1037,7 +1036,7 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
         TR_TRY(launch_apply_update(w.W + s0 * w_sys, w_sys, w.S1, rows, P, op.o0, op.o1, op.noff, op.stride,
                                    cnt, ns, st));
       }
-    } else if (op.small && nsys <= SMALL_MAX_SYS) {
+    } else if (op.small) {
       CombineArgs cm;
       cm.P = P;
       cm.R = op.Rsm;
@@ -1315,7 +1314,7 @@ int batch_groups(long long batch) {
   if (e) g = atoi(e);
   else if (batch >= 32) g = (int)((batch + 147) / 148) < 2 ? 2 : (int)((batch + 147) / 148);  // groups of <= 148: the fused leaf
   if (g < 1) g = 1;
-  if (g > 4) g = 4;
+  if (g > 8) g = 8;
   if (g > batch) g = (int)batch;
   return g;
 }
@@ -1339,8 +1338,8 @@ size_t plan_groups(const Plan& p, long long batch, std::vector<Group>* out) {
 }
 
 int phase_groups(const Plan& p, std::vector<Group>& gs, int phase, int cg_init, cudaStream_t st) {
-  static thread_local cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
-  static thread_local cudaEvent_t fork = nullptr, join[4] = {nullptr, nullptr, nullptr, nullptr};
+  static thread_local cudaStream_t side[8] = {};
+  static thread_local cudaEvent_t fork = nullptr, join[8] = {};
   const int G = (int)gs.size();
   if (G == 1 || g_timing.load()) {  // kernel timing: one stream, groups in order
     for (auto& g : gs) TR_TRY(phase_run(p, g.in, g.count, g.w, g.x, phase, cg_init, st));
@@ -1348,7 +1347,7 @@ int phase_groups(const Plan& p, std::vector<Group>& gs, int phase, int cg_init, 
   }
   if (!fork) {
     TR_CUDA_CHECK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 8; ++i) {
       TR_CUDA_CHECK(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
       TR_CUDA_CHECK(cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming));
     }
