@@ -1,4 +1,5 @@
 #include <tuple>
+#include <algorithm>
 #include <stdlib.h>
 #include <cmath>
 // Batched complex128 multi-pass Stockham FFT (see fft.cuh).
@@ -6,6 +7,7 @@
 #include "kernels.cuh"
 
 extern thread_local long long g_fft_tag;
+thread_local int g_fft_groups = 0;  // set while a solve enqueues work for several concurrent stream groups
 #include "fft_fast.cuh"
 
 #include <math.h>
@@ -546,6 +548,81 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
       fft_cl_exec(n, in, in_ls, in_len, out, out_ls, lines, sign, p.twN, mul, mul_ls, mul_scale, st) == 0)
     return 0;
   if (p.col) {
+    // Both passes in one cluster launch (fft_col.cu fft_col2_kernel), opt-in
+    // with TR_FFT_C2=1 (one cluster per line) or 2 (persistent clusters).
+    // Measured on B200 (tools/fft_c2.py, tools/fft_graph_lat.py): 1.3-1.55x the
+    // chunked launches on transforms of hundreds of lines run alone (32768 x
+    // 3200: 1484 -> 2310 GB/s), but no faster on the few-line transforms of a
+    // single system, and inside a solve whose batch is split into stream
+    // groups the long cluster launches delay the other groups' leaf sweeps
+    // (which need whole SMs): c2 34.7 -> 37.1 ms, c5 360 -> 372 ms per step.
+    // The chunked launches below therefore stay the default.
+    static const bool c2_on = [] {
+      const char* e = getenv("TR_FFT_C2");
+      return e && e[0] != '0';
+    }();
+    static const bool c2_force = [] {
+      const char* e = getenv("TR_FFT_C2_GROUPS");  // 1: also with concurrent stream groups
+      return e && e[0] == '1';
+    }();
+    static const long long c2_only = [] {
+      const char* e = getenv("TR_FFT_C2_ONLY");  // diagnostic: fuse only this length
+      return e ? atoll(e) : 0LL;
+    }();
+    // (a batch split into stream groups keeps the chunked launches: their short
+    // kernels interleave with the other groups' leaf sweeps, which need whole SMs
+    // and would otherwise wait behind a long cluster launch -- measured slower)
+    if (c2_on && (!g_fft_groups || c2_force) && (c2_only == 0 || c2_only == n)) {
+      const long long N1 = 1LL << p.a1, N2 = (long long)p.q2 << p.a2;
+      ColArgs ca, cb;
+      ca.in = in;
+      ca.in_ls = in_ls;
+      ca.in_len = in_len;
+      ca.in_es = (int)N2;
+      ca.out = scratch;
+      ca.out_ls = n;
+      ca.out_es = 1;
+      ca.subs = (int)N2;
+      ca.lines = lines;
+      ca.twR = p.tw1;
+      ca.twN = p.twN;
+      ca.tw2 = p.twc;
+      ca.sign = sign;
+      ca.mul = mul;
+      ca.mul_ls = mul_ls;
+      ca.mul_scale = mul_scale;
+      cb = ca;
+      cb.mul = nullptr;
+      cb.in = scratch;
+      cb.in_ls = n;
+      cb.in_len = n;
+      cb.in_es = (int)N1;
+      cb.out = out;
+      cb.out_ls = out_ls;
+      cb.out_es = (int)N1;
+      cb.subs = (int)N1;
+      cb.twR = p.tw2;
+      // TR_FFT_C2_LINES: at most that many lines per launch (0: all in one)
+      static const long long c2_lines = [] {
+        const char* e = getenv("TR_FFT_C2_LINES");
+        return e ? atoll(e) : 0LL;
+      }();
+      const long long step = c2_lines > 0 ? c2_lines : lines;
+      bool ok = true;
+      for (long long s0 = 0; s0 < lines && ok; s0 += step) {
+        ColArgs xa = ca, xb = cb;
+        xa.in = in + s0 * in_ls;
+        xa.lines = xb.lines = std::min(step, lines - s0);
+        if (mul) xa.mul = mul + s0 * mul_ls;
+        xb.out = out + s0 * out_ls;
+        ok = col2_launch(p.a1, p.a2, p.q2, xa, xb, n, st) == 0;
+        if (!ok && s0 > 0) { tr_set_error("fused two-pass FFT launch failed (n=%lld)", n); return 4; }
+      }
+      if (ok) {
+        TR_CUDA_CHECK(cudaGetLastError());
+        return 0;
+      }
+    }
     // Lines go through both passes in chunks whose intermediate fits in L2
     // (the same scratch region for every chunk): pass B reads pass A's output
     // from L2, and the dirty scratch lines are overwritten by the next chunk

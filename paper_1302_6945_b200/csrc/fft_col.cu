@@ -14,6 +14,13 @@
 // [TL][R + 1] shared tile (odd row pitch: conflict-free across lanes).
 #include <stdlib.h>
 
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
+#include <string.h>
+#include <cooperative_groups.h>
+
 #include "fft.cuh"
 #include "fft_bfly.cuh"
 #include "fft_fast.cuh"
@@ -67,7 +74,7 @@ TR_D void tw_apply(cplx (&v)[RS], const cplx* twR, int k, int step, int sign) {
 }
 
 // element e of sub-transform s of line: in[line*in_ls + s + e*in_es]
-template <int LOG2, int Q, bool PASSA, int S, int TLX = 0>
+template <int LOG2, int Q, bool PASSA, int S, int TLX = 0, bool LDCG = false>
 TR_D void col_stage(cplx* sm, const ColArgs& a, long long lbase_in, long long lbase_out, int s, bool live,
                     int tb, const cplx* mrow, const cplx* stg = nullptr) {
   using G = CPlan<LOG2, Q, TLX>;
@@ -86,8 +93,14 @@ TR_D void col_stage(cplx* sm, const ColArgs& a, long long lbase_in, long long lb
         if constexpr (FIRST) {
           const long long gi = s + (long long)e * a.in_es;
           // staged tile ([e][TL], zero filled past in_len) or straight from HBM
-          cplx x = stg ? stg[e * G::TL + (int)(threadIdx.x % G::TL)]
-                       : (gi < a.in_len ? a.in[lbase_in + gi] : cmk(0.0, 0.0));
+          cplx x;
+          if constexpr (LDCG) {
+            // written by other CTAs of the cluster just before: L2 only
+            x = __ldcg(&a.in[lbase_in + gi]);
+          } else {
+            x = stg ? stg[e * G::TL + (int)(threadIdx.x % G::TL)]
+                    : (gi < a.in_len ? a.in[lbase_in + gi] : cmk(0.0, 0.0));
+          }
           if constexpr (PASSA) {
             if (mrow) x = cmul(x, cscale(mrow[gi], a.mul_scale));
           }
@@ -130,7 +143,7 @@ TR_D void col_stage(cplx* sm, const ColArgs& a, long long lbase_in, long long lb
   }
   if constexpr (!LAST) {
     __syncthreads();
-    col_stage<LOG2, Q, PASSA, S + 1, TLX>(sm, a, lbase_in, lbase_out, s, live, tb, mrow, nullptr);
+    col_stage<LOG2, Q, PASSA, S + 1, TLX, LDCG>(sm, a, lbase_in, lbase_out, s, live, tb, mrow, nullptr);
   }
 }
 
@@ -180,6 +193,228 @@ int launch(const ColArgs& a, cudaStream_t st) {
   }
 }
 
+
+// ------------------------------------------------ both passes in one launch
+// A cluster of C CTAs owns one line at a time (persistent: cluster c takes
+// lines c, c + #clusters, ...).  Its CTAs share the line's pass-A tiles, meet at
+// a cluster barrier (release / acquire: pass A's global stores are visible to
+// the cluster), then share the pass-B tiles.  The intermediate Y lives in one
+// scratch slot per cluster (#clusters * n values, a few tens of MB): it is
+// rewritten for every line, so it stays dirty in L2 and HBM sees one read and
+// one write per element; the whole transform is one launch whose clusters
+// drift out of phase, so loads, butterflies and stores of different lines
+// overlap (the chunked two-launch plan runs every CTA in lockstep, 1-2 waves
+// per launch).
+TR_D void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+TR_D unsigned cluster_rank() { unsigned r; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r)); return r; }
+TR_D unsigned cluster_size() { unsigned r; asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r)); return r; }
+TR_D unsigned cluster_id() { unsigned r; asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r)); return r; }
+TR_D unsigned cluster_count() { unsigned r; asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r)); return r; }
+
+// Free scratch slots as S mailboxes (0 = empty, else slot + 1) with ticket
+// counters: a cluster takes ticket t = head++ and empties mailbox t % S
+// (waiting while it is empty), and returns its slot with ticket u = tail++
+// into mailbox u % S (waiting while it is full).  With at most S clusters
+// between take and return, every wait is on a cluster that is already running,
+// and after a launch all S slots are back in the mailboxes: the state carries
+// over from launch to launch without a reset.
+struct Col2Ring {
+  unsigned long long head, tail;
+  unsigned box[80];
+};
+constexpr int ring_slots(int C) { return C == 4 ? 76 : 38; }  // >= resident clusters of size C on 148 SMs
+
+template <int LA, int LB, int QB>
+__global__ void __launch_bounds__(NTH, FFT_COL_MINB) fft_col2_kernel(ColArgs a, ColArgs b, Col2Ring* ring, int S) {
+  using GA = CPlan<LA, 1>;
+  using GB = CPlan<LB, QB>;
+  extern __shared__ __align__(16) unsigned char fsm[];
+  __shared__ int s_slot;
+  cplx* tile = reinterpret_cast<cplx*>(fsm);
+  const int rank = (int)cluster_rank(), C = (int)cluster_size();
+  const long long cid = cluster_id(), ncl = cluster_count();
+  const int sla = threadIdx.x % GA::TL, tba = threadIdx.x / GA::TL;
+  const int slb = threadIdx.x % GB::TL, tbb = threadIdx.x / GB::TL;
+  const int tiles_a = a.subs / GA::TL, tiles_b = b.subs / GB::TL;
+  long long slot_id = cid;
+  if (ring) {  // more clusters than slots: take a free one
+    if (rank == 0 && threadIdx.x == 0) {
+      const unsigned long long t = atomicAdd(&ring->head, 1ULL);
+      unsigned* box = &ring->box[t % (unsigned)S];
+      unsigned v;
+      while ((v = atomicExch(box, 0u)) == 0u) __nanosleep(200);
+      __threadfence();
+      s_slot = (int)v - 1;
+    }
+    cluster_sync_all();
+    slot_id = *cooperative_groups::this_cluster().map_shared_rank(&s_slot, 0);
+  }
+  const long long slot = slot_id * a.out_ls;  // scratch slot of this cluster (out_ls = n)
+  for (long long line = cid; line < a.lines; line += ncl) {
+    const long long lin = line * a.in_ls;
+    const cplx* mrow = a.mul ? a.mul + line * a.mul_ls : nullptr;
+    for (int t = rank; t < tiles_a; t += C) {
+      const int s0 = t * GA::TL;
+      col_stage<LA, 1, true, 0>(tile + (size_t)sla * GA::LS, a, lin, slot, s0 + sla, true, tba, mrow);
+      __syncthreads();
+      for (int e = threadIdx.x; e < GA::TL * GA::R; e += NTH) {
+        const int u = e / GA::R, k = e - u * GA::R;
+        a.out[slot + (long long)(s0 + u) * GA::R + k] = tile[(size_t)u * GA::LS + k];
+      }
+      __syncthreads();
+    }
+    cluster_sync_all();
+    const long long lout = line * b.out_ls;
+    for (int t = rank; t < tiles_b; t += C) {
+      const int s0 = t * GB::TL;
+      col_stage<LB, QB, false, 0, 0, true>(tile + (size_t)slb * GB::LS, b, slot, lout, s0 + slb, true, tbb, nullptr);
+      __syncthreads();
+    }
+    if (ring || line + ncl < a.lines) cluster_sync_all();  // the slot is rewritten by the next pass A
+  }
+  if (ring && rank == 0 && threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long u = atomicAdd(&ring->tail, 1ULL);
+    unsigned* box = &ring->box[u % (unsigned)S];
+    while (atomicCAS(box, 0u, (unsigned)slot_id + 1u) != 0u) __nanosleep(200);
+  }
+}
+
+// mailbox state per (scratch buffer, cluster size), created on first use
+Col2Ring* ring_for(const void* scratch, int C, cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, Col2Ring*> rings;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(scratch, C);
+  auto it = rings.find(key);
+  if (it != rings.end()) return it->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  Col2Ring h;
+  memset(&h, 0, sizeof h);
+  const int S = ring_slots(C);
+  h.head = 0;
+  h.tail = (unsigned long long)S;
+  for (int i = 0; i < S; ++i) h.box[i] = (unsigned)i + 1u;
+  Col2Ring* d = nullptr;
+  if (cudaMalloc(&d, sizeof h) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, &h, sizeof h, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  rings[key] = d;
+  return d;
+}
+
+// TR_FFT_C2 = 0: off (default), 1: one cluster per line (scratch slots from the mailboxes), 2: persistent clusters
+int col2_mode() {
+  static const int m = [] {
+    const char* e = getenv("TR_FFT_C2");
+    return e ? atoi(e) : 0;
+  }();
+  return m;
+}
+
+template <int LA, int LB, int QB>
+int launch2(const ColArgs& a, const ColArgs& b, long long n, cudaStream_t st) {
+  using GA = CPlan<LA, 1>;
+  using GB = CPlan<LB, QB>;
+  if (a.subs % GA::TL || b.subs % GB::TL) return -1;
+  const size_t sa = sizeof(cplx) * (size_t)GA::TL * GA::LS, sb = sizeof(cplx) * (size_t)GB::TL * GB::LS;
+  const size_t smem = sa > sb ? sa : sb;
+  auto kern = fft_col2_kernel<LA, LB, QB>;
+  // active clusters per cluster size (4, 8), once per instantiation and device
+  static int act[2] = {0, 0};
+  static bool set = false;
+  if (!set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024) != cudaSuccess) return -1;
+    for (int i = 0; i < 2; ++i) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 4u << i;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(4u << i);
+      cfg.blockDim = dim3(NTH);
+      cfg.dynamicSmemBytes = smem;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess) nc = 0;
+      act[i] = nc;
+    }
+    cudaGetLastError();
+    set = true;
+  }
+  // cluster size: 4 for throughput (least barrier wait) when its scratch slots
+  // stay L2-sized and there are lines enough to fill the GPU, else 8
+  static const long long budget = [] {
+    const char* e = getenv("TR_FFT_C2_MB");  // scratch slots of one launch (MB)
+    return (long long)((e ? atof(e) : 40.0) * (1 << 20));
+  }();
+  const long long lb = n * (long long)sizeof(cplx);
+  const bool persistent = col2_mode() == 2;
+  auto slots = [&](int i) { return persistent ? act[i] : ring_slots(4 << i); };
+  int ci = -1;
+  static const int force_c = [] {
+    const char* e = getenv("TR_FFT_C2_CL");  // 4 / 8: force the cluster size
+    return e ? atoi(e) : 0;
+  }();
+  if (force_c == 4 || force_c == 8) {
+    const int i = force_c == 4 ? 0 : 1;
+    if (act[i] > 0 && std::min<long long>(slots(i), a.lines) * lb <= budget) ci = i;
+  } else {
+    // rounds of resident clusters x tiles per CTA and round; ties go to the
+    // smaller cluster (fewer CTAs idle at the barriers)
+    const int ta = a.subs / GA::TL, tb = b.subs / GB::TL;
+    long long best = -1;
+    for (int i = 0; i < 2; ++i) {
+      const int C = 4 << i;
+      if (act[i] <= 0 || std::min<long long>(slots(i), a.lines) * lb > budget) continue;
+      const long long rounds = (a.lines + act[i] - 1) / act[i];
+      const long long cost = rounds * ((ta + C - 1) / C + (tb + C - 1) / C);
+      if (best < 0 || cost < best) {
+        best = cost;
+        ci = i;
+      }
+    }
+  }
+  if (ci < 0) return -1;
+  const int C = 4 << ci;
+  long long ncl = std::min<long long>(act[ci], a.lines);
+  Col2Ring* ring = nullptr;
+  int S = 0;
+  if (!persistent) {
+    ncl = a.lines;
+    S = ring_slots(C);
+    if (a.lines > S) {
+      ring = ring_for(a.out, C, st);
+      if (!ring) return -1;
+    }
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)(ncl * C));
+  cfg.blockDim = dim3(NTH);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  TrKTimer _kt(TRK_FFT, st);
+  if (cudaLaunchKernelEx(&cfg, kern, a, b, ring, S) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return 0;
+}
+
 }  // namespace
 
 int col_launch(bool pass_a, int log2, int q, const ColArgs& a, cudaStream_t st) {
@@ -207,4 +442,22 @@ int col_launch(bool pass_a, int log2, int q, const ColArgs& a, cudaStream_t st) 
   }
 #undef TR_Q
 #undef TR_L
+}
+
+// Both passes in one launch (fft_col2_kernel); -1 when the split has no
+// instantiation or the scratch slots would outgrow L2 (the caller then runs
+// the two launches above).
+int col2_launch(int a1, int a2, int q2, const ColArgs& a, const ColArgs& b, long long n, cudaStream_t st) {
+#define TR_C2(LA, LB, QB) \
+  if (a1 == LA && a2 == LB && q2 == QB) return launch2<LA, LB, QB>(a, b, n, st);
+#define TR_C2A(LB, QB) TR_C2(6, LB, QB) TR_C2(7, LB, QB) TR_C2(8, LB, QB)
+  TR_C2A(6, 1) TR_C2A(7, 1) TR_C2A(8, 1)
+  TR_C2A(5, 3) TR_C2A(6, 3)
+  TR_C2A(4, 5) TR_C2A(5, 5)
+  TR_C2A(4, 7) TR_C2A(5, 7)
+  TR_C2A(4, 9)
+  TR_C2A(4, 15)
+#undef TR_C2A
+#undef TR_C2
+  return -1;
 }

@@ -56,3 +56,5 @@ inline int col_tile(int R) {
   return t > 16 ? 16 : (t < 4 ? 4 : t);
 }
 int col_launch(bool pass_a, int log2, int q, const ColArgs& a, cudaStream_t st);
+// both passes in one cluster launch (a: pass A into the scratch slots, b: pass B out of them)
+int col2_launch(int a1, int a2, int q2, const ColArgs& a, const ColArgs& b, long long n, cudaStream_t st);

@@ -61,6 +61,7 @@ thread_local int g_kcur = -1;
 std::map<long long, std::pair<double, long long>> g_fft_by_tag;
 }  // namespace
 thread_local long long g_fft_tag = 0;  // set by fft_exec (fft.cu)
+extern thread_local int g_fft_groups;  // fft.cu
 namespace {
 
 cudaEvent_t kev_get() {
@@ -1352,6 +1353,10 @@ int phase_groups(const Plan& p, std::vector<Group>& gs, int phase, int cg_init, 
       TR_CUDA_CHECK(cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming));
     }
   }
+  struct Shared {  // fft_exec keeps short launches while groups run side by side
+    Shared() { g_fft_groups = 1; }
+    ~Shared() { g_fft_groups = 0; }
+  } shared_gpu;
   TR_CUDA_CHECK(cudaEventRecord(fork, st));
   for (int g = 1; g < G; ++g) {
     TR_CUDA_CHECK(cudaStreamWaitEvent(side[g], fork, 0));
