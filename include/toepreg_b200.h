@@ -55,6 +55,9 @@ typedef struct tr_desc {
   int32_t refine_cg;        /* refinement by up to this many CG iterations warm-started at the
                                direct solution; systems CG leaves unfinished (and every system
                                when 0) get `refine` direct refinement solves instead */
+  int32_t real_data;        /* 1: every input (T, b / normal rhs) has a zero imaginary part; the CG
+                               refinement of the l2 variant then runs on real vectors with
+                               half-length transforms.  0: unknown / complex (always valid) */
 } tr_desc;
 
 /* Per-system report (ref: SolveReport solver.py:48-55, TanIntDiagnostics

@@ -33,6 +33,7 @@ class TrDesc(C.Structure):
         ("force_even", C.c_int32),
         ("refine", C.c_int32),
         ("refine_cg", C.c_int32),
+        ("real_data", C.c_int32),
     ]
 
 

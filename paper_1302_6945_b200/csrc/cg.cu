@@ -102,23 +102,38 @@ __global__ void __launch_bounds__(CGT) cg_update_kernel(cplx* X, cplx* R, cplx* 
 // restarts from x = 0 instead; its CG is never abandoned for the direct
 // refinement and stops at the iteration cap (rescued = 1).  A system with a
 // zero right-hand side keeps status 3 (the operator itself is singular).
+//
+// XR != nullptr (real data, solver.cu real CG refinement): the CG state is kept
+// as real vectors -- x in XR, r in R, d in D, each line n doubles (n / 2
+// complex values: the layout the half-length transforms and cg_update read);
+// imaginary parts (rounding noise of a real problem) are dropped.
 __global__ void __launch_bounds__(CGT) cg_warm_kernel(cplx* X, cplx* R, cplx* D, const cplx* AX,
                                                       const cplx* Y, const double* beta_sq, long long beta_bs,
                                                       int ridge, long long n, double* st, int* it, int* status,
-                                                      int* rescued, const int* trim_over) {
+                                                      int* rescued, const int* trim_over, double* XR) {
   __shared__ double sh[CGT / 32];
   __shared__ int rescue_sh;
   const long long sys = blockIdx.x;
   const double b2 = ridge ? beta_sq[sys * beta_bs] : 0.0;
+  double* Rr = reinterpret_cast<double*>(R);
+  double* Dr = reinterpret_cast<double*>(D);
   double s = 0.0, sy = 0.0;
   for (long long i = threadIdx.x; i < n; i += CGT) {
     const long long o = sys * n + i;
     const cplx x = X[o], ax = AX[o], y = Y[o];
     const cplx r = cmk(y.x - (ax.x + b2 * x.x), y.y - (ax.y + b2 * x.y));
-    R[o] = r;
-    D[o] = r;
-    s += cabs2(r);
-    sy += cabs2(y);
+    if (XR) {
+      XR[o] = x.x;
+      Rr[o] = r.x;
+      Dr[o] = r.x;
+      s += r.x * r.x;
+      sy += y.x * y.x;
+    } else {
+      R[o] = r;
+      D[o] = r;
+      s += cabs2(r);
+      sy += cabs2(y);
+    }
   }
   s = blk_sum(s, sh);
   sy = blk_sum(sy, sh);
@@ -129,9 +144,15 @@ __global__ void __launch_bounds__(CGT) cg_warm_kernel(cplx* X, cplx* R, cplx* D,
     for (long long i = threadIdx.x; i < n; i += CGT) {
       const long long o = sys * n + i;
       const cplx y = Y[o];
-      X[o] = cmk(0.0, 0.0);
-      R[o] = y;
-      D[o] = y;
+      if (XR) {
+        XR[o] = 0.0;
+        Rr[o] = y.x;
+        Dr[o] = y.x;
+      } else {
+        X[o] = cmk(0.0, 0.0);
+        R[o] = y;
+        D[o] = y;
+      }
     }
     s = sy;
   }
@@ -303,6 +324,38 @@ __global__ void cg_active_kernel(const double* st, long long nsys, int* any) {
   if (threadIdx.x == 0 && a) atomicOr(any, 1);
 }
 
+
+// x (complex, zero imaginary part) from the real CG state
+__global__ void real_unpack_kernel(cplx* X, const double* XR, long long total) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < total) X[i] = cmk(XR[i], 0.0);
+}
+
+// Factors of the half-length spectrum product (ref solver.py:104-167 applies
+// the blocks through full-length circulant embeddings).  A real sequence x of
+// q values read as h = q / 2 complex ones z_j = x_2j + i x_2j+1 has the
+// transform Z; with E the circulant spectrum (length q, forward sign -1) of a
+// real block, the h-point inverse transform of
+//   V_k = P_k Z_k + M_k conj(Z_(-k mod h)),
+//   P_k = (E_k + E_(k+h)) - (E_k - E_(k+h)) sin(2 pi k / q),
+//   M_k = i (E_k - E_(k+h)) cos(2 pi k / q)
+// is the (real) circulant product E * x in the same interleaved layout.
+// out: [line][2 (P, M)][h] for every input line [line][q]; blockIdx.z = system
+// (strides out_bs / e_bs).
+__global__ void pm_spectra_kernel(cplx* out, long long out_bs, const cplx* E, long long e_bs, long long q,
+                                  const cplx* twq, long long lines) {
+  const long long h = q / 2;
+  const long long line = blockIdx.y;
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= h || line >= lines) return;
+  out += blockIdx.z * out_bs;
+  E += blockIdx.z * e_bs;
+  const cplx e0 = E[line * q + k], e1 = E[line * q + k + h];
+  const cplx w = twq[k];  // cos + i sin (2 pi k / q)
+  const cplx S = cadd(e0, e1), Dm = csub(e0, e1);
+  out[(line * 2 + 0) * h + k] = cmk(S.x - Dm.x * w.y, S.y - Dm.y * w.y);
+  out[(line * 2 + 1) * h + k] = cmk(-Dm.y * w.x, Dm.x * w.x);
+}
 }  // namespace
 
 int launch_cg_init(cplx* X, cplx* R, cplx* D, const cplx* Y, long long n, double* st, int* it, long long nsys,
@@ -340,11 +393,11 @@ int launch_cg_active(const double* st, long long nsys, int* any, cudaStream_t s)
 
 int launch_cg_warm(cplx* X, cplx* R, cplx* D, const cplx* AX, const cplx* Y, const double* beta_sq,
                    long long beta_bs, int ridge, long long n, double* st, int* it, long long nsys, int* status,
-                   int* rescued, const int* trim_over, cudaStream_t s) {
+                   int* rescued, const int* trim_over, cudaStream_t s, double* XR) {
   {
     TrKTimer _kt(TRK_NORMAL, s);
     cg_warm_kernel<<<(unsigned)nsys, CGT, 0, s>>>(X, R, D, AX, Y, beta_sq, beta_bs, ridge, n, st, it, status,
-                                                  rescued, trim_over);
+                                                  rescued, trim_over, XR);
   }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
@@ -377,6 +430,21 @@ int launch_refine_apply(cplx* X, const cplx* D, const int* status, const double*
                         cudaStream_t s) {
   dim3 g((unsigned)((n + 255) / 256), (unsigned)nsys);
   { TrKTimer _kt(TRK_FINISH, s); refine_apply_kernel<<<g, 256, 0, s>>>(X, D, status, st, n); }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int launch_real_unpack(cplx* X, const double* XR, long long n, long long nsys, cudaStream_t s) {
+  const long long total = n * nsys;
+  { TrKTimer _kt(TRK_NORMAL, s); real_unpack_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(X, XR, total); }
+  TR_CUDA_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int launch_pm_spectra(cplx* out, long long out_bs, const cplx* E, long long e_bs, long long q, const cplx* twq,
+                      long long lines, long long nsys, cudaStream_t s) {
+  dim3 g((unsigned)((q / 2 + 255) / 256), (unsigned)lines, (unsigned)nsys);
+  { TrKTimer _kt(TRK_NORMAL, s); pm_spectra_kernel<<<g, 256, 0, s>>>(out, out_bs, E, e_bs, q, twq, lines); }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }

@@ -513,10 +513,15 @@ static int launch_pass(const FftPlan& p, int i, const cplx* in, long long in_ls,
 
 int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len, cplx* out,
              long long out_ls, cplx* scratch, long long lines, int sign, cudaStream_t st,
-             const cplx* mul, long long mul_ls, double mul_scale, long long chunk_bytes_override) {
+             const cplx* mul, long long mul_ls, double mul_scale, long long chunk_bytes_override,
+             const cplx* mul2) {
   if (lines <= 0) return 0;
   if (in_len > p.n) in_len = p.n;
   const long long n = p.n;
+  if (mul2 && (!mul || !p.col || in_len != n)) {
+    tr_set_error("fft_exec: the mirrored factor needs a two-pass column plan and full-length lines (n=%lld)", n);
+    return 2;
+  }
   g_fft_tag = (n << 20) + (lines & ((1 << 20) - 1));
   if (mul) {
     // the column kernels and the single-pass register kernel fuse the factor
@@ -544,7 +549,7 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
     const char* e = getenv("TR_FFT_CL");
     return e && e[0] == '1';
   }();
-  if (cl_on && fft_cl_supported(n) &&
+  if (cl_on && !mul2 && fft_cl_supported(n) &&
       fft_cl_exec(n, in, in_ls, in_len, out, out_ls, lines, sign, p.twN, mul, mul_ls, mul_scale, st) == 0)
     return 0;
   if (p.col) {
@@ -589,10 +594,12 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
       ca.tw2 = p.twc;
       ca.sign = sign;
       ca.mul = mul;
+      ca.mul2 = mul2;
       ca.mul_ls = mul_ls;
       ca.mul_scale = mul_scale;
       cb = ca;
       cb.mul = nullptr;
+      cb.mul2 = nullptr;
       cb.in = scratch;
       cb.in_ls = n;
       cb.in_len = n;
@@ -614,6 +621,7 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
         xa.in = in + s0 * in_ls;
         xa.lines = xb.lines = std::min(step, lines - s0);
         if (mul) xa.mul = mul + s0 * mul_ls;
+        if (mul2) xa.mul2 = mul2 + s0 * mul_ls;
         xb.out = out + s0 * out_ls;
         ok = col2_launch(p.a1, p.a2, p.q2, xa, xb, n, st) == 0;
         if (!ok && s0 > 0) { tr_set_error("fused two-pass FFT launch failed (n=%lld)", n); return 4; }
@@ -657,6 +665,7 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
       c.tw2 = p.twc;
       c.sign = sign;
       c.mul = mul ? mul + s0 * mul_ls : nullptr;
+      c.mul2 = mul2 ? mul2 + s0 * mul_ls : nullptr;
       c.mul_ls = mul_ls;
       c.mul_scale = mul_scale;
       int rc = col_launch(true, p.a1, 1, c, st);
@@ -666,6 +675,7 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
         return 2;
       }
       c.mul = nullptr;
+      c.mul2 = nullptr;
       c.in = scratch;
       c.in_ls = n;
       c.in_len = n;
@@ -682,6 +692,10 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
         return 0;
       }
     }
+  }
+  if (mul2) {
+    tr_set_error("fft_exec: no column kernel for the mirrored factor (n=%lld)", n);
+    return 2;
   }
   if (p.npass == 1) {
     launch_pass(p, 0, in, in_ls, in_len, out, out_ls, lines, sign, st, mul, mul_ls, mul_scale);

@@ -49,12 +49,14 @@ long long fft_good_len(long long n);
 // mul[line * mul_ls + e], the product fused into the load).  Line i of the input starts at
 // in + i*in_ls and holds in_len <= n valid values (zero-padded to n); the
 // output line i starts at out + i*out_ls.  `scratch` must hold lines*n
-// values.  in == out is allowed.
+// values.  in == out is allowed.  With mul2 (two-pass column plans only,
+// full-length lines) the loaded value is mul_scale * (in[e] mul[e] +
+// conj(in[(n - e) mod n]) mul2[e]).
 int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len,
              cplx* out, long long out_ls, cplx* scratch, long long lines, int sign,
              cudaStream_t st,
              const cplx* mul = nullptr, long long mul_ls = 0, double mul_scale = 1.0,
-             long long chunk_bytes_override = -1);
+             long long chunk_bytes_override = -1, const cplx* mul2 = nullptr);
 
 // Twiddle table exp(2 pi i k / n), k < n (cached, device memory).
 const cplx* twiddle_table(long long n);

@@ -74,7 +74,7 @@ TR_D void tw_apply(cplx (&v)[RS], const cplx* twR, int k, int step, int sign) {
 }
 
 // element e of sub-transform s of line: in[line*in_ls + s + e*in_es]
-template <int LOG2, int Q, bool PASSA, int S, int TLX = 0, bool LDCG = false>
+template <int LOG2, int Q, bool PASSA, int S, int TLX = 0, bool LDCG = false, bool M2 = false>
 TR_D void col_stage(cplx* sm, const ColArgs& a, long long lbase_in, long long lbase_out, int s, bool live,
                     int tb, const cplx* mrow, const cplx* stg = nullptr) {
   using G = CPlan<LOG2, Q, TLX>;
@@ -101,7 +101,14 @@ TR_D void col_stage(cplx* sm, const ColArgs& a, long long lbase_in, long long lb
             x = stg ? stg[e * G::TL + (int)(threadIdx.x % G::TL)]
                     : (gi < a.in_len ? a.in[lbase_in + gi] : cmk(0.0, 0.0));
           }
-          if constexpr (PASSA) {
+          if constexpr (PASSA && M2) {
+            // x m + conj(x[-gi]) m2 (full-length lines; no run-time branch, so
+            // the unrolled loads of all elements still issue together)
+            const long long nn = (long long)R * a.subs;
+            const cplx xm = cconj(a.in[lbase_in + (gi ? nn - gi : 0)]);
+            const cplx m2 = a.mul2[(mrow - a.mul) + gi];
+            x = cscale(cfma(xm, m2, cmul(x, mrow[gi])), a.mul_scale);
+          } else if constexpr (PASSA) {
             if (mrow) x = cmul(x, cscale(mrow[gi], a.mul_scale));
           }
           if constexpr (!PASSA) {
@@ -143,11 +150,11 @@ TR_D void col_stage(cplx* sm, const ColArgs& a, long long lbase_in, long long lb
   }
   if constexpr (!LAST) {
     __syncthreads();
-    col_stage<LOG2, Q, PASSA, S + 1, TLX, LDCG>(sm, a, lbase_in, lbase_out, s, live, tb, mrow, nullptr);
+    col_stage<LOG2, Q, PASSA, S + 1, TLX, LDCG, M2>(sm, a, lbase_in, lbase_out, s, live, tb, mrow, nullptr);
   }
 }
 
-template <int LOG2, int Q, bool PASSA>
+template <int LOG2, int Q, bool PASSA, bool M2 = false>
 __global__ void __launch_bounds__(NTH, FFT_COL_MINB) fft_col_kernel(ColArgs a) {
   using G = CPlan<LOG2, Q>;
   extern __shared__ __align__(16) unsigned char fsm[];
@@ -159,7 +166,7 @@ __global__ void __launch_bounds__(NTH, FFT_COL_MINB) fft_col_kernel(ColArgs a) {
   const bool live = line < a.lines;
   const long long lin = line * a.in_ls, lout = line * a.out_ls;
   const cplx* mrow = (PASSA && a.mul) ? a.mul + line * a.mul_ls : nullptr;
-  col_stage<LOG2, Q, PASSA, 0>(tile + (size_t)sl * G::LS, a, lin, lout, s0 + sl, live, tb, mrow);
+  col_stage<LOG2, Q, PASSA, 0, 0, false, M2>(tile + (size_t)sl * G::LS, a, lin, lout, s0 + sl, live, tb, mrow);
   if constexpr (PASSA) {
     // outputs of each sub-transform are contiguous: Y[s R + k]
     __syncthreads();
@@ -172,23 +179,27 @@ __global__ void __launch_bounds__(NTH, FFT_COL_MINB) fft_col_kernel(ColArgs a) {
   }
 }
 
-template <int LOG2, int Q, bool PASSA>
+template <int LOG2, int Q, bool PASSA, bool M2 = false>
 int launch(const ColArgs& a, cudaStream_t st) {
   if constexpr ((Q << LOG2) > 1024 || (Q << LOG2) < 2) {
     return -1;
   } else {
     using G = CPlan<LOG2, Q>;
     if (a.subs % G::TL) return -1;
+    if constexpr (PASSA && !M2) {
+      if (a.mul2) return launch<LOG2, Q, PASSA, true>(a, st);
+    }
+    if (M2 && !a.mul) return -1;
     const size_t smem = sizeof(cplx) * (size_t)G::TL * G::LS;
     static bool set = false;
     if (!set) {
-      cudaFuncSetAttribute(fft_col_kernel<LOG2, Q, PASSA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(fft_col_kernel<LOG2, Q, PASSA, M2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            100 * 1024);
       set = true;
     }
     const long long blocks = a.lines * a.subs / G::TL;
     TrKTimer _kt(TRK_FFT, st);
-    fft_col_kernel<LOG2, Q, PASSA><<<(unsigned)blocks, NTH, smem, st>>>(a);
+    fft_col_kernel<LOG2, Q, PASSA, M2><<<(unsigned)blocks, NTH, smem, st>>>(a);
     return 0;
   }
 }
@@ -321,7 +332,7 @@ template <int LA, int LB, int QB>
 int launch2(const ColArgs& a, const ColArgs& b, long long n, cudaStream_t st) {
   using GA = CPlan<LA, 1>;
   using GB = CPlan<LB, QB>;
-  if (a.subs % GA::TL || b.subs % GB::TL) return -1;
+  if (a.subs % GA::TL || b.subs % GB::TL || a.mul2) return -1;
   const size_t sa = sizeof(cplx) * (size_t)GA::TL * GA::LS, sb = sizeof(cplx) * (size_t)GB::TL * GB::LS;
   const size_t smem = sa > sb ? sa : sb;
   auto kern = fft_col2_kernel<LA, LB, QB>;

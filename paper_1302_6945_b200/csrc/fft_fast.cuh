@@ -47,6 +47,10 @@ struct ColArgs {
   const cplx* mul = nullptr;
   long long mul_ls = 0;
   double mul_scale = 1.0;
+  // with mul2 (same strides, full-length lines): mul_scale * (x[gi] mul[gi] +
+  // conj(x[(n - gi) mod n]) mul2[gi]) -- the spectrum product of a real sequence
+  // transformed as a half-length complex one (solver.cu, real CG refinement)
+  const cplx* mul2 = nullptr;
 };
 // sub-transforms per CTA of the column kernels for transform length R
 inline int col_tile(int R) {

@@ -156,7 +156,11 @@ int launch_cg_update(cplx* X, cplx* R, cplx* D, const cplx* AD, const double* be
 int launch_cg_active(const double* st, long long nsys, int* any, cudaStream_t s);
 int launch_cg_warm(cplx* X, cplx* R, cplx* D, const cplx* AX, const cplx* Y, const double* beta_sq,
                    long long beta_bs, int ridge, long long n, double* st, int* it, long long nsys, int* status,
-                   int* rescued, const int* trim_over, cudaStream_t s);
+                   int* rescued, const int* trim_over, cudaStream_t s, double* XR = nullptr);
+// real CG refinement (solver.cu): x from the real state; P / M factors of the half-length spectrum product
+int launch_real_unpack(cplx* X, const double* XR, long long n, long long nsys, cudaStream_t s);
+int launch_pm_spectra(cplx* out, long long out_bs, const cplx* E, long long e_bs, long long q, const cplx* twq,
+                      long long lines, long long nsys, cudaStream_t s);
 
 // ---- nonuniform Fourier sums (nufft.cu) ----
 // adjoint: y[d] = sum_k c_k exp(sign 2 pi i f_k d), d < n; forward: y[k] = sum_j x_j exp(sign 2 pi i f_k j)

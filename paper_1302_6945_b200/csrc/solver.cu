@@ -604,6 +604,7 @@ int ensure_fft(Plan* p) {
   std::lock_guard<std::mutex> lk(g_plan_mu);
   if (p->fft_ready) return 0;
   std::vector<long long> sizes = {p->N, p->q};
+  if (p->q % 2 == 0 && fft_supported(p->q / 2)) sizes.push_back(p->q / 2);  // real CG refinement
   for (const Op& op : p->ops) {
     if (op.kind == OP_UPDATE) sizes.push_back(p->N / op.stride);
     if (op.kind == OP_COMBINE) sizes.push_back(op.R);
@@ -639,6 +640,8 @@ struct Carve {
 struct WS {
   cplx *W, *Wp, *Y, *X, *X0, *X2, *Rv, *AX;
   cplx* spec_emb;  // [nsys or 1][5][q]
+  cplx* spec_pm;   // [nsys or 1][2 (T, T^H)][2 (P, M)][q / 2]: real CG refinement (cg.cu pm_spectra_kernel)
+  double* XR;      // [nsys][n] real CG iterate
   std::vector<cplx*> slot;
   cplx* leaf_scratch;
   cplx *S1, *S2, *S3;
@@ -667,6 +670,8 @@ size_t layout(const Plan& p, long long nsys, char* base, WS* w) {
   w->Rv = c.take<cplx>((size_t)nsys * n);
   w->AX = c.take<cplx>((size_t)nsys * n);
   w->spec_emb = c.take<cplx>((size_t)nsys * 5 * q);
+  w->spec_pm = c.take<cplx>((size_t)nsys * 2 * q);
+  w->XR = c.take<double>((size_t)nsys * n);
   w->slot.assign(p.slot_cap.size(), nullptr);
   for (size_t s = 0; s < p.slot_cap.size(); ++s)
     if (p.slot_cap[s] > 0) w->slot[s] = c.take<cplx>((size_t)nsys * p.PP * p.slot_cap[s]);
@@ -731,6 +736,7 @@ struct Inputs {
   const double* beta_sq;
   long long beta_bs;
   int rhs_is_normal;
+  int real_cg = 0;  // real data: CG refinement on real vectors with half-length transforms
 };
 
 __global__ void init_state_kernel(int* cd, int P, const long long* tau_dummy, int* dcount, int* retried,
@@ -1164,7 +1170,7 @@ int normal_rhs(const Plan& p, const Inputs& in, long long nsys, const WS& w, lon
 // error ~1e-9) to the FP64 floor on well-conditioned systems
 // for a small fraction of a second solve; systems CG cannot finish within
 // the iteration cap (ill-conditioned ones) get the direct refinement solve.
-enum { PH_DIRECT = 0, PH_CG = 1, PH_REFINE = 2, PH_FINAL = 3, PH_REFINE_CG = 4 };
+enum { PH_DIRECT = 0, PH_CG = 1, PH_REFINE = 2, PH_FINAL = 3, PH_REFINE_CG = 4, PH_UNPACK = 5 };
 constexpr int CG_BLOCK = 16;
 
 int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx* x_out, int phase,
@@ -1183,11 +1189,41 @@ int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
       TR_CUDA_CHECK(cudaMemcpyAsync(w.X0, w.X, sizeof(cplx) * nsys * n, cudaMemcpyDeviceToDevice, st));
       TR_TRY(normal_apply(p, nsys, w, sbs, w.X, st));
       TR_TRY(launch_cg_warm(w.X, w.Rv, w.X2, w.AX, w.Y, in.beta_sq, in.beta_bs, add_ridge, n, cst, its, nsys,
-                            w.status, w.rescued, w.trim_over, st));
+                            w.status, w.rescued, w.trim_over, st, in.real_cg ? w.XR : nullptr));
+      if (in.real_cg) {  // P / M factors of T and T^H (blocks 0, 1 of every spectra line group)
+        const long long q = p.q;
+        TR_TRY(launch_pm_spectra(w.spec_pm, 2 * q, w.spec_emb, 5 * q, q, F(p, q).twN, 2, sbs ? nsys : 1, st));
+      }
     }
     return 0;
   }
   const long long sbs = spectra_bstride(p, in);
+  if (phase == PH_UNPACK) {
+    TR_TRY(launch_real_unpack(w.X, w.XR, n, nsys, st));
+    return 0;
+  }
+  if (phase == PH_CG && in.real_cg) {
+    // The same iteration on real vectors: a line of n reals is n / 2 complex
+    // values z_j = v_2j + i v_2j+1, the circulant products run as half-length
+    // complex transforms with the P / M factors fused into the loads
+    // (cg.cu pm_spectra_kernel), and the vector update is the complex kernel on
+    // n / 2 values (all of its operations are componentwise real).
+    const long long q = p.q, h = q / 2, nh = n / 2, mh = p.m / 2;
+    const FftPlan& fh = F(p, h);
+    const long long pbs = sbs ? 2 * q : 0;
+    const cplx *PT = w.spec_pm, *MT = w.spec_pm + h, *PA = w.spec_pm + 2 * h, *MA = w.spec_pm + 3 * h;
+    const long long cb = nop_chunk();
+    for (int k = 0; k < CG_BLOCK; ++k) {
+      TR_TRY(fft_exec(fh, w.X2, nh, nh, w.S1, h, w.S3, nsys, -1, st, nullptr, 0, 1.0, cb));
+      TR_TRY(fft_exec(fh, w.S1, h, h, w.S2, h, w.S3, nsys, +1, st, PT, pbs, 1.0, cb, MT));
+      TR_TRY(fft_exec(fh, w.S2, h, mh, w.S2, h, w.S3, nsys, -1, st, nullptr, 0, 1.0, cb));
+      TR_TRY(fft_exec(fh, w.S2, h, h, w.S2, h, w.S3, nsys, +1, st, PA, pbs, 1.0 / ((double)q * (double)q), cb, MA));
+      TR_TRY(launch_cg_update(reinterpret_cast<cplx*>(w.XR), w.Rv, w.X2, w.S2, in.beta_sq, in.beta_bs, add_ridge,
+                              nh, 1.0, cst, its, nsys, st, h));
+    }
+    TR_TRY(launch_cg_check(cst, its, nsys, cg_init, w.rescued, st));
+    return 0;
+  }
   if (phase == PH_CG) {
     for (int k = 0; k < CG_BLOCK; ++k) {
       if (p.variant == TR_L2) {  // one Gram term: the update reads it from the transform buffer
@@ -1380,10 +1416,10 @@ int run_phase(const Plan& p, std::vector<Group>& gs, long long nsys, int phase, 
   int dev = 0;
   cudaGetDevice(&dev);
   char key[512];
-  snprintf(key, sizeof key, "%d|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%d|%p|%p|%d|%d|%d", dev,
+  snprintf(key, sizeof key, "%d|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%p|%lld|%d|%p|%p|%d|%d|%d|%d", dev,
            (const void*)&p, nsys, (const void*)in.T, in.T_bs, (const void*)in.L, in.L_bs,
            (const void*)in.G, in.G_bs, (const void*)in.beta_sq, in.beta_bs, (const void*)in.rhs,
-           in.rhs_bs, in.rhs_is_normal, (void*)gs[0].x, ws, phase, cg_init, (int)gs.size());
+           in.rhs_bs, in.rhs_is_normal, (void*)gs[0].x, ws, phase, cg_init, (int)gs.size(), in.real_cg);
   std::lock_guard<std::mutex> lk(g_graph_mu);
   GraphEntry& e = g_graphs[key];
   e.calls += 1;
@@ -1503,6 +1539,7 @@ int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine,
     TR_TRY(run_phase(p, gs, nsys, PH_CG, cap, st, ws));
     TR_TRY(cg_any_active(gs, st, &any));
   }
+  if (gs[0].in.real_cg) TR_TRY(run_phase(p, gs, nsys, PH_UNPACK, 0, st, ws));
   // systems CG did not converge on: direct refinement from their direct solution
   bool need = false;
   TR_TRY(cg_any_unconverged(gs, st, &need));
@@ -1555,6 +1592,17 @@ extern "C" int tr_solve_batch(const tr_desc* d, int64_t batch, const double* T_g
   if (p->variant == TR_GRAMIAN && !G_col) { tr_set_error("G column required"); return 2; }
   if (p->variant == TR_L2 && !beta_sq) { tr_set_error("beta_sq required"); return 2; }
   if (!rhs || !x_out) { tr_set_error("rhs and x_out required"); return 2; }
+  // Real data (tr_desc.real_data: every input has a zero imaginary part), ridge
+  // variant, even sizes and a two-pass half-length plan: the CG refinement runs
+  // on real vectors with half-length transforms (TR_REAL_CG=0 keeps the complex one).
+  static const bool real_off = [] {
+    const char* e = getenv("TR_REAL_CG");
+    return e && e[0] == '0';
+  }();
+  int real_cg = 0;
+  if (d->real_data && !real_off && p->variant == TR_L2 && p->n % 2 == 0 && p->m % 2 == 0 && p->q % 2 == 0 &&
+      p->fft.count(p->q / 2) && p->fft.at(p->q / 2).col)
+    real_cg = 1;
   for (auto& g : gs) {
     layout(*p, g.count, (char*)workspace + g.off, &g.w);
     Inputs& in = g.in;
@@ -1570,6 +1618,7 @@ extern "C" int tr_solve_batch(const tr_desc* d, int64_t batch, const double* T_g
     in.beta_sq = beta_sq ? beta_sq + f * beta_bs : nullptr;
     in.beta_bs = beta_bs;
     in.rhs_is_normal = rhs_is_normal;
+    in.real_cg = real_cg;
     // beta_sq is only read for l2; point others at the workspace norm slot
     if (!in.beta_sq) { in.beta_sq = g.w.nrm; in.beta_bs = 0; }
     g.x = reinterpret_cast<cplx*>(x_out) + f * p->n;
@@ -1616,6 +1665,17 @@ extern "C" int tr_solve_batch_host(const tr_desc* d, int64_t batch, const double
   TR_TRY(get_plan(d, &p));
   if (batch <= 0) return 0;
   const long long n = p->n, m = p->m, pl = p->pl;
+  tr_desc dd = *d;
+  if (!dd.real_data && p->variant == TR_L2 && T_gen && rhs) {  // host buffers: look
+    auto is_real = [&](const double* v, long long bs, long long len) {
+      const long long tot = bs ? bs * (batch - 1) + len : len;
+      for (long long i = 0; i < tot; ++i)
+        if (v[2 * i + 1] != 0.0) return false;
+      return true;
+    };
+    dd.real_data = is_real(T_gen, T_bs, m + n - 1) && is_real(rhs, rhs_bs, rhs_is_normal ? n : m);
+  }
+  d = &dd;
   auto sz = [&](const void* ptr, long long bs, long long len) -> size_t {
     if (!ptr) return 0;
     return sizeof(cplx) * (size_t)(bs ? bs * (batch - 1) + len : len);

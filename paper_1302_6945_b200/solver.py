@@ -219,6 +219,9 @@ class DeviceBatch:
             hosts["rhs"], self.bs["rhs"] = pack([np.asarray(p.b, dtype=np.complex128)
                                                  for p in problems], self.m)
         self.hosts = hosts
+        # real data (l2): the library's CG refinement then works on real vectors
+        self.desc.real_data = int(v == "l2" and not any(
+            np.iscomplexobj(hosts[k]) and hosts[k].imag.any() for k in ("T", "rhs")))
         self.h2d_bytes = sum(h.nbytes for h in hosts.values())
         self.dev = {}
         self.x = torch.empty((self.batch, self.n, 2), dtype=torch.float64, device="cuda")

@@ -592,3 +592,31 @@ def test_full_size_c5b_single_system(gpu):
     x_cg, it = tb.cg_solve(prob, tb.CGConfig(tolerance=1e-14))
     assert 0 < it < 10 * n
     assert rel(rep.x_hat, x_cg) < 1e-10
+
+
+def test_real_cg_refinement_matches_complex_path(gpu):
+    """Real l2 data refines by CG on real vectors with half-length transforms
+    (csrc/cg.cu pm_spectra_kernel; needs a two-pass half-length plan: c2's
+    shape).  The same systems with one right-hand side entry carrying a 1e-300
+    imaginary part take the complex path; both must agree to rounding, match
+    the exact (dense) solution, and batch == single bit for bit."""
+    tb = gpu
+    raw = wl.c2_rect(m=8192, n=4096, nrhs=3, seed=5)
+    probs = [wl.to_problem(raw, tb, i) for i in range(3)]
+    reps = tb.solve_tikhonov_batch(probs)
+    tagged = []
+    for p in probs:
+        b = np.array(p.b, dtype=np.complex128)
+        b[0] += 1e-300j
+        tagged.append(tb.ProblemSpec(variant="l2", T=p.T, beta=p.beta, b=b))
+    reps_c = tb.solve_tikhonov_batch(tagged)
+    single = tb.solve_tikhonov(probs[1])
+    assert np.array_equal(single.x_hat, reps[1].x_hat)
+    exact = O.dense_solution(probs[1])
+    for r, rc in zip(reps, reps_c):
+        assert r.diagnostics.refine_cg_iterations > 0 and rc.diagnostics.refine_cg_iterations > 0
+        assert not r.x_hat.imag.any()          # real state: no imaginary rounding noise
+        assert rel(r.x_hat, rc.x_hat) < 1e-13
+        assert abs(r.diagnostics.refine_cg_iterations - rc.diagnostics.refine_cg_iterations) <= 2
+    assert rel(reps[1].x_hat, exact) < 1e-12
+    assert rel(reps_c[1].x_hat, exact) < 1e-12
