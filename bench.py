@@ -80,8 +80,11 @@ def make_workload(cfg: str, rank: int, batch: int, world: int = 1):
         raw = wl.c5_random(n=1 << 22, count=1, seed=0, first=rank)
         return raw, 1, "c5b: one square system n=2^22 (l2, beta=0.1)"
     if cfg == "c3":
-        raw = wl.c3_firstdiff(n=65536, lam=1e-2, seed=0, item=rank)
-        return raw, 1, "c3: general n=65536, first-difference L, lambda=1e-2"
+        # BASELINE config 3: one instance, lambda swept over four values -- the
+        # four systems (same T and b, L scaled) are one batch of independent solves
+        lams = (1e-3, 1e-2, 1e-1, 1.0)
+        raws = [wl.c3_firstdiff(n=65536, lam=l, seed=0, item=rank) for l in lams]
+        return raws, len(raws), "c3: general n=65536, first-difference L, lambda in {1e-3, 1e-2, 1e-1, 1} (one batch of 4)"
     raise SystemExit(f"unknown config {cfg}")
 
 
@@ -89,6 +92,8 @@ def problems_from(raw, count, mod=None):
     if mod is None:
         import paper_1302_6945_b200 as mod
     from paper_1302_6945_b200 import workloads as wl
+    if isinstance(raw, (list, tuple)):  # one raw problem per system
+        return [wl.to_problem(r, mod) for r in raw]
     if count == 1 and np.asarray(raw.get("b", raw.get("normal_rhs"))).ndim == 1:
         return [wl.to_problem(raw, mod)]
     return [wl.to_problem(raw, mod, i) for i in range(count)]
@@ -356,7 +361,8 @@ def main():
     # through one leaf sweep in order (SURVEY 8(d) chain bound C x t_step);
     # groups of <= 148 systems (solver.cu batch_groups) run one after the
     # other in this eager timing pass, their systems in parallel
-    rows = 3 if raw.get("variant", "") == "general" else 2
+    raw0 = raw[0] if isinstance(raw, (list, tuple)) else raw
+    rows = 3 if raw0.get("variant", "") == "general" else 2
     n_cond = rows * info["order"]
     groups = 1 if count < 32 else min(4, max(2, -(-count // 148)))
     leaf_ms = sum(kst[k][0] for k in ("leaf_pivot", "leaf_build", "leaf_check", "leaf_exact") if k in kst) / nk

@@ -672,11 +672,15 @@ struct WS {
   SplitState split;
 };
 
-// TR_PRE_FFT=0: no early left-factor transforms (A/B)
+// TR_PRE_FFT=1: forward transform of a combine's left factor on a side stream
+// while the right subtree is built (+50% workspace).  Off by default: measured
+// on B200 it takes the transform off the critical path but the side stream's
+// launches contend with the group's own (c2 direct phase 30.53 -> 30.98 ms,
+// c5 258.3 -> 261.1 ms; gpurun_out/r2l, profiles/r2_ab_pre_fft.txt).
 bool pre_fft_on() {
   static const bool on = [] {
     const char* e = getenv("TR_PRE_FFT");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }

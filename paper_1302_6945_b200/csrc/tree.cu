@@ -265,8 +265,14 @@ int launch_trim_cl(const TrimArgs& a, long long nsys, cudaStream_t st) {
 
 template <int P>
 int dispatch_trim_cl(const TrimArgs& a, long long nsys, cudaStream_t st) {
-  // CTAs per system: enough to cover the GPU, slices of >= 256 coefficients
-  long long want = (2 * 148 + nsys - 1) / nsys;
+  // CTAs per system: enough to keep the streaming passes HBM-bound (about 8
+  // resident CTAs per SM; 2 per SM ran the top-level trims of a 128-system
+  // group at 1.9 TB/s), slices of >= 256 coefficients (TR_TRIM_CTAS: per SM)
+  static const long long per_sm = [] {
+    const char* e = getenv("TR_TRIM_CTAS");
+    return e ? atoll(e) : 8LL;
+  }();
+  long long want = (per_sm * 148 + nsys - 1) / nsys;
   long long by_len = (a.L + 255) / 256;
   long long c = want < by_len ? want : by_len;
   if (c >= 8) return launch_trim_cl<P, 8>(a, nsys, st);

@@ -620,3 +620,25 @@ def test_real_cg_refinement_matches_complex_path(gpu):
         assert abs(r.diagnostics.refine_cg_iterations - rc.diagnostics.refine_cg_iterations) <= 2
     assert rel(reps[1].x_hat, exact) < 1e-12
     assert rel(reps_c[1].x_hat, exact) < 1e-12
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_fused_two_pass_fft_modes(gpu, mode):
+    """The opt-in fused two-pass transform (csrc/fft_col.cu fft_col2_kernel:
+    TR_FFT_C2 = 1 per-line clusters with the scratch-slot mailboxes, 2
+    persistent clusters) against numpy-class accuracy, out of place / in place,
+    both signs, line counts below and above the slot count.  The mode is read
+    once per process, so each runs in its own."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    shapes = ["12288x40", "8192x100", "32768x90", "20480x33"]
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fft_c2.py"), "child"] + shapes,
+                         env=dict(os.environ, TR_FFT_C2=mode), capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if " err " in l]
+    assert len(lines) == len(shapes), out.stdout
+    for l in lines:
+        err = float(l.split(" err ")[1].split()[0])
+        err2 = float(l.split("inplace/inv ")[1].split()[0])
+        assert err < 5e-15 and err2 < 5e-15, l

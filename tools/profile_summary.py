@@ -5,7 +5,8 @@ import collections, csv, glob, json, os, subprocess, sys
 R = sys.argv[1] if len(sys.argv) > 1 else "r1"
 SRC = f"gpurun_out/{R}"
 OUT = "profiles"
-CLASS = [("leaf_fused", "leaf_pivot"), ("leaf_chain", "leaf_pivot"), ("leaf_pivot", "leaf_pivot"), ("need_reset", "leaf_pivot"),
+CLASS = [("update_small", "update"), ("combine_small", "combine"), ("real_unpack", "normal"), ("pm_spectra", "normal"),
+         ("leaf_fused", "leaf_pivot"), ("leaf_chain", "leaf_pivot"), ("leaf_pivot", "leaf_pivot"), ("need_reset", "leaf_pivot"),
          ("cg_", "normal"), ("spec_mul", "normal"), ("mask_scale", "normal"), ("accum", "normal"),
          ("residual", "normal"), ("norm_", "normal"), ("nudft", "assemble"),
          ("leaf_basis", "leaf_build"), ("leaf_build", "leaf_build"), ("leaf_check", "leaf_check"),
