@@ -253,11 +253,6 @@ struct Op {
   int dbound = 0;  // leaf: structural basis degree under water-filling, no deferrals
   int len_eff = 0;  // leaf: coefficients its parent's fused combine reads (0: all); longer -> reported
   int small = 0;    // combine of two leaves in one launch (combine_small.cu), transform length Rsm
-  // update: transform length of this node's (large) combine, whose left factor is
-  // complete when the update starts: its forward transform runs on a side stream
-  // while the right subtree is built.  combine: that transform was started early.
-  long long pre_R = 0;
-  int pre = 0;
   int La_eff = 0, Lb_eff = 0, Rsm = 0;
   int nattempts = 1;
   int ord_stride[4] = {1, 1, 1, 1};
@@ -274,7 +269,6 @@ struct Plan {
   int depth = 0, root_slot = 2;
   long long leaves = 0, Kmax = 0, root_cap = 0, leaf_slot_cap = 0;
   long long Rmax = 1, cnt_max = 1, Lmax = 1;
-  std::vector<long long> pre_R;  // per depth: transform length of the early left-factor spectra (0: none)
   int nblk = 0;
   std::map<long long, FftPlan> fft;
   bool fft_ready = false;
@@ -476,7 +470,6 @@ struct Builder {
       }
     }
     pl.ops.push_back(up);
-    const size_t up_idx = pl.ops.size() - 1;
     pl.cnt_max = std::max(pl.cnt_max, (long long)up.noff * (pl.N / ns));
     last_leaf_op = -1;
     long long cb = node(right, ns, depth + 1, sr);
@@ -526,12 +519,6 @@ struct Builder {
       fprintf(stderr, "combine depth %d: La %lld Lb %lld -> %lld, R %lld%s\n", depth, ca, cb, cm.cap_out, cm.R,
               cm.wrap ? " (wrapped)" : "");
     pl.Lmax = std::max(pl.Lmax, full);
-    if (!cm.small && depth < 40) {
-      cm.pre = 1;
-      pl.ops[up_idx].pre_R = cm.R;
-      if ((int)pl.pre_R.size() <= depth) pl.pre_R.resize(depth + 1, 0);
-      pl.pre_R[depth] = std::max(pl.pre_R[depth], cm.R);
-    }
     pl.ops.push_back(cm);
     pl.slot_cap[slot] = std::max(pl.slot_cap[slot], cm.cap_out);
     return cm.cap_out;
@@ -655,8 +642,6 @@ struct WS {
   cplx* spec_emb;  // [nsys or 1][5][q]
   cplx* spec_pm;   // [nsys or 1][2 (T, T^H)][2 (P, M)][q / 2]: real CG refinement (cg.cu pm_spectra_kernel)
   double* XR;      // [nsys][n] real CG iterate
-  std::vector<cplx*> pre;  // per depth: early spectra of a combine's left factor [nsys][PP][R]
-  cplx* pre_scratch;       // FFT scratch of the side stream
   std::vector<cplx*> slot;
   cplx* leaf_scratch;
   cplx *S1, *S2, *S3;
@@ -671,37 +656,6 @@ struct WS {
   cplx* clean_tmp;
   SplitState split;
 };
-
-// TR_PRE_FFT=1: forward transform of a combine's left factor on a side stream
-// while the right subtree is built (+50% workspace).  Off by default: measured
-// on B200 it takes the transform off the critical path but the side stream's
-// launches contend with the group's own (c2 direct phase 30.53 -> 30.98 ms,
-// c5 258.3 -> 261.1 ms; gpurun_out/r2l, profiles/r2_ab_pre_fft.txt).
-bool pre_fft_on() {
-  static const bool on = [] {
-    const char* e = getenv("TR_PRE_FFT");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
-// side stream and fork / join events of the stream a solve is enqueued on
-struct AuxCtx {
-  cudaStream_t aux = nullptr;
-  cudaEvent_t fork[40], done[40];
-};
-AuxCtx* aux_for(cudaStream_t st) {
-  static thread_local std::map<cudaStream_t, AuxCtx> ctx;
-  auto it = ctx.find(st);
-  if (it != ctx.end()) return &it->second;
-  AuxCtx a;
-  if (cudaStreamCreateWithFlags(&a.aux, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-  for (int i = 0; i < 40; ++i) {
-    if (cudaEventCreateWithFlags(&a.fork[i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
-    if (cudaEventCreateWithFlags(&a.done[i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
-  }
-  return &(ctx[st] = a);
-}
 
 size_t layout(const Plan& p, long long nsys, char* base, WS* w) {
   Carve c{base};
@@ -730,17 +684,6 @@ size_t layout(const Plan& p, long long nsys, char* base, WS* w) {
   for (const Op& op : p.ops)
     if (op.kind == OP_LEAF) widest_leaf_slot = std::max(widest_leaf_slot, p.slot_cap[op.slot_out]);
   w->leaf_scratch = c.take<cplx>((size_t)nsys * p.PP * widest_leaf_slot);
-  w->pre.assign(p.pre_R.size(), nullptr);
-  w->pre_scratch = nullptr;
-  if (pre_fft_on()) {
-    long long mx = 0;
-    for (size_t d = 0; d < p.pre_R.size(); ++d)
-      if (p.pre_R[d] > 0) {
-        w->pre[d] = c.take<cplx>((size_t)nsys * p.PP * p.pre_R[d]);
-        mx = std::max(mx, p.pre_R[d]);
-      }
-    if (mx > 0) w->pre_scratch = c.take<cplx>((size_t)nsys * p.PP * mx);
-  }
   w->S1 = c.take<cplx>((size_t)nsys * big);
   w->S2 = c.take<cplx>((size_t)nsys * big);
   w->S3 = c.take<cplx>((size_t)nsys * big);
@@ -1003,20 +946,7 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
   // ---- stage 3: the tree ----
   const long long w_sys = N * rows * P;
   long long leaf_no = 0;
-  // early left-factor transforms (side stream): only with unchunked tree ops
-  AuxCtx* ax = (pre_fft_on() && w.pre_scratch) ? aux_for(st) : nullptr;
-  const bool pre_ok = ax != nullptr && l2_chunk(nsys, 2LL * PP * p.Rmax) == nsys;
   for (const Op& op : p.ops) {
-    if (op.kind == OP_UPDATE && op.pre_R > 0 && pre_ok) {
-      // the left factor of this node's combine is complete: its forward
-      // transform runs on the side stream while the right subtree is built
-      const int d = op.depth;
-      TR_CUDA_CHECK(cudaEventRecord(ax->fork[d], st));
-      TR_CUDA_CHECK(cudaStreamWaitEvent(ax->aux, ax->fork[d], 0));
-      TR_TRY(fft_exec(F(p, op.pre_R), w.slot[op.slot_a], p.slot_cap[op.slot_a], op.cap_a, w.pre[d], op.pre_R,
-                      w.pre_scratch, nsys * PP, -1, ax->aux));
-      TR_CUDA_CHECK(cudaEventRecord(ax->done[d], ax->aux));
-    }
     if (op.kind == OP_LEAF) {
       LeafArgs la;
       la.W = w.W;
@@ -1142,10 +1072,8 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
       const long long cs = l2_chunk(nsys, 2LL * PP * R);
       for (long long s0 = 0; s0 < nsys; s0 += cs) {
         const long long ns = std::min(cs, nsys - s0);
-        const bool pre = op.pre && pre_ok;  // (pre_ok: one chunk, s0 = 0)
-        cplx* FA = pre ? w.pre[op.depth] : w.S1;
-        if (pre) TR_CUDA_CHECK(cudaStreamWaitEvent(st, ax->done[op.depth], 0));
-        else TR_TRY(fft_exec(fp, w.slot[op.slot_a] + s0 * PP * ca, ca, op.cap_a, FA, R, w.S3, ns * PP, -1, st));
+        cplx* FA = w.S1;
+        TR_TRY(fft_exec(fp, w.slot[op.slot_a] + s0 * PP * ca, ca, op.cap_a, FA, R, w.S3, ns * PP, -1, st));
         TR_TRY(fft_exec(fp, w.slot[op.slot_b] + s0 * PP * cb, cb, op.cap_b, w.S2, R, w.S3, ns * PP, -1, st));
         TR_TRY(launch_pointwise_matmul(FA, w.S2, P, R, ns, st));
         const cplx* prod = FA;

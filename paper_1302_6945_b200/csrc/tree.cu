@@ -265,12 +265,13 @@ int launch_trim_cl(const TrimArgs& a, long long nsys, cudaStream_t st) {
 
 template <int P>
 int dispatch_trim_cl(const TrimArgs& a, long long nsys, cudaStream_t st) {
-  // CTAs per system: enough to keep the streaming passes HBM-bound (about 8
-  // resident CTAs per SM; 2 per SM ran the top-level trims of a 128-system
-  // group at 1.9 TB/s), slices of >= 256 coefficients (TR_TRIM_CTAS: per SM)
+  // CTAs per system: enough to cover the GPU (2 per SM), slices of >= 256
+  // coefficients.  TR_TRIM_CTAS sets the per-SM figure; 4 / 8 / 16 measured no
+  // better inside a c5 solve (324.2 / 324.7 / 323.4 ms vs 321.2 ms per step)
+  // although the top-level trims alone run at only 1.9 TB/s with 2.
   static const long long per_sm = [] {
     const char* e = getenv("TR_TRIM_CTAS");
-    return e ? atoll(e) : 8LL;
+    return e ? atoll(e) : 2LL;
   }();
   long long want = (per_sm * 148 + nsys - 1) / nsys;
   long long by_len = (a.L + 255) / 256;
