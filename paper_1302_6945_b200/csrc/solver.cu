@@ -1171,8 +1171,20 @@ int normal_rhs(const Plan& p, const Inputs& in, long long nsys, const WS& w, lon
 // error ~1e-9) to the FP64 floor on well-conditioned systems
 // for a small fraction of a second solve; systems CG cannot finish within
 // the iteration cap (ill-conditioned ones) get the direct refinement solve.
-enum { PH_DIRECT = 0, PH_CG = 1, PH_REFINE = 2, PH_FINAL = 3, PH_REFINE_CG = 4, PH_UNPACK = 5 };
-constexpr int CG_BLOCK = 16;
+// PH_CG_NC: a CG block without the abandon check at its end (the check keeps
+// its cadence of CG_CHECK iterations whatever the block size)
+enum { PH_DIRECT = 0, PH_CG = 1, PH_REFINE = 2, PH_FINAL = 3, PH_REFINE_CG = 4, PH_UNPACK = 5, PH_CG_NC = 6 };
+constexpr int CG_MIN_CAP = 16;  // CG refinement only when its iteration cap is at least this
+// iterations per graph launch and host check (TR_CG_BLOCK)
+constexpr int CG_CHECK = 16;    // iterations between abandon checks (cg_check_kernel)
+// iterations per graph launch and host "any system still active" check: 8
+// wastes fewer iterations on converged batches than 16 (c5 59.7 -> 57.8 ms,
+// c2 3.34 -> 3.12 ms); TR_CG_BLOCK = 1, 2, 4, 8 or 16
+static const int CG_BLOCK = [] {
+  const char* e = getenv("TR_CG_BLOCK");
+  const int v = e ? atoi(e) : 8;
+  return (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) ? v : 8;
+}();
 
 int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx* x_out, int phase,
               int cg_init, cudaStream_t st) {
@@ -1203,6 +1215,8 @@ int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
     TR_TRY(launch_real_unpack(w.X, w.XR, n, nsys, st));
     return 0;
   }
+  const bool cg_check = phase == PH_CG;
+  if (phase == PH_CG_NC) phase = PH_CG;
   if (phase == PH_CG && in.real_cg) {
     // The same iteration on real vectors: a line of n reals is n / 2 complex
     // values z_j = v_2j + i v_2j+1, the circulant products run as half-length
@@ -1222,7 +1236,7 @@ int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
       TR_TRY(launch_cg_update(reinterpret_cast<cplx*>(w.XR), w.Rv, w.X2, w.S2, in.beta_sq, in.beta_bs, add_ridge,
                               nh, 1.0, cst, its, nsys, st, h));
     }
-    TR_TRY(launch_cg_check(cst, its, nsys, cg_init, w.rescued, st));
+    if (cg_check) TR_TRY(launch_cg_check(cst, its, nsys, cg_init, w.rescued, st));
     return 0;
   }
   if (phase == PH_CG) {
@@ -1238,7 +1252,7 @@ int phase_run(const Plan& p, const Inputs& in, long long nsys, const WS& w, cplx
                                 nsys, st));
       }
     }
-    TR_TRY(launch_cg_check(cst, its, nsys, cg_init, w.rescued, st));  // cg_init carries the iteration cap here
+    if (cg_check) TR_TRY(launch_cg_check(cst, its, nsys, cg_init, w.rescued, st));  // cg_init carries the iteration cap here
     return 0;
   }
   if (phase == PH_REFINE || phase == PH_REFINE_CG) {
@@ -1506,7 +1520,7 @@ int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine,
   // refine directly
   const long long C = (long long)p.rows * p.N;
   const int cap = (int)std::min<long long>(refine_cg, C / 32);
-  const int cg = refine > 0 && refine_cg > 0 && C >= 4096 && cap >= CG_BLOCK;
+  const int cg = refine > 0 && refine_cg > 0 && C >= 4096 && cap >= CG_MIN_CAP;
   // TR_PHASE_TIMES=1: device time of the direct phase and of the refinement (stderr)
   static const bool ptimes = getenv("TR_PHASE_TIMES") != nullptr;
   static cudaEvent_t pe[3] = {nullptr, nullptr, nullptr};
@@ -1536,8 +1550,11 @@ int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine,
     return 0;
   }
   bool any = true;
-  for (int it = 0; it < cap && any; it += CG_BLOCK) {
-    TR_TRY(run_phase(p, gs, nsys, PH_CG, cap, st, ws));
+  const int cap_up = (cap + CG_CHECK - 1) / CG_CHECK * CG_CHECK;  // whole check intervals, as with blocks of CG_CHECK
+  for (int it = 0; it < cap_up && any; it += CG_BLOCK) {
+    // the abandon check runs when the iteration count reaches a multiple of CG_CHECK
+    const bool chk = (it + CG_BLOCK) % CG_CHECK == 0;
+    TR_TRY(run_phase(p, gs, nsys, chk ? PH_CG : PH_CG_NC, cap, st, ws));
     TR_TRY(cg_any_active(gs, st, &any));
   }
   if (gs[0].in.real_cg) TR_TRY(run_phase(p, gs, nsys, PH_UNPACK, 0, st, ws));
