@@ -15,6 +15,13 @@
 // back, and the trim/normalise reductions (global maximum, last significant
 // coefficient, column maxima) run across the cluster through distributed
 // shared memory.
+// DS variant (batches that would not fit the GPU in one wave otherwise): CTA i
+// transforms only row i of B and the product reads the other rows from their
+// CTAs through distributed shared memory -- 10 lines and 41 KB of shared
+// memory per CTA at R = 256 instead of 30 lines and 123 KB, several CTAs per
+// SM.  Same arithmetic per line and per product, so the results are bit for
+// bit the same (a 128-system group: 97 -> ~75 us per launch; small groups are
+// faster with the redundant transforms and one cluster barrier less).
 #include <cooperative_groups.h>
 
 #include "fft_smem.cuh"
@@ -33,9 +40,9 @@ struct StLine {  // natural-order output k of line q back in place
   TR_D void operator()(int q, int k, cplx v) const { S[q * LP + k] = v; }
 };
 
-template <int P, int R1, int R2, int NTH>
+template <int P, int R1, int R2, int NTH, bool DS>
 __global__ void __launch_bounds__(NTH) combine_small_kernel(CombineArgs a) {
-  constexpr int R = R1 * R2, NL = P + P * P, LP = R + 1, NV = 1 + P;
+  constexpr int R = R1 * R2, NL = DS ? 2 * P : P + P * P, LP = R + 1, NV = 1 + P;
   extern __shared__ __align__(16) unsigned char smraw[];
   cplx* S = reinterpret_cast<cplx*>(smraw);  // [NL][LP]: element l of line q at S[q * LP + l]
   __shared__ double part[NV], glob[NV];
@@ -48,7 +55,7 @@ __global__ void __launch_bounds__(NTH) combine_small_kernel(CombineArgs a) {
   // ---- load A row i (lines 0..P-1) and all of B (lines P..), zero padded to
   // R: a warp per line, lanes along the coefficients (coalesced, conflict-free)
   const cplx* A = a.A + sys * a.a_sys + (long long)i * P * a.a_cap;
-  const cplx* B = a.B + sys * a.b_sys;
+  const cplx* B = a.B + sys * a.b_sys + (DS ? (long long)i * P * a.b_cap : 0LL);
   constexpr int NWP = NTH / 32, LPW = (NL + NWP - 1) / NWP, EPL = R / 32;
 #pragma unroll
   for (int u = 0; u < LPW; ++u) {
@@ -71,7 +78,17 @@ __global__ void __launch_bounds__(NTH) combine_small_kernel(CombineArgs a) {
   stage1<R1, R2, NL, 1, NTH, Ident, LP>(S, -1, a.twR, Ident());
   stage2<R1, R2, NL, 1, NTH, StLine<LP>, LP>(S, -1, StLine<LP>{S});
   __syncthreads();
-  // ---- C_i(f) = sum_j A_ij(f) B_jk(f), into lines 0..P-1
+  // ---- C_i(f) = sum_j A_ij(f) B_jk(f), into lines 0..P-1 (DS: row j of B
+  // lives in CTA j, lines P..2P-1)
+  const cplx* Brow[P];
+  if constexpr (DS) {
+    cl.sync();  // every row of B is transformed
+#pragma unroll
+    for (int j = 0; j < P; ++j) Brow[j] = cl.map_shared_rank(S, j) + P * LP;
+  } else {
+#pragma unroll
+    for (int j = 0; j < P; ++j) Brow[j] = S + (P + j * P) * LP;
+  }
   for (int f = tid; f < R; f += NTH) {
     cplx av[P];
 #pragma unroll
@@ -81,7 +98,7 @@ __global__ void __launch_bounds__(NTH) combine_small_kernel(CombineArgs a) {
     for (int k = 0; k < P; ++k) {
       cplx acc = cmk(0.0, 0.0);
 #pragma unroll
-      for (int j = 0; j < P; ++j) acc = cfma(av[j], S[(P + j * P + k) * LP + f], acc);
+      for (int j = 0; j < P; ++j) acc = cfma(av[j], Brow[j][k * LP + f], acc);
       cv[k] = acc;
     }
 #pragma unroll
@@ -194,13 +211,17 @@ __global__ void __launch_bounds__(NTH) combine_small_kernel(CombineArgs a) {
   }
 }
 
-template <int P, int R1, int R2>
+template <int P, int R1, int R2, bool DS = false>
 int launch_cs(const CombineArgs& a, long long nsys, cudaStream_t st) {
-  constexpr int NTH = 256, R = R1 * R2, NL = P + P * P, LP = R + 1;
+  constexpr int NTH = 256, R = R1 * R2, NL = DS ? 2 * P : P + P * P, LP = R + 1;
+  if constexpr (!DS) {
+    // more CTAs than one wave of the redundant variant (one CTA per SM at R >= 128)
+    if (P * nsys > 296) return launch_cs<P, R1, R2, true>(a, nsys, st);
+  }
   const size_t smem = sizeof(cplx) * (size_t)NL * LP;
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(combine_small_kernel<P, R1, R2, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(combine_small_kernel<P, R1, R2, NTH, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     set = true;
   }
@@ -217,7 +238,7 @@ int launch_cs(const CombineArgs& a, long long nsys, cudaStream_t st) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   TrKTimer _kt(TRK_COMBINE, st);
-  TR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, combine_small_kernel<P, R1, R2, NTH>, a));
+  TR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, combine_small_kernel<P, R1, R2, NTH, DS>, a));
   return 0;
 }
 
@@ -298,20 +319,64 @@ __global__ void __launch_bounds__(256) update_small_kernel(UpdateArgs a) {
     G[e] = acc;
   }
   __syncthreads();
-  // c-point DFT (sign +1: values at sigma_k = w^(o + s k))
-  for (int e = threadIdx.x; e < PP * c; e += NTH) {
-    const int ee = e / c, k = e - ee * c;
-    const cplx* g = G + ee * c;
-    cplx acc = cmk(0.0, 0.0);
-    int t = 0;
-    for (int q = 0; q < c; ++q) {
-      acc = cfma(g[q], Wc[t], acc);
-      t += k;
-      if (t >= c) t -= c;
+  // c-point DFT (sign +1: values at sigma_k = w^(o + s k)).  c = c1 c2 runs as
+  // two passes of c1- and c2-term sums (q = c2 q1 + q2, k = k1 + c1 k2:
+  // w_c^(q k) = w_c1^(q1 k1) w_c^(q2 k1) w_c2^(q2 k2)), c (c1 + c2) instead of
+  // c^2 complex FMAs per entry; the direct sums (c1 = 1) for small or prime c.
+  int c1 = 1;
+  if (c > 12)
+    for (int d = 2; d * d <= c; ++d)
+      if (c % d == 0) c1 = d;
+  const int c2 = c / c1;
+  if (c1 == 1) {
+    for (int e = threadIdx.x; e < PP * c; e += NTH) {
+      const int ee = e / c, k = e - ee * c;
+      const cplx* g = G + ee * c;
+      cplx acc = cmk(0.0, 0.0);
+      int t = 0;
+      for (int q = 0; q < c; ++q) {
+        acc = cfma(g[q], Wc[t], acc);
+        t += k;
+        if (t >= c) t -= c;
+      }
+      V[e] = acc;
     }
-    V[e] = acc;
+    __syncthreads();
+  } else {
+    // pass 1: H[q2][k1] = w_c^(q2 k1) sum_q1 G[c2 q1 + q2] w_c1^(q1 k1), into V
+    for (int e = threadIdx.x; e < PP * c; e += NTH) {
+      const int ee = e / c, r = e - ee * c;
+      const int q2 = r / c1, k1 = r - q2 * c1;
+      const cplx* g = G + ee * c + q2;
+      cplx acc = cmk(0.0, 0.0);
+      int t = 0;  // (q1 k1 mod c1) c2
+      const int st = k1 * c2;
+      for (int q1 = 0; q1 < c1; ++q1) {
+        acc = cfma(g[c2 * q1], Wc[t], acc);
+        t += st;
+        if (t >= c) t -= c;
+      }
+      V[ee * c + r] = cmul(acc, Wc[(q2 * k1) % c]);
+    }
+    __syncthreads();
+    // pass 2: V[k1 + c1 k2] = sum_q2 H[q2][k1] w_c2^(q2 k2), back into G
+    for (int e = threadIdx.x; e < PP * c; e += NTH) {
+      const int ee = e / c, k = e - ee * c;
+      const int k2 = k / c1, k1 = k - k2 * c1;
+      const cplx* h = V + ee * c + k1;
+      cplx acc = cmk(0.0, 0.0);
+      int t = 0;  // (q2 k2 mod c2) c1
+      const int st = k2 * c1;
+      for (int q2 = 0; q2 < c2; ++q2) {
+        acc = cfma(h[q2 * c1], Wc[t], acc);
+        t += st;
+        if (t >= c) t -= c;
+      }
+      G[e] = acc;
+    }
+    __syncthreads();
+    V = G;  // the apply below reads the values from here
   }
-  __syncthreads();
   // apply to the sibling's weights at its nodes
   cplx* W = a.W + sys * a.w_sys;
   for (int e = threadIdx.x; e < c * a.rows; e += NTH) {
