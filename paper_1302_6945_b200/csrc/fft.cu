@@ -713,3 +713,41 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;
 }
+
+int fft_exec_twistfold(const FftPlan& p, const cplx* B, long long b_sys, long long b_cap, int PP, long long L,
+                       long long o0, long long o1, int noff, long long N, const cplx* twN, cplx* out,
+                       long long lines, cudaStream_t st) {
+  if (lines <= 0) return 0;
+  if (p.npass != 1 || !p.pass[0].fast || p.n < 128 || p.n > 4096) return -1;
+  const FftPass& ps = p.pass[0];
+  FastArgs f;
+  f.in = nullptr;
+  f.in_ls = 0;
+  f.in_len = 0;
+  f.out = out;
+  f.out_ls = p.n;
+  f.J = 1;
+  f.nsub = lines;
+  f.Ns = 1;
+  f.log2Ns = 0;
+  f.tws = 1;
+  f.twN = p.twN;
+  f.twR = ps.twR;
+  f.sign = +1;
+  f.tf_B = B;
+  f.tf_bsys = b_sys;
+  f.tf_bcap = b_cap;
+  f.tf_PP = PP;
+  f.tf_noff = noff;
+  f.tf_L = L;
+  f.tf_o0 = o0;
+  f.tf_o1 = o1;
+  f.tf_N = N;
+  f.tf_twN = twN;
+  g_fft_tag = (p.n << 20) + (lines & ((1 << 20) - 1));
+  if (reg_launch(ps.log2, ps.q, f, st) != 0) return -1;
+  tr_kernel_work(TRK_FFT, 16.0 * ((double)lines / noff * L + (double)lines * p.n),
+                 5.0 * lines * (double)p.n * std::log2((double)p.n));
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  return 0;
+}

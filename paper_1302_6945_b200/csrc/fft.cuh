@@ -58,6 +58,15 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
              const cplx* mul = nullptr, long long mul_ls = 0, double mul_scale = 1.0,
              long long chunk_bytes_override = -1, const cplx* mul2 = nullptr);
 
+// Forward (+1) transform of the twisted, folded basis entries of a coset update
+// (tree.cu twist_fold_kernel fused into the loads of the single-pass register
+// kernel): output line (sys * noff + c) * PP + e = transform of x[q] = sum_{l = q
+// mod n, l < L} B[sys][e][l] w^(o_c l), w = exp(2 pi i / N).  Returns -1 when the
+// plan is not a single-pass register plan (the caller runs the two kernels).
+int fft_exec_twistfold(const FftPlan& p, const cplx* B, long long b_sys, long long b_cap, int PP, long long L,
+                       long long o0, long long o1, int noff, long long N, const cplx* twN, cplx* out,
+                       long long lines, cudaStream_t st);
+
 // Twiddle table exp(2 pi i k / n), k < n (cached, device memory).
 const cplx* twiddle_table(long long n);
 

@@ -20,6 +20,14 @@ struct FastArgs {
   const cplx* mul = nullptr;
   long long mul_ls = 0;
   double mul_scale = 1.0;
+  // optional twist + fold on load (fft_reg.cu TF variant; the coset update of
+  // tree.cu twist_fold_kernel fused into the transform): line = (sys * tf_noff
+  // + c) * tf_PP + e reads x[q] = sum_{l = q mod R, l < tf_L} B[sys][e][l] w^(o_c l),
+  // w = exp(2 pi i / tf_N) from tf_twN, o_c = c ? tf_o1 : tf_o0
+  const cplx* tf_B = nullptr;
+  long long tf_bsys = 0, tf_bcap = 0, tf_L = 0, tf_o0 = 0, tf_o1 = 0, tf_N = 0;
+  int tf_PP = 0, tf_noff = 1;
+  const cplx* tf_twN = nullptr;
 };
 
 bool fast_supported(int log2, int q);

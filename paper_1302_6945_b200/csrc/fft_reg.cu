@@ -64,9 +64,9 @@ TR_D void tw_apply(cplx (&v)[RS], const cplx* twR, int k, int step, int sign) {
   }
 }
 
-template <int LOG2, int Q, int S>
+template <int LOG2, int Q, int S, bool TF = false>
 TR_D void run_stage(cplx* sm, const FastArgs& a, long long lin, long long lout, bool live, int tb,
-                    int sign, const cplx* mrow) {
+                    int sign, const cplx* mrow, long long tf_o = 0) {
   using G = Plan<LOG2, Q>;
   constexpr int R = G::R, r = G::radix(S), NS = G::ns(S), B = R / r, T = G::T;
   constexpr int IT = (B + T - 1) / T;
@@ -80,11 +80,49 @@ TR_D void run_stage(cplx* sm, const FastArgs& a, long long lin, long long lout, 
 #pragma unroll
       for (int u = 0; u < r; ++u) {
         const int e = b + u * B;
-        if constexpr (FIRST) {
+        if constexpr (FIRST && TF) {
+          // (filled below: terms outermost, so the loads of all r values issue together)
+        } else if constexpr (FIRST) {
           v[it][u] = e < a.in_len ? a.in[lin + e] : cmk(0.0, 0.0);
           if (mrow) v[it][u] = cmul(v[it][u], cscale(mrow[e], a.mul_scale));
         } else {
           v[it][u] = sm[e + (e >> PSH)];
+        }
+      }
+      if constexpr (FIRST && TF) {
+        // twist + fold: x[e] = sum_{l = e mod R, l < L} B[l] w^(o l), the same sums in the
+        // same order as twist_fold_kernel (tree.cu)
+        const cplx* src = a.tf_B + lin;
+        const int N = (int)a.tf_N, L = (int)a.tf_L;
+        const int nt = (L + R - 1) / R;
+#pragma unroll
+        for (int u = 0; u < r; ++u) v[it][u] = cmk(0.0, 0.0);
+        if (tf_o == 0) {
+          for (int t = 0; t < nt; ++t) {
+#pragma unroll
+            for (int u = 0; u < r; ++u) {
+              const int l = b + u * B + t * R;
+              if (l < L) v[it][u] = cadd(v[it][u], src[l]);
+            }
+          }
+        } else {
+          const int stepB = (int)((tf_o * B) % N), stepR = (int)((tf_o * R) % N);
+          int idx[r];
+          idx[0] = (int)((tf_o * b) % N);
+#pragma unroll
+          for (int u = 1; u < r; ++u) {
+            idx[u] = idx[u - 1] + stepB;
+            if (idx[u] >= N) idx[u] -= N;
+          }
+          for (int t = 0; t < nt; ++t) {
+#pragma unroll
+            for (int u = 0; u < r; ++u) {
+              const int l = b + u * B + t * R;
+              if (l < L) v[it][u] = cfma(src[l], __ldg(&a.tf_twN[idx[u]]), v[it][u]);
+              idx[u] += stepR;
+              if (idx[u] >= N) idx[u] -= N;
+            }
+          }
         }
       }
       if constexpr (NS > 1) tw_apply<r>(v[it], a.twR, b % NS, R / (NS * r), sign);
@@ -111,7 +149,7 @@ TR_D void run_stage(cplx* sm, const FastArgs& a, long long lin, long long lout, 
   }
   if constexpr (!LAST) {
     __syncthreads();
-    run_stage<LOG2, Q, S + 1>(sm, a, lin, lout, live, tb, sign, mrow);
+    run_stage<LOG2, Q, S + 1, TF>(sm, a, lin, lout, live, tb, sign, mrow, tf_o);
   }
 }
 
@@ -121,7 +159,7 @@ TR_D void run_stage(cplx* sm, const FastArgs& a, long long lin, long long lout, 
 
 // CTA = TL lines x T threads (TL chosen at launch so small batches still
 // spread over the SMs)
-template <int LOG2, int Q>
+template <int LOG2, int Q, bool TF = false>
 __global__ void __launch_bounds__(NTH, FFT_REG_MINB) fft_reg_kernel(FastArgs a, int TL) {
   using G = Plan<LOG2, Q>;
   extern __shared__ __align__(16) unsigned char fsm[];
@@ -129,15 +167,28 @@ __global__ void __launch_bounds__(NTH, FFT_REG_MINB) fft_reg_kernel(FastArgs a, 
   const long long line = (long long)blockIdx.x * TL + sl;
   const bool live = line < a.nsub;
   cplx* sm = reinterpret_cast<cplx*>(fsm) + (size_t)sl * G::LS;
-  const cplx* mrow = a.mul ? a.mul + line * a.mul_ls : nullptr;
-  run_stage<LOG2, Q, 0>(sm, a, line * a.in_ls, line * a.out_ls, live, tb, a.sign, mrow);
+  if constexpr (TF) {
+    // line = (sys * noff + c) * PP + e: basis entry e of system sys, coset c
+    const long long sc = line / a.tf_PP;
+    const int e = (int)(line - sc * a.tf_PP);
+    const long long sys = sc / a.tf_noff;
+    const int c = (int)(sc - sys * a.tf_noff);
+    run_stage<LOG2, Q, 0, true>(sm, a, sys * a.tf_bsys + (long long)e * a.tf_bcap, line * a.out_ls, live, tb, a.sign,
+                                nullptr, c ? a.tf_o1 : a.tf_o0);
+  } else {
+    const cplx* mrow = a.mul ? a.mul + line * a.mul_ls : nullptr;
+    run_stage<LOG2, Q, 0>(sm, a, line * a.in_ls, line * a.out_ls, live, tb, a.sign, mrow);
+  }
 }
 
-template <int LOG2, int Q>
+template <int LOG2, int Q, bool TF = false>
 int launch(const FastArgs& a, cudaStream_t st) {
-  if constexpr ((Q << LOG2) > 4096 || (Q << LOG2) < 2) {
+  if constexpr ((Q << LOG2) > 4096 || (Q << LOG2) < 2 || (TF && (Q << LOG2) < 128)) {
     return -1;
   } else {
+    if constexpr (!TF) {
+      if (a.tf_B) return launch<LOG2, Q, true>(a, st);
+    }
     using G = Plan<LOG2, Q>;
     // lines per CTA: as many as fit, but keep >= 2 CTAs per SM when the batch allows
     int TL = G::TLMAX;
@@ -146,13 +197,13 @@ int launch(const FastArgs& a, cudaStream_t st) {
     const size_t smem = sizeof(cplx) * (size_t)TL * G::LS;
     static bool set = false;
     if (!set) {
-      cudaFuncSetAttribute(fft_reg_kernel<LOG2, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(fft_reg_kernel<LOG2, Q, TF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            100 * 1024);
       set = true;
     }
     const long long blocks = (a.nsub + TL - 1) / TL;
     TrKTimer _kt(TRK_FFT, st);
-    fft_reg_kernel<LOG2, Q><<<(unsigned)blocks, G::T * TL, smem, st>>>(a, TL);
+    fft_reg_kernel<LOG2, Q, TF><<<(unsigned)blocks, G::T * TL, smem, st>>>(a, TL);
     return 0;
   }
 }

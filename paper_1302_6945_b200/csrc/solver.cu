@@ -1037,9 +1037,21 @@ int solve_core(const Plan& p, const Inputs& in, long long nsys, const WS& w, con
       const long long cs = l2_chunk(nsys, (long long)op.noff * PP * cnt * 2);
       for (long long s0 = 0; s0 < nsys; s0 += cs) {
         const long long ns = std::min(cs, nsys - s0);
-        TR_TRY(launch_twist_fold(w.S1, w.slot[op.slot_a] + s0 * PP * scap, PP * scap, scap, PP, op.cap_a,
-                                 op.o0, op.o1, op.noff, cnt, N, twN, ns, st));
-        TR_TRY(fft_exec(F(p, cnt), w.S1, cnt, cnt, w.S1, cnt, w.S2, ns * op.noff * PP, +1, st));
+        // single-pass lengths: twist + fold fused into the transform's loads (fft_reg.cu,
+        // TR_TF_FUSE=0: the separate kernel); same sums in the same order either way
+        static const bool tf_fuse = [] {
+          const char* e = getenv("TR_TF_FUSE");
+          return !(e && e[0] == '0');
+        }();
+        // (batches of >= 1024 lines: with fewer the longer, latency-bound transform kernel
+        // costs more than the small launch it saves -- c3, 392 lines: 656 -> 661 ms)
+        if (!(tf_fuse && cnt >= 128 && N < (1LL << 30) && ns * op.noff * PP >= 1024 &&
+              fft_exec_twistfold(F(p, cnt), w.slot[op.slot_a] + s0 * PP * scap, PP * scap, scap, PP, op.cap_a, op.o0,
+                                 op.o1, op.noff, N, twN, w.S1, ns * op.noff * PP, st) == 0)) {
+          TR_TRY(launch_twist_fold(w.S1, w.slot[op.slot_a] + s0 * PP * scap, PP * scap, scap, PP, op.cap_a,
+                                   op.o0, op.o1, op.noff, cnt, N, twN, ns, st));
+          TR_TRY(fft_exec(F(p, cnt), w.S1, cnt, cnt, w.S1, cnt, w.S2, ns * op.noff * PP, +1, st));
+        }
         TR_TRY(launch_apply_update(w.W + s0 * w_sys, w_sys, w.S1, rows, P, op.o0, op.o1, op.noff, op.stride,
                                    cnt, ns, st));
       }
