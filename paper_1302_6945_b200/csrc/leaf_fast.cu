@@ -976,6 +976,7 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
   const int tid = threadIdx.x, lane = tid & 31, nt = blockDim.x;
   const int warp = __shfl_sync(FULL, tid >> 5, 0);
   const int nw = nt >> 5;
+  if (g_chain_trace_on && sys == 0 && rank == 0 && tid == 0) g_chain_trace[3072 + 129] = clock64();  // kernel entry
   const cplx* W = a.W + (long long)sys * a.w_sys;
   const long long rowstride = (long long)RP;
   const int H = (K + 31) / 32;

@@ -20,7 +20,8 @@ f(1, None, 0)
 db.run(); torch.cuda.synchronize()
 buf = (C.c_longlong * 4096)()
 f(0, C.addressof(buf), 4096)
-b = np.frombuffer(buf, dtype=np.int64)[3072:3072 + 129].copy()
+b = np.frombuffer(buf, dtype=np.int64)[3072:3072 + 130].copy()
+print("kernel entry to the first chain step: %d cycles" % (b[0] - b[129]))
 t0 = b[0]
 for r in range(4):
     x = b[32 * r:32 * r + 24]
