@@ -211,9 +211,12 @@ __global__ void __launch_bounds__(NTH) combine_small_kernel(CombineArgs a) {
   }
 }
 
+#ifndef TR_CS_NTH
+#define TR_CS_NTH 512  // threads per CTA of the redundant variant (30-56 lines per CTA)
+#endif
 template <int P, int R1, int R2, bool DS = false>
 int launch_cs(const CombineArgs& a, long long nsys, cudaStream_t st) {
-  constexpr int NTH = 256, R = R1 * R2, NL = DS ? 2 * P : P + P * P, LP = R + 1;
+  constexpr int NTH = DS ? 256 : TR_CS_NTH, R = R1 * R2, NL = DS ? 2 * P : P + P * P, LP = R + 1;
   if constexpr (!DS) {
     // more CTAs than one wave of the redundant variant (one CTA per SM at R >= 128)
     if (P * nsys > 296) return launch_cs<P, R1, R2, true>(a, nsys, st);
@@ -291,9 +294,12 @@ int launch_combine_small(const CombineArgs& a, long long nsys, cudaStream_t st) 
 //   w[r][node_k][:] <- w[r][node_k][:] V(sigma_k)        (apply)
 namespace {
 
+#ifndef TR_UPD_NTH
+#define TR_UPD_NTH 1024  // threads per CTA: the phases are short per-entry loops, latency-bound at 256
+#endif
 template <int P>
-__global__ void __launch_bounds__(256) update_small_kernel(UpdateArgs a) {
-  constexpr int PP = P * P, NTH = 256;
+__global__ void __launch_bounds__(TR_UPD_NTH) update_small_kernel(UpdateArgs a) {
+  constexpr int PP = P * P, NTH = TR_UPD_NTH;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int c = a.cnt;
   cplx* G = reinterpret_cast<cplx*>(smraw);  // [PP][c]
@@ -413,14 +419,14 @@ int launch_update_small(const UpdateArgs& a, long long nsys, cudaStream_t st) {
       cudaFuncSetAttribute(update_small_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       set5 = true;
     }
-    update_small_kernel<5><<<grid, 256, smem, st>>>(a);
+    update_small_kernel<5><<<grid, TR_UPD_NTH, smem, st>>>(a);
   } else {
     static bool set7 = false;
     if (!set7) {
       cudaFuncSetAttribute(update_small_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       set7 = true;
     }
-    update_small_kernel<7><<<grid, 256, smem, st>>>(a);
+    update_small_kernel<7><<<grid, TR_UPD_NTH, smem, st>>>(a);
   }
   TR_CUDA_CHECK(cudaGetLastError());
   return 0;

@@ -471,15 +471,17 @@ bool leaf_supported(int P, int K) {
   return false;
 }
 
-int leaf_launch(const LeafArgs& a_in, int nsys, cudaStream_t st, const SplitState* split) {
+int leaf_launch(const LeafArgs& a_in, int nsys, cudaStream_t st, const SplitState* split, bool exact_pass) {
   if (nsys <= 0) return 0;
   LeafArgs a = a_in;
   if (split && leaf_fast_supported(a)) {
     TR_TRY_LEAF(leaf_fast_launch(a, *split, nsys, st));
     a.only = split->need;  // re-run leaves whose rescale speculation failed
+    if (!exact_pass) return 0;  // (flagged in split->any_viol: the caller re-runs with the fallback)
   } else if (split && leaf_split_supported(a)) {
     TR_TRY_LEAF(leaf_split_launch(a, *split, nsys, st));
     a.only = split->need;
+    if (!exact_pass) return 0;
   }
   int rc;
   if (a.P == 5) rc = launch_t<5, 3, 96>(a, nsys, st);

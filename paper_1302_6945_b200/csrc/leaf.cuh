@@ -43,11 +43,15 @@ struct LeafArgs {
   const int* only = nullptr; // when set: only systems with only[sys] == -2 run (exact fallback)
   int len_eff = 0;           // coefficients the parent's fused combine reads (0: all)
   int* trim_over = nullptr;  // [sys] the exact kernel counts a basis longer than len_eff here
+  int force_viol = 0;        // test hook (TR_TEST_VIOL): system 0 reports a violated speculation here
 };
 
 struct SplitState;
 // Launch the leaf sweep for every system of the batch (split kernels when a
 // SplitState is given and the shape fits, else the exact coupled kernel).
-int leaf_launch(const LeafArgs& a, int nsys, cudaStream_t st, const SplitState* split = nullptr);
+// exact_pass = false: the exact fallback for leaves the split kernels hand over is not
+// launched (they are flagged in split->any_viol; the caller re-runs with it).
+int leaf_launch(const LeafArgs& a, int nsys, cudaStream_t st, const SplitState* split = nullptr,
+                bool exact_pass = true);
 // Whether a (P, K) leaf fits the register kernels.
 bool leaf_supported(int P, int K);

@@ -783,6 +783,7 @@ TR_D void finish_attempt(const LeafArgs& a, const SplitState& s, int round, int 
     const bool done = s.res_best[sys] <= a.check_tol || round + 1 >= a.nattempts;
     if (viol) {
       s.need[sys] = SPLIT_EXACT;  // speculation failed: exact coupled kernel
+      *s.any_viol = 1;
     } else if (!done) {
       s.need[sys] = round + 1;    // retry with the next absorption order
     } else {
@@ -1417,10 +1418,11 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
   __syncthreads();
   if (g_chain_trace_on && sys == 0 && tid == 0) g_chain_trace[3072 + 128] = clock64();
   // ---- commit (ref tanint.py:430-434) or hand the leaf to the exact kernel ----
-  if (viol) {
+  if (viol || (a.force_viol && sys == 0)) {
     if (tid == 0) {
       s.viol[sys] = 1;
       s.need[sys] = SPLIT_EXACT;
+      *s.any_viol = 1;
     }
     return;
   }

@@ -577,6 +577,7 @@ __global__ void __launch_bounds__(CK) leaf_check_kernel(LeafArgs a, SplitState s
     const bool done = s.res_best[sys] <= a.check_tol || round + 1 >= a.nattempts;
     if (s.viol[sys]) {
       s.need[sys] = SPLIT_EXACT;  // speculation failed: exact coupled kernel
+      *s.any_viol = 1;
     } else if (!done) {
       s.need[sys] = round + 1;    // retry with the next absorption order
     } else {

@@ -21,6 +21,7 @@ struct SplitState {
   double* factor_best;
   double* res_best;
   int* viol;           // [sys] rescale speculation violated
+  int* any_viol;       // [1] sticky: some leaf of some system was handed to the exact kernel
   double* colpart;     // [sys][8][8] per-row column max^2 (row-parallel build)
 };
 

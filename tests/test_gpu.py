@@ -642,3 +642,52 @@ def test_fused_two_pass_fft_modes(gpu, mode):
         err = float(l.split(" err ")[1].split()[0])
         err2 = float(l.split("inplace/inv ")[1].split()[0])
         assert err < 5e-15 and err2 < 5e-15, l
+
+
+_SPEC_CODE = r"""
+import hashlib, sys
+import numpy as np
+import paper_1302_6945_b200 as tb
+from paper_1302_6945_b200 import workloads as wl
+import toepreg_oracle as O
+h = hashlib.sha1()
+errs = []
+for n, count, seed in ((4096, 3, 3), (256, 3, 7)):      # CG refinement / direct refinement
+    raw = wl.c5_random(n=n, count=count, seed=seed)
+    probs = [wl.to_problem(raw, tb, i) for i in range(count)]
+    for p, r in zip(probs, tb.solve_tikhonov_batch(probs)):
+        h.update(r.x_hat.tobytes())
+        h.update(r.final_col_degrees.tobytes())
+        if n == 256:
+            x = O.dense_solution(p)
+            errs.append(float(np.linalg.norm(r.x_hat - x) / np.linalg.norm(x)))
+print(h.hexdigest(), max(errs))
+"""
+
+
+def test_speculative_direct_phase_reruns_with_the_exact_fallback(gpu):
+    """The direct phase leaves the exact-fallback leaf launches out and runs
+    again with them only when a leaf was handed over (csrc/solver.cu
+    run_solve).  TR_TEST_VIOL makes system 0 hand a leaf over: the result must
+    equal the non-speculative run (TR_SPEC_LEAF=0) bit for bit, with and
+    without a hand-over, on the CG and the direct refinement paths."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+
+    def go(**env):
+        e = dict(os.environ, **env)
+        e["PYTHONPATH"] = os.pathsep.join([ROOT, os.path.join(ROOT, "oracle"), e.get("PYTHONPATH", "")])
+        out = subprocess.run([sys.executable, "-c", _SPEC_CODE], env=e, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        digest, err = out.stdout.split()
+        return digest, float(err)
+
+    base_on, e1 = go(TR_SPEC_LEAF="1")
+    base_off, e2 = go(TR_SPEC_LEAF="0")
+    assert base_on == base_off and max(e1, e2) < 1e-12
+    for leaf in ("0", "2"):
+        on, e3 = go(TR_SPEC_LEAF="1", TR_TEST_VIOL=leaf)
+        off, e4 = go(TR_SPEC_LEAF="0", TR_TEST_VIOL=leaf)
+        assert on == off, leaf
+        assert max(e3, e4) < 1e-12
