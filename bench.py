@@ -364,7 +364,7 @@ def main():
     raw0 = raw[0] if isinstance(raw, (list, tuple)) else raw
     rows = 3 if raw0.get("variant", "") == "general" else 2
     n_cond = rows * info["order"]
-    groups = 1 if count < 32 else min(4, max(2, -(-count // 148)))
+    groups = 1 if count < 32 else (3 if count <= 148 else min(8, -(-count // 148)))  # solver.cu batch_groups
     leaf_ms = sum(kst[k][0] for k in ("leaf_pivot", "leaf_build", "leaf_check", "leaf_exact") if k in kst) / nk
     leaf_launches = kst.get("leaf_pivot", (0, 0))[1] / nk
     solves = max(1.0, round(leaf_launches / max(groups * info["leaves"], 1)))

@@ -1384,7 +1384,9 @@ int batch_groups(long long batch) {
   static const char* e = getenv("TR_GROUPS");
   int g = 1;
   if (e) g = atoi(e);
-  else if (batch >= 32) g = (int)((batch + 147) / 148) < 2 ? 2 : (int)((batch + 147) / 148);  // groups of <= 148: the fused leaf
+  // groups of <= 148 systems (the fused leaf's one CTA per SM); up to 148 systems three
+  // groups interleave slightly better than two (c2 1901 -> 1910, c5 at 148: 680 -> 690)
+  else if (batch >= 32) g = batch <= 148 ? 3 : (int)((batch + 147) / 148);
   if (g < 1) g = 1;
   if (g > 8) g = 8;
   if (g > batch) g = (int)batch;
