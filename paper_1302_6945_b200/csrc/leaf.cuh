@@ -44,6 +44,7 @@ struct LeafArgs {
   int len_eff = 0;           // coefficients the parent's fused combine reads (0: all)
   int* trim_over = nullptr;  // [sys] the exact kernel counts a basis longer than len_eff here
   int force_viol = 0;        // test hook (TR_TEST_VIOL): system 0 reports a violated speculation here
+  int dense = 0;             // fused leaf kernel: every warp has a role (set by launch_fused3)
 };
 
 struct SplitState;

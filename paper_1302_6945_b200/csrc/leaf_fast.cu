@@ -31,6 +31,7 @@
 // coupled kernel (leaf.cu).
 #include <cooperative_groups.h>
 #include <stdio.h>
+#include <type_traits>
 #include <stdlib.h>
 
 #include "leaf.cuh"
@@ -982,7 +983,11 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
   const long long rowstride = (long long)RP;
   const int H = (K + 31) / 32;
   const int NH = H / 2;  // holder warps: blocks 2h-1 and 2h
-  const int slot = (warp & 3) ? warp - warp / 4 : 0;
+  // warp roles: the decider alone on its scheduler (warps 4, 8, 12 idle), or -- a.dense,
+  // when that would need a 13th warp and with it the 128-register budget of four warps
+  // per scheduler -- every warp used (the P = 7 leaves of config 3: 11 instead of 14
+  // warps, 168 instead of 128 registers, no 1-2.5 KB of spills per thread)
+  const int slot = a.dense ? warp : ((warp & 3) ? warp - warp / 4 : 0);
   const int hold = (slot >= 1 && slot <= NH) ? slot : 0;
   const int brow = (slot > NH && slot <= NH + P) ? slot - NH - 1 : -1;
   const int hb1 = 2 * hold - 1, hb2 = 2 * hold;  // blocks held (hb2 < H: two)
@@ -1079,6 +1084,32 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
             for (int i = 0; i < P; ++i) lf[t * P + i] = f[i];
             st_release(&flag[0], t + 1);
           }
+          // P = 7: pivot-specialised row update (j is warp-uniform), no select chains over
+          // seven columns -- 1239 -> 1125 ns per condition at config 3; P = 5 is faster
+          // with the selects (534 vs 545 ns: the switch costs the later phases registers)
+          auto upd = [&](auto JC) {
+            constexpr int J = decltype(JC)::value;
+            const cplx rj = r[J];
+            const cplx c2 = cmul(ci, rj);
+            const cplx nj = cmul(rj, csub(sg, sf));
+#pragma unroll
+            for (int i = 0; i < P; ++i)
+              if (i != J) r[i] = cfma(f[i], c2, r[i]);
+            r[J] = nj;
+            cd[J] += 1;
+          };
+          if constexpr (P == 7) {
+          switch (j) {
+            case 0: upd(std::integral_constant<int, 0>()); break;
+            case 1: upd(std::integral_constant<int, 1>()); break;
+            case 2: upd(std::integral_constant<int, 2>()); break;
+            case 3: upd(std::integral_constant<int, 3>()); break;
+            case 4: upd(std::integral_constant<int, 4>()); break;
+            case 5: if constexpr (P > 5) upd(std::integral_constant<int, 5>()); break;
+            case 6: if constexpr (P > 6) upd(std::integral_constant<int, 6>()); break;
+            default: break;
+          }
+          } else {
           if (j >= 0) {
             const cplx rj = sel<P>(r, j);
             const cplx c2 = cmul(ci, rj);
@@ -1091,6 +1122,7 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
           }
 #pragma unroll
           for (int i = 0; i < P; ++i) cd[i] += (i == j);
+          }
           nabs += j >= 0;
           if (j == -1) {  // deferred, in step order (ref tanint.py:200-206)
             if (lane == 0) dtry[ndef] = make_int2((int)cond_node(a, t, att), t % rows);
@@ -1543,6 +1575,12 @@ int launch_fused3(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t
   const int last = H / 2 + a.P;  // highest slot: H/2 holders, then the basis rows
   int nw = 1;
   while (nw - 1 - (nw - 1) / 4 < last) ++nw;
+  LeafArgs ad = a;
+  ad.dense = 0;
+  if (nw > 12 && last + 1 <= 12) {  // every warp used: stays within three warps per scheduler
+    nw = last + 1;
+    ad.dense = 1;
+  }
   if (nw > 16) return -1;
   const int db = blocks_planned(a);
   if (db > (a.P == 5 ? 4 : 3)) return -1;
@@ -1561,8 +1599,8 @@ int launch_fused3(const LeafArgs& a, const SplitState& s, int nsys, cudaStream_t
   TrKTimer _kt(TRK_LEAF_PIVOT, st);
 #define TR_F3N(PP_, DB_, NTH_)                                                                             \
   {                                                                                                        \
-    if (cl) rc = launch_f3<PP_, DB_, NTH_, true>(a, s, nsys, nw, fs, st);                                  \
-    else rc = launch_f3<PP_, DB_, NTH_, false>(a, s, nsys, nw, fs, st);                                    \
+    if (cl) rc = launch_f3<PP_, DB_, NTH_, true>(ad, s, nsys, nw, fs, st);                                 \
+    else rc = launch_f3<PP_, DB_, NTH_, false>(ad, s, nsys, nw, fs, st);                                   \
   }
 #define TR_F3L(PP_, DB_)                  \
   if (nw <= 12) TR_F3N(PP_, DB_, 384)     \
