@@ -2,7 +2,7 @@
 # Round check for tag $R: gpu tests, smoke, bench lines (c2 default with the CPU arm, c5, c3, c4, c1,
 # c5b, the reference arm), then ncu: launch list of the c2 timed region and --set full captures of the
 # top kernels.  Every ncu command runs only after the same command line exited 0 without ncu.
-R=${R:-r2f}
+R=${R:-r2g}
 O=gpurun_out/$R
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
