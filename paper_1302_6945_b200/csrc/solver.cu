@@ -272,6 +272,9 @@ struct Plan {
   int nblk = 0;
   std::map<long long, FftPlan> fft;
   bool fft_ready = false;
+  // solves left for which the direct phase is not run speculatively (run_solve): set
+  // when a solve of this shape needed the exact leaf fallback (results do not depend on it)
+  mutable std::atomic<int> spec_holdoff{0};
 };
 
 int gcd_ll(long long a, long long b) {
@@ -1582,13 +1585,23 @@ int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine,
   auto set_exact = [&](int v) {
     for (auto& g : gs) g.in.exact_pass = v;
   };
-  set_exact(spec_leaf ? 0 : 1);
+  // A shape whose last solve handed a leaf over (ill-conditioned data: config 4 does)
+  // skips the speculation for the next 16 solves instead of paying the phase twice.
+  bool spec = spec_leaf;
+  if (spec && p.spec_holdoff.load() > 0) {
+    p.spec_holdoff.fetch_sub(1);
+    spec = false;
+  }
+  set_exact(spec ? 0 : 1);
   TR_TRY(run_phase(p, gs, nsys, PH_DIRECT, cg, st, ws));
-  if (spec_leaf && !cg) {  // (with CG the flag rides on the first block's host check)
+  if (spec && !cg) {  // (with CG the flag rides on the first block's host check)
     bool viol = false;
     TR_TRY(any_leaf_viol(gs, st, &viol));
     set_exact(1);
-    if (viol) TR_TRY(run_phase(p, gs, nsys, PH_DIRECT, cg, st, ws));
+    if (viol) {
+      p.spec_holdoff.store(16);
+      TR_TRY(run_phase(p, gs, nsys, PH_DIRECT, cg, st, ws));
+    }
   }
   if (ptimes) TR_CUDA_CHECK(cudaEventRecord(pe[1], st));
   struct PhaseReport {
@@ -1613,7 +1626,7 @@ int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine,
   }
   bool any = true;
   const int cap_up = (cap + CG_CHECK - 1) / CG_CHECK * CG_CHECK;  // whole check intervals, as with blocks of CG_CHECK
-  bool spec_pending = spec_leaf;
+  bool spec_pending = spec;
   for (int it = 0; it < cap_up && any; it += CG_BLOCK) {
     // the abandon check runs when the iteration count reaches a multiple of CG_CHECK
     const bool chk = (it + CG_BLOCK) % CG_CHECK == 0;
@@ -1624,6 +1637,7 @@ int run_solve(const Plan& p, std::vector<Group>& gs, long long nsys, int refine,
       spec_pending = false;
       set_exact(1);
       if (viol) {  // a leaf was handed over: the direct phase again with the fallback, CG from its start
+        p.spec_holdoff.store(16);
         TR_TRY(run_phase(p, gs, nsys, PH_DIRECT, cg, st, ws));
         any = true;
         it = -CG_BLOCK;
