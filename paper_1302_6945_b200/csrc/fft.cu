@@ -570,14 +570,10 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
       const char* e = getenv("TR_FFT_C2_GROUPS");  // 1: also with concurrent stream groups
       return e && e[0] == '1';
     }();
-    static const long long c2_only = [] {
-      const char* e = getenv("TR_FFT_C2_ONLY");  // diagnostic: fuse only this length
-      return e ? atoll(e) : 0LL;
-    }();
     // (a batch split into stream groups keeps the chunked launches: their short
     // kernels interleave with the other groups' leaf sweeps, which need whole SMs
     // and would otherwise wait behind a long cluster launch -- measured slower)
-    if (c2_on && (!g_fft_groups || c2_force) && (c2_only == 0 || c2_only == n)) {
+    if (c2_on && (!g_fft_groups || c2_force)) {
       const long long N1 = 1LL << p.a1, N2 = (long long)p.q2 << p.a2;
       ColArgs ca, cb;
       ca.in = in;
@@ -609,24 +605,7 @@ int fft_exec(const FftPlan& p, const cplx* in, long long in_ls, long long in_len
       cb.out_es = (int)N1;
       cb.subs = (int)N1;
       cb.twR = p.tw2;
-      // TR_FFT_C2_LINES: at most that many lines per launch (0: all in one)
-      static const long long c2_lines = [] {
-        const char* e = getenv("TR_FFT_C2_LINES");
-        return e ? atoll(e) : 0LL;
-      }();
-      const long long step = c2_lines > 0 ? c2_lines : lines;
-      bool ok = true;
-      for (long long s0 = 0; s0 < lines && ok; s0 += step) {
-        ColArgs xa = ca, xb = cb;
-        xa.in = in + s0 * in_ls;
-        xa.lines = xb.lines = std::min(step, lines - s0);
-        if (mul) xa.mul = mul + s0 * mul_ls;
-        if (mul2) xa.mul2 = mul2 + s0 * mul_ls;
-        xb.out = out + s0 * out_ls;
-        ok = col2_launch(p.a1, p.a2, p.q2, xa, xb, n, st) == 0;
-        if (!ok && s0 > 0) { tr_set_error("fused two-pass FFT launch failed (n=%lld)", n); return 4; }
-      }
-      if (ok) {
+      if (col2_launch(p.a1, p.a2, p.q2, ca, cb, n, st) == 0) {
         TR_CUDA_CHECK(cudaGetLastError());
         return 0;
       }
