@@ -92,6 +92,30 @@ TR_D int ld_acquire(const int* p) {
                : "memory");
   return v;
 }
+// Predicated shared-memory stores on precomputed 32-bit shared addresses: the
+// decider publishes a step from lane 0 without a divergent branch (the
+// branch's lane-0 block -- address rematerialisation through S2R, seven
+// stores, the fence -- sat in the middle of every chain step: ~29% of the
+// step's stall samples, profiles/r2_leaf_publish.txt)
+TR_D unsigned smem_u32(const void* p) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("" : "+r"(a));  // opaque: held in a register, not recomputed per step
+  return a;
+}
+TR_D void sts_c_if(int pred, unsigned addr, cplx v) {
+  asm volatile("{ .reg .pred p; setp.ne.s32 p, %0, 0; @p st.shared.v2.f64 [%1], {%2, %3}; }" ::"r"(pred), "r"(addr),
+               "d"(v.x), "d"(v.y)
+               : "memory");
+}
+TR_D void sts_i_if(int pred, unsigned addr, int v) {
+  asm volatile("{ .reg .pred p; setp.ne.s32 p, %0, 0; @p st.shared.u32 [%1], %2; }" ::"r"(pred), "r"(addr), "r"(v)
+               : "memory");
+}
+TR_D void st_release_if(int pred, unsigned addr, int v) {
+  asm volatile("{ .reg .pred p; setp.ne.s32 p, %0, 0; @p st.release.cta.shared.u32 [%1], %2; }" ::"r"(pred),
+               "r"(addr), "r"(v)
+               : "memory");
+}
 // wait until the published step counter passes t (backs off so that spinning
 // warps leave the shared-memory pipe to the decider)
 TR_D int wait_steps(const int* flag, int t, int avail) {
@@ -1056,6 +1080,8 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
 #pragma unroll
       for (int i = 0; i < P; ++i) cd[i] = cd0[i];
       int nabs = 0, ndef = 0;  // absorbed / deferred conditions (the chain epilogue, kept on the fly)
+      const unsigned a_lf = smem_u32(lf), a_lci = smem_u32(lci), a_lj = smem_u32(lj), a_flag = smem_u32(flag);
+      const int pub = lane == 0;
       for (int b = 0; b < H; ++b) {
         if (b > 0) {
           while (ld_acquire(&flag[1]) < b) {
@@ -1077,12 +1103,13 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
           const int j = decide_bits<P>(f, cd, thr2, fj, a2j);
           const double inv2 = rcp_nr(a2j);
           const cplx ci = cmk(-fj.x * inv2, fj.y * inv2);
-          if (lane == 0) {
-            lj[t] = j;
-            lci[t] = ci;
+          {
+            const unsigned plf = a_lf + (unsigned)t * (P * 16u);
+            sts_i_if(pub, a_lj + 4u * (unsigned)t, j);
+            sts_c_if(pub, a_lci + 16u * (unsigned)t, ci);
 #pragma unroll
-            for (int i = 0; i < P; ++i) lf[t * P + i] = f[i];
-            st_release(&flag[0], t + 1);
+            for (int i = 0; i < P; ++i) sts_c_if(pub, plf + 16u * i, f[i]);
+            st_release_if(pub, a_flag, t + 1);
           }
           // P = 7: pivot-specialised row update (j is warp-uniform), no select chains over
           // seven columns -- 1239 -> 1125 ns per condition at config 3; P = 5 is faster

@@ -65,6 +65,27 @@ __global__ void lat_kernel(double* out, long long* cyc, int n, double s, int sel
   for (int i = 0; i < n; ++i) a = sqrt(a + s);
   t1 = clock64();
   if (threadIdx.x == 0) cyc[7] = t1 - t0;
+  // 8: MUFU.RCP64H estimate + dependent DADD (subtract one DFMA latency)
+  t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    double r;
+    asm volatile("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+    a = r + s;
+  }
+  t1 = clock64();
+  if (threadIdx.x == 0) cyc[8] = t1 - t0;
+  // 9: 64-bit unsigned compare + select chain (the pivot tree's level)
+  unsigned long long u = (unsigned long long)__double_as_longlong(a), w = u ^ 0x5555ull;
+  t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    const bool take = w > u;
+    const unsigned long long nu = take ? w : u;
+    w = (take ? u : w) + 0x10001ull * (unsigned)i;
+    u = nu;
+  }
+  t1 = clock64();
+  if (threadIdx.x == 0) cyc[9] = t1 - t0;
+  a += __longlong_as_double((long long)(u ^ w));
   out[threadIdx.x] = a;
 }
 
@@ -74,7 +95,7 @@ int main() {
   cudaMalloc(&out, 4096 * sizeof(double));
   cudaMallocManaged(&cyc, 16 * sizeof(long long));
   const char* names[] = {"DFMA dep", "DMUL dep", "SHFL dep", "LDS dep", "DDIV(1/x) dep",
-                         "switch5+DFMA", "syncthreads", "DSQRT dep"};
+                         "switch5+DFMA", "syncthreads", "DSQRT dep", "MUFU.RCP64H+DADD", "cmp64+sel"};
   for (int threads : {32, 256, 512}) {
     int n = 1024;
     lat_kernel<<<1, threads>>>(out, cyc, n, 1e-9, 1);
@@ -82,7 +103,7 @@ int main() {
     lat_kernel<<<1, threads>>>(out, cyc, n, 1e-9, 1);
     cudaDeviceSynchronize();
     printf("block=%d:", threads);
-    for (int i = 0; i < 8; ++i) printf("  %s=%.1f", names[i], (double)cyc[i] / n);
+    for (int i = 0; i < 10; ++i) printf("  %s=%.1f", names[i], (double)cyc[i] / n);
     printf("\n");
   }
   return 0;
