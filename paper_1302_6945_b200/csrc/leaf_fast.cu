@@ -997,7 +997,7 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
   __shared__ double csafe[8];
   __shared__ double wred[16];
   __shared__ F3Book bk;
-  __shared__ long long tsm[24];  // clock stamps of system 0 (tr_debug_chain_trace)
+  __shared__ long long tsm[32];  // clock stamps of system 0 (tr_debug_chain_trace)
   __shared__ int cd0[8];         // column degrees entering the leaf
   const int tid = threadIdx.x, lane = tid & 31, nt = blockDim.x;
   const int warp = __shfl_sync(FULL, tid >> 5, 0);
@@ -1084,8 +1084,10 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
       const int pub = lane == 0;
       for (int b = 0; b < H; ++b) {
         if (b > 0) {
+          const long long tw0 = clock64();
           while (ld_acquire(&flag[1]) < b) {
           }
+          if (lane == 0 && b < 8) tsm[24 + b] = clock64() - tw0;  // hand-over wait of block b
 #pragma unroll
           for (int i = 0; i < P; ++i) r[i] = xfer[lane * P + i];
           sg = lsig[min(32 * b + lane, K - 1)];
@@ -1400,7 +1402,7 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
     if (tid == 0) {
       tsm[15] = clock64();
       if (g_chain_trace_on && sys == 0 && round < 4)
-        for (int e = 0; e < 24; ++e) g_chain_trace[3072 + 32 * round + e] = tsm[e];
+        for (int e = 0; e < 32; ++e) g_chain_trace[3072 + 32 * round + e] = tsm[e];
     }
     // ---- best attempt, retry or commit ----
     if (tid == 0) {

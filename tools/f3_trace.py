@@ -30,5 +30,6 @@ for r in range(4):
         print("round %d: start %d, block starts %s, decider end %d, chain+basis %d, normalised %d, residual %d"
               % (r, x[0] - t0, blocks, x[12] - x[0], x[13] - x[0], x[14] - x[0], x[15] - x[0]))
         print("   residual detail (fold, dft, rows per coset):", [int(v - x[0]) for v in x[16:22]])
+        print("   hand-over waits of blocks 1..7 (cycles):", [int(v) for v in b[32 * r + 25:32 * r + 32]])
         print("   epilogue done %d, normalised rows written %d" % (x[22] - x[0], x[23] - x[0]))
 print("commit at %d" % (b[128] - t0))
