@@ -16,6 +16,8 @@ Printed JSON (rank 0): the contract keys plus
   roofline     the dominant kernel class: leaf classes FP64-bound against the
                FP64 FMA peak measured by tr_fp64_peak(); FFT / combine /
                update HBM-bound against MEASURED_PEAKS.json hbm_gbs
+  roofline_hbm the batched-FFT class against the measured HBM peak (tracked from round 1)
+  roofline_solve  the whole solve against SURVEY 8(d)'s summed roofline
   chain        the sequential absorption chain: conditions per
                solve and the leaf time per absorbed condition
   kernels      per-class device time from CUDA events (separate pass)
@@ -357,6 +359,25 @@ def main():
     roof["avg_launch_ms"] = ms / max(nl, 1)
     roof["share_of_step"] = ms / tot_k
 
+    # the HBM-bound class the round-1 review tracks (batched FFT), whatever the dominant class is
+    roof_hbm = None
+    if "fft" in kst and kst["fft"][0] > 0:
+        fms, fnl, fby, ffl = kst["fft"]
+        fach = fby / (fms * 1e-3) / 1e9
+        roof_hbm = {"kernel": "fft", "bound": "hbm", "achieved": fach, "peak": hbm_peak, "unit": "GB/s",
+                    "peak_source": hbm_src, "frac": fach / hbm_peak if hbm_peak else None,
+                    "traffic": ncu_traffic(args.config, "fft"),
+                    "algorithmic_bytes_per_launch": fby / max(fnl, 1), "avg_launch_ms": fms / max(fnl, 1),
+                    "share_of_step": fms / tot_k}
+    # whole solve against SURVEY 8(d)'s summed per-class roofline (T_roof per solve at 37 TFLOP/s
+    # FP64 and 6.449 TB/s: the table's "roofline solves/s/GPU" column)
+    roof_table = {"c1": 5.5e5, "c2": 2.24e4, "c3": 667.0, "c4": 6.49e3, "c5": 6.49e3, "c5b": 17.5}
+    roof_solve = None
+    if args.config in roof_table:
+        rs = roof_table[args.config] * world
+        roof_solve = {"roofline_solves_per_s": rs, "frac": value / rs,
+                      "source": "SURVEY 8(d): sum over kernel classes of max(flops / FP64 peak, bytes / HBM peak)"}
+
     # the sequential absorption chain: every condition of a solve passes
     # through one leaf sweep in order (SURVEY 8(d) chain bound C x t_step);
     # groups of <= 148 systems (solver.cu batch_groups) run one after the
@@ -395,6 +416,8 @@ def main():
                 "d2h_bytes_per_step": db.d2h_bytes,
                 "path": "DeviceBatch.stage (pinned H2D) -> run -> x D2H"},
         "roofline": roof,
+        "roofline_hbm": roof_hbm,
+        "roofline_solve": roof_solve,
         "chain": chain,
         "kernels": {k: {"ms_per_step": v[0] / nk, "launches_per_step": v[1] / nk,
                         "share": v[0] / tot_k,

@@ -1006,7 +1006,15 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
   const cplx* W = a.W + (long long)sys * a.w_sys;
   const long long rowstride = (long long)RP;
   const int H = (K + 31) / 32;
-  const int NH = H / 2;  // holder warps: blocks 2h-1 and 2h
+  // holder warps: blocks 2h-1 and 2h; when the layout leaves a warp unused (P = 5, K = 192:
+  // 3 holders + 5 basis rows on 9 warps) the first two blocks -- the ones with the least
+  // time to catch up -- get a holder each (TR_EXTRA_HOLDER)
+#ifndef TR_EXTRA_HOLDER
+#define TR_EXTRA_HOLDER 1
+#endif
+  const int nslots = a.dense ? nw - 1 : nw - 1 - (nw - 1) / 4;
+  const bool extra = TR_EXTRA_HOLDER && !a.dense && H >= 4 && H / 2 + 1 + P <= nslots;
+  const int NH = H / 2 + (extra ? 1 : 0);
   // warp roles: the decider alone on its scheduler (warps 4, 8, 12 idle), or -- a.dense,
   // when that would need a 13th warp and with it the 128-register budget of four warps
   // per scheduler -- every warp used (the P = 7 leaves of config 3: 11 instead of 14
@@ -1014,7 +1022,9 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
   const int slot = a.dense ? warp : ((warp & 3) ? warp - warp / 4 : 0);
   const int hold = (slot >= 1 && slot <= NH) ? slot : 0;
   const int brow = (slot > NH && slot <= NH + P) ? slot - NH - 1 : -1;
-  const int hb1 = 2 * hold - 1, hb2 = 2 * hold;  // blocks held (hb2 < H: two)
+  // blocks held (hb2 < H: two)
+  const int hb1 = extra ? (hold <= 2 ? hold : 2 * hold - 3) : 2 * hold - 1;
+  const int hb2 = extra ? (hold <= 2 ? H : 2 * hold - 2) : 2 * hold;
 
   // ---- once per leaf: weights, DFT table, coset twists, weight scale ----
   double sc = 0.0;
