@@ -16,7 +16,9 @@
 //   * holders apply published steps to the later rows (acquire polling) and
 //     hand their block to the decider when it gets there;
 //   * P basis-row warps replay the log on the coefficient cube (coefficient
-//     l = 32 d + lane in registers, structurally-zero blocks skipped);
+//     l = 32 d + lane in registers, structurally-zero blocks skipped); for
+//     P = 5 the multipliers mu_i = f_i c_i they all need are formed once per
+//     step by the mu warp (warp 4, beside the decider) and read from lmu;
 //   * finish_attempt: column normalisation, the self-residual (coset fold +
 //     factored M-point DFT) and the retry rule; attempts 0 and 1 run side by
 //     side in a 2-CTA cluster when the batch leaves SMs free.
@@ -57,6 +59,9 @@ constexpr double RESCALE_TRIGGER = 1e8;
 constexpr int RESCALE_PERIOD = 8;
 constexpr int NT = 256;  // threads per CTA of both kernels
 constexpr int NW = NT / 32;
+#ifndef TR_MU_WARP
+#define TR_MU_WARP 1  // one warp forms the multipliers mu_i = f_i c_i for all basis rows (leaf_fused3_kernel)
+#endif
 #ifndef TR_SPIN_NS
 #define TR_SPIN_NS 0  // pure acquire polling measured ~1% better than back-off (16-256 ns)
 #endif
@@ -136,6 +141,19 @@ TR_D double rcp_nr(double x) {
   r = fma(r, e, r);
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
+}
+// mu_i = f_i c_i with a fixed rounding sequence: the multipliers are formed in three places
+// (the mu warp of the fused kernel, its basis rows when no mu warp runs, the chain kernel of
+// the split path) and must not depend on how the compiler contracts each of them
+TR_D cplx cmul_mu(cplx a, cplx b) {
+  return cmk(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)), __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
+}
+// (P = 7 keeps the plain product in both of its kernels: its leaves run no mu warp, and the
+// pinned sequence costs the decider-bound general variant 2% -- config 3: 6.75 -> 6.6 solves/s)
+template <int P>
+TR_D cplx mu_prod(cplx a, cplx b) {
+  if constexpr (P == 5) return cmul_mu(a, b);
+  else return cmul(a, b);
 }
 // a b - c d, the two products in parallel
 TR_D cplx cmsub(cplx a, cplx b, cplx c, cplx d) {
@@ -522,7 +540,7 @@ __global__ void __launch_bounds__(SPREAD ? 352 : 288, SPREAD ? 1 : 2) leaf_chain
   for (int e = tid; e < K * P; e += blockDim.x) {
     const int t = e / P, i = e - t * P;
     const int j = lj[t];
-    mulog[e] = (j < 0 || i == j) ? cmk(0.0, 0.0) : cmul(lf[e], lci[t]);
+    mulog[e] = (j < 0 || i == j) ? cmk(0.0, 0.0) : mu_prod<P>(lf[e], lci[t]);
   }
 }
 
@@ -902,7 +920,8 @@ __global__ void __launch_bounds__(NT, (DB <= 3 ? 2 : 1)) leaf_basis_kernel(LeafA
 // (slots H..H+P-1).
 template <int P, int DB, int NB>
 TR_D int poll_steps(cplx (&c)[DB][P], int (&deg)[P], RowState& st, int t, int& avail, int K, const int* lj,
-                    const cplx* lf, const cplx* lci, const cplx* lsig, const int* flag, int lane) {
+                    const cplx* lf, const cplx* lci, const cplx* lsig, const int* flag, const cplx* lmu,
+                    int lane) {
   for (; t < K; ++t) {
     avail = wait_steps(flag, t, avail);
     const int j = lj[t];
@@ -914,10 +933,15 @@ TR_D int poll_steps(cplx (&c)[DB][P], int (&deg)[P], RowState& st, int t, int& a
 #pragma unroll
         for (int i = 0; i < P; ++i) deg[i] = (i == j) ? dj + 1 : max(deg[i], dj);
         st.dmax = nd;
-        const cplx ci = lci[t];
         cplx mu[P];
+        if (lmu) {  // published by the mu warp (the same products)
 #pragma unroll
-        for (int i = 0; i < P; ++i) mu[i] = cmul(lf[t * P + i], ci);
+          for (int i = 0; i < P; ++i) mu[i] = lmu[t * P + i];
+        } else {
+          const cplx ci = lci[t];
+#pragma unroll
+          for (int i = 0; i < P; ++i) mu[i] = mu_prod<P>(lf[t * P + i], ci);
+        }
         basis_step_j<P, DB, NB>(c, j, mu, cneg(lsig[t]), lane);
       }
     }
@@ -941,8 +965,9 @@ struct Fused3Smem {
     const size_t capr = 32 * (size_t)DB;
     return sizeof(cplx) * ((size_t)K * P /*wl*/ + (size_t)K * P /*lf*/ + 2 * (size_t)K /*lci, lsig*/ +
                            32 * (size_t)P /*xfer*/ + M /*wtab*/ + 2 * capr /*twl x2*/ +
-                           2 * (size_t)P * P * M /*gbuf, vbuf*/ + (size_t)P * P * capr /*cbuf*/) +
-           sizeof(int2) * 2 * (size_t)K /*dtry, dbest*/ + sizeof(int) * ((size_t)K + 2);
+                           2 * (size_t)P * P * M /*gbuf, vbuf*/ + (size_t)P * P * capr /*cbuf*/ +
+                           (size_t)K * P /*lmu*/) +
+           sizeof(int2) * 2 * (size_t)K /*dtry, dbest*/ + sizeof(int) * ((size_t)K + 4);
   }
 };
 
@@ -989,10 +1014,11 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
   cplx* gbuf = twl + 2 * CAPR;                     // [P*P][M]
   cplx* vbuf = gbuf + (size_t)PP * M;              // [P*P][M]
   cplx* cbuf = vbuf + (size_t)PP * M;              // [P*P][CAPR] normalised basis
-  int2* dtry = reinterpret_cast<int2*>(cbuf + (size_t)PP * CAPR);  // [K]
+  cplx* lmu = cbuf + (size_t)PP * CAPR;            // [K][P] multipliers mu_i = f_i c_i (the mu warp)
+  int2* dtry = reinterpret_cast<int2*>(lmu + (size_t)K * P);  // [K]
   int2* dbest = dtry + K;                          // [K]
   int* lj = reinterpret_cast<int*>(dbest + K);     // [K]
-  int* flag = lj + K;                              // [0] published steps, [1] blocks handed over
+  int* flag = lj + K;  // [0] published steps, [1] blocks handed over, [2] steps whose multipliers are in lmu
   __shared__ double red[8][8];
   __shared__ double csafe[8];
   __shared__ double wred[16];
@@ -1013,7 +1039,7 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
 #define TR_EXTRA_HOLDER 1
 #endif
   const int nslots = a.dense ? nw - 1 : nw - 1 - (nw - 1) / 4;
-  const bool extra = TR_EXTRA_HOLDER && !a.dense && H >= 4 && H / 2 + 1 + P <= nslots;
+  const bool extra = P == 5 && TR_EXTRA_HOLDER && !a.dense && H >= 4 && H / 2 + 1 + P <= nslots;
   const int NH = H / 2 + (extra ? 1 : 0);
   // warp roles: the decider alone on its scheduler (warps 4, 8, 12 idle), or -- a.dense,
   // when that would need a 13th warp and with it the 128-register budget of four warps
@@ -1022,6 +1048,14 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
   const int slot = a.dense ? warp : ((warp & 3) ? warp - warp / 4 : 0);
   const int hold = (slot >= 1 && slot <= NH) ? slot : 0;
   const int brow = (slot > NH && slot <= NH + P) ? slot - NH - 1 : -1;
+  // The multipliers mu_i = f_i c_i of a step are the same for every basis row: one warp beside
+  // the decider (warp 4, otherwise idle; a few instructions per step, lanes one
+  // product each) computes them once and publishes them for the P basis-row warps, which
+  // otherwise spend a third to a half of their FP64 work recomputing them -- the consumer
+  // schedulers, not the decider, set the pace of the hand-overs (profiles/r2_leaf_decider.txt)
+  // (not in the dense layout of the P = 7 leaves: their chain is bound by the decider, measured)
+  const bool mu_on = P == 5 && TR_MU_WARP && !a.dense && nw > 4;
+  const bool muw = mu_on && warp == 4;
   // blocks held (hb2 < H: two)
   const int hb1 = extra ? (hold <= 2 ? hold : 2 * hold - 3) : 2 * hold - 1;
   const int hb2 = extra ? (hold <= 2 ? H : 2 * hold - 2) : 2 * hold;
@@ -1075,7 +1109,7 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
       load_row(32 * hb1 + lane, r, sg);
       if (hb2 < H) load_row(32 * hb2 + lane, r2, sg2);
     }
-    if (tid < 2) flag[tid] = 0;
+    if (tid < 3) flag[tid] = 0;
     if (tid == 0) bk.viol_try = 0;
     cplx c[DB][P];  // basis row (basis warps only; set in their branch)
     RowState st;
@@ -1090,14 +1124,17 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
 #pragma unroll
       for (int i = 0; i < P; ++i) cd[i] = cd0[i];
       int nabs = 0, ndef = 0;  // absorbed / deferred conditions (the chain epilogue, kept on the fly)
-      const unsigned a_lf = smem_u32(lf), a_lci = smem_u32(lci), a_lj = smem_u32(lj), a_flag = smem_u32(flag);
+      unsigned a_lf = 0, a_lci = 0, a_lj = 0, a_flag = 0;
+      if constexpr (P != 7) a_lf = smem_u32(lf), a_lci = smem_u32(lci), a_lj = smem_u32(lj), a_flag = smem_u32(flag);
       const int pub = lane == 0;
       for (int b = 0; b < H; ++b) {
         if (b > 0) {
-          const long long tw0 = clock64();
+          long long tw0 = 0;
+          if constexpr (P == 5) tw0 = clock64();
           while (ld_acquire(&flag[1]) < b) {
           }
-          if (lane == 0 && b < 8) tsm[24 + b] = clock64() - tw0;  // hand-over wait of block b
+          if constexpr (P == 5)
+            if (lane == 0 && b < 8) tsm[24 + b] = clock64() - tw0;  // hand-over wait of block b
 #pragma unroll
           for (int i = 0; i < P; ++i) r[i] = xfer[lane * P + i];
           sg = lsig[min(32 * b + lane, K - 1)];
@@ -1115,7 +1152,17 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
           const int j = decide_bits<P>(f, cd, thr2, fj, a2j);
           const double inv2 = rcp_nr(a2j);
           const cplx ci = cmk(-fj.x * inv2, fj.y * inv2);
-          {
+          if constexpr (P == 7) {
+            // (the general variant's decider is register-bound: four hoisted addresses cost it
+            // spills, config 3 leaf time 399 -> 407 ms; it keeps the lane-0 block)
+            if (lane == 0) {
+              lj[t] = j;
+              lci[t] = ci;
+#pragma unroll
+              for (int i = 0; i < P; ++i) lf[t * P + i] = f[i];
+              st_release(&flag[0], t + 1);
+            }
+          } else {
             const unsigned plf = a_lf + (unsigned)t * (P * 16u);
             sts_i_if(pub, a_lj + 4u * (unsigned)t, j);
             sts_c_if(pub, a_lci + 16u * (unsigned)t, ci);
@@ -1214,8 +1261,20 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
         }
         hand_over(hb2, r2);
       }
+    } else if (muw) {
+      // ---------------- multipliers of the published steps ----------------
+      int done = 0, avail = 0;
+      while (done < K) {
+        avail = wait_steps(&flag[0], done, avail);
+        for (int e = done * P + lane; e < avail * P; e += 32) lmu[e] = mu_prod<P>(lf[e], lci[e / P]);
+        __syncwarp();
+        if (lane == 0) st_release(&flag[2], avail);
+        done = avail;
+      }
     } else if (brow >= 0) {
       // ---------------- basis row brow: replay published steps ----------------
+      const int* bflag = mu_on ? &flag[2] : &flag[0];
+      const cplx* bmu = mu_on ? lmu : nullptr;
       int deg[P];
 #pragma unroll
       for (int d = 0; d < DB; ++d)
@@ -1229,7 +1288,7 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
       int tb = 0, avail = 0;
       while (tb < K) {
         int need = st.dmax / 32 + 1;
-        avail = wait_steps(&flag[0], tb, avail);
+        avail = wait_steps(bflag, tb, avail);
         const int j = lj[tb];
         if (j >= 0) {
           const int dj = sel_i<P>(deg, j);
@@ -1240,7 +1299,7 @@ __global__ void __launch_bounds__(NTH, 1) leaf_fused3_kernel(LeafArgs a, SplitSt
           break;
         }
 #define TR_RUN3(NB) \
-  case NB: if constexpr (NB <= DB) tb = poll_steps<P, DB, NB>(c, deg, st, tb, avail, K, lj, lf, lci, lsig, flag, lane); break;
+  case NB: if constexpr (NB <= DB) tb = poll_steps<P, DB, NB>(c, deg, st, tb, avail, K, lj, lf, lci, lsig, bflag, bmu, lane); break;
         switch (need) {
           TR_RUN3(1) TR_RUN3(2) TR_RUN3(3) TR_RUN3(4) TR_RUN3(5) TR_RUN3(6) TR_RUN3(7)
           default: tb = K; break;

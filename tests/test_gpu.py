@@ -172,6 +172,24 @@ def test_batch_groups_invariant(gpu, count):
         assert rel(reps[i].x_hat, O.dense_solution(probs[i])) < 1e-10
 
 
+def test_split_leaf_path_bit_identical_to_fused(gpu):
+    """More than 8 x 148 systems: the groups no longer fit one CTA per SM and
+    the leaves run the split path (chain kernel + row-parallel basis kernel,
+    leaf_fast.cu).  Its multipliers mu_i = f_i c_i are formed by the same
+    pinned rounding sequence as the fused kernel's mu warp (cmul_mu), so a
+    system's solution does not depend on the batch it is solved in."""
+    tb = gpu
+    count = 1300
+    raw = wl.c5_random(n=64, count=count, seed=31)
+    probs = [wl.to_problem(raw, tb, i) for i in range(count)]
+    reps = tb.solve_tikhonov_batch(probs)
+    for i in (0, 1, 647, 1299):
+        single = tb.solve_tikhonov(probs[i])
+        assert np.array_equal(reps[i].x_hat, single.x_hat), i
+        assert np.array_equal(reps[i].final_col_degrees, single.final_col_degrees)
+        assert rel(reps[i].x_hat, O.dense_solution(probs[i])) < 1e-10
+
+
 def test_shared_operator_groups(gpu):
     """Config-2 shape (one T, many right-hand sides) across stream groups."""
     tb = gpu

@@ -25,7 +25,7 @@ for _ in range(3):
     db.run()
 torch.cuda.synchronize()
 print(cfg, count, "s/run %.4f" % ((time.time() - t0) / 3))
-reps = db.reports(db.fetch(), 1.0)
+reps = db.reports(db.fetch())
 np.savez(out, x=np.stack([r.x_hat for r in reps]),
          deg=np.stack([np.asarray(r.final_col_degrees) for r in reps]),
          res=np.array([r.relative_residual for r in reps]),
